@@ -1,0 +1,86 @@
+"""ctypes binding of the in-tree C-ABI library ``libspecexec_b200.so``.
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is present, every device call raises. The declarations mirror
+``include/specexec_b200.h``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libspecexec_b200.so"
+
+_c_int = ctypes.c_int
+_c_ll = ctypes.c_longlong
+_vp = ctypes.c_void_p
+_ip = ctypes.POINTER(ctypes.c_int)
+_llp = ctypes.POINTER(ctypes.c_longlong)
+
+# name -> (restype, argtypes); must list every symbol the header declares.
+SIGNATURES: dict[str, tuple] = {
+    "sx_abi_version": (_c_int, []),
+    "sx_last_error": (ctypes.c_char_p, []),
+    "sx_gemm_plan": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _ip, _ip, _llp]),
+    "sx_gemm_bf16": (
+        _c_int,
+        [_vp, _vp, _vp, _vp, _vp, _c_ll, _c_int, _c_int, _c_int, _c_ll, _c_int, _c_int, _vp],
+    ),
+}
+
+EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16 = 0, 1, 2, 3
+
+_lib = None
+
+
+class SxError(RuntimeError):
+    """A CUDA error reported by the native library."""
+
+
+def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
+    """Load (once) and return the native library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = pathlib.Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"native library {p} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = (load().sx_last_error() or b"").decode(errors="replace")
+    if status < 0:
+        raise ValueError(f"{what}: {msg}")
+    raise SxError(f"{what}: CUDA error {status}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a tensor (None stays None)."""
+    if t is None:
+        return None
+    return int(t.data_ptr())

@@ -1,0 +1,88 @@
+#include "capi_util.h"
+
+#include <cudaTypedefs.h>
+#include <stdarg.h>
+
+#include <mutex>
+#include <tuple>
+#include <map>
+
+namespace sx {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+const char* get_last_error() { return g_last_error.c_str(); }
+
+int arg_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  set_last_error(buf);
+  return SX_EARG;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return SX_OK;
+  set_last_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return static_cast<int>(e);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tmap_bf16_kmajor(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                          int box_rows) {
+  using Key = std::tuple<uintptr_t, int64_t, int64_t, int64_t, int>;
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  Key key{reinterpret_cast<uintptr_t>(ptr), rows, cols, ld, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return SX_OK;
+    }
+  }
+  auto fn = get_encode_fn();
+  if (!fn) {
+    set_last_error("cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
+    return static_cast<int>(cudaErrorNotSupported);
+  }
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
+    return arg_error("tensor map: base and row pitch must be 16-byte aligned");
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld box=%d", (int)r,
+             (long long)rows, (long long)cols, box_rows);
+    set_last_error(buf);
+    return static_cast<int>(cudaErrorInvalidValue);
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 65536) cache.clear();
+  cache[key] = *out;
+  return SX_OK;
+}
+
+}  // namespace sx

@@ -1,0 +1,79 @@
+"""KG tcgen05 GEMM vs a plain PyTorch fp32 reference of the same op."""
+
+import pytest
+import torch
+
+from paper_2406_02532_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(x, w):
+    return x.float() @ w.float().t()
+
+
+@pytest.mark.parametrize(
+    "M,N,Kd",
+    [(1, 128, 64), (17, 256, 128), (64, 4096, 4096), (100, 384, 512), (1025, 1024, 1024), (300, 1000, 192)],
+)
+def test_gemm_bf16_and_f32(cuda, M, N, Kd):
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+    w = (torch.randn(N, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+    ref = _ref(x, w)
+    y32 = K.gemm(x, w, epi=K.EPI_F32)
+    torch.cuda.synchronize()
+    tol = 1e-3 * (Kd ** 0.5)
+    assert (y32 - ref).abs().max().item() < tol
+    y16 = K.gemm(x, w, epi=K.EPI_BF16)
+    assert (y16.float() - ref).abs().max().item() < tol + ref.abs().max().item() * 1e-2
+
+
+@pytest.mark.parametrize("splits", [1, 2, 4])
+def test_gemm_residual_add_and_splitk(cuda, splits):
+    M, N, Kd = 48, 512, 2048
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+    w = (torch.randn(N, Kd, generator=g, device=cuda) * 0.03).bfloat16()
+    resid = torch.randn(M, N, generator=g, device=cuda)
+    expect = resid + _ref(x, w)
+    K.gemm(x, w, out=resid, epi=K.EPI_ADD_F32, splits=splits)
+    torch.cuda.synchronize()
+    assert (resid - expect).abs().max().item() < 5e-3
+
+
+@pytest.mark.parametrize("M,splits", [(64, 0), (257, 1), (16, 4)])
+def test_gemm_swiglu_dual(cuda, M, splits):
+    N, Kd = 640, 1024
+    g = torch.Generator(device=cuda).manual_seed(M)
+    x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+    wg = (torch.randn(N, Kd, generator=g, device=cuda) * 0.03).bfloat16()
+    wu = (torch.randn(N, Kd, generator=g, device=cuda) * 0.03).bfloat16()
+    y = K.gemm(x, wg, epi=K.EPI_SWIGLU_BF16, w2=wu, splits=splits)
+    gate = _ref(x, wg)
+    up = _ref(x, wu)
+    ref = torch.nn.functional.silu(gate) * up
+    torch.cuda.synchronize()
+    assert (y.float() - ref).abs().max().item() < 2e-2 * max(1.0, ref.abs().max().item())
+
+
+def test_gemm_large_perf_smoke(cuda):
+    # 70B-shaped projection over a K=1024 tree (N = K+1 = 1025 tokens).
+    M, N, Kd = 1025, 8192, 8192
+    x = torch.randn(M, Kd, device=cuda).bfloat16()
+    w = (torch.randn(N, Kd, device=cuda) * 0.02).bfloat16()
+    y = K.gemm(x, w, epi=K.EPI_BF16)
+    torch.cuda.synchronize()
+    ref = _ref(x, w)
+    assert (y.float() - ref).abs().max().item() < 0.05
+    for _ in range(3):
+        K.gemm(x, w, out=y, epi=K.EPI_BF16)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        K.gemm(x, w, out=y, epi=K.EPI_BF16)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / 10
+    tflops = 2 * M * N * Kd / ms / 1e9
+    print(f"\n[gemm] 1025x8192x8192: {ms:.3f} ms  {tflops:.0f} TFLOP/s")
