@@ -65,6 +65,68 @@ SX_API int sx_gemm_plan(int M, int N, int K, int dual, int splits_req, int* bn_o
 SX_API int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* out, float* ws, long long ws_floats,
                  int M, int N, int K, long long ldo, int epi, int splits_req, cudaStream_t stream);
 
+/* ------------------------------------- KT1-KT3: draft-tree build (stage 1)
+ * build_sssp, pkg/src/speckit/tree.py:240-327, as a device-resident state
+ * machine in one caller-allocated workspace of sx_tree_workspace_bytes(K,B,V,D)
+ * bytes (K = budget, B = batch_size, V = vocab, D = max_depth; BuilderParams
+ * tree.py:36-55). Per draft call the caller evaluates the draft on the current
+ * batch (its tokens / ancestor KV slots are in the workspace, see
+ * sx_tree_offsets) and hands the rows to sx_tree_round, which scores them
+ * (tree.py:299-306; warp per _scored_dist tree.py:222-227), keeps the K best by
+ * (nll, depth, path-lex) (tree.py:308-318) and selects the next batch
+ * (tree.py:282-295). `host_ctl` (pinned, >= 64 bytes) receives the control
+ * block (batch size == 0 ends the build). sx_tree_finalize lays the result out
+ * in node-id order (ids in key order, tree.py:320-327).
+ */
+enum { SX_ROWS_LOGITS_F32 = 0, SX_ROWS_PROBS_F64 = 1 };
+enum { SX_SCORE_RAW = 0, SX_SCORE_ARGMAX = 1, SX_SCORE_WARP = 2 };
+SX_API long long sx_tree_workspace_bytes(int K, int B, int V, int D);
+SX_API int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n);
+SX_API int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, cudaStream_t stream);
+SX_API int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
+                         int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream);
+SX_API int sx_tree_finalize(void* ws, int K, int B, int V, int D, int* out_parent, int* out_token, double* out_edge,
+                            int* out_depth, cudaStream_t stream);
+
+/* ------------------------------------------------ exact table models on GPU
+ * MarkovModel / TabularModel (pkg/src/speckit/models.py:77-151) rows for tree
+ * nodes: table fp64 [V**order, V]; ctx0 = anchor's last `order` tokens
+ * left-padded with 0 (device int[order]); node_ids = positions in the tree
+ * workspace's current node list or -1 for the anchor (or from_batch=1: the
+ * current batch). out fp64 [n, ld].
+ */
+SX_API int sx_markov_rows(const double* table, int V, int order, const int* ctx0, void* ws, int K, int B, int D,
+                          const int* node_ids, int n_nodes, int from_batch, double* out, long long ld,
+                          cudaStream_t stream);
+
+/* ---------------------------------------- KV1/KV2: verification (stage 4)
+ * The acceptance walk of generate_specexec (pkg/src/speckit/engine.py:118-128):
+ * rows = target rows of the flattened tree (row 0 = anchor, row i+1 = node i;
+ * fp32 logits or fp64 probabilities); parent/token = the tree in node-id
+ * order. Per step: token = sample(apply_warp(row[cursor]), uniforms[step])
+ * (sampling.py:66-113; t = 0 -> argmax, lowest id); move to the child with that
+ * token (tree.py:132-136); stop on a miss or after max_steps.
+ * out (device int[3 + 2*max_steps]): [emitted, fell_off, cursor, tokens..., path rows...].
+ * scratch: sx_row_scratch_bytes(V) bytes.
+ */
+SX_API long long sx_row_scratch_bytes(int V);
+SX_API int sx_verify_walk(const void* rows, int row_kind, long long ld, int V, const int* parent, const int* token,
+                          int n_nodes, int start_cursor, const double* uniforms, int max_steps, double temperature,
+                          double top_p, int* out, void* scratch, cudaStream_t stream);
+/* apply_warp (sampling.py:66-98) of n rows (row_ids may be NULL) into fp64 out [n, ldo];
+ * scratch: sx_warp_scratch_bytes(n, V). */
+SX_API long long sx_warp_scratch_bytes(int n, int V);
+SX_API int sx_warp_rows(const void* rows, int row_kind, long long ld, int V, const int* row_ids, int n,
+                        double temperature, double top_p, double* out, long long ldo, void* scratch,
+                        cudaStream_t stream);
+/* canonical float64 probabilities of fp32 logits rows (ProbCache row materialisation) */
+SX_API int sx_softmax_rows(const float* rows, long long ld, int V, const int* row_ids, int n, double* out,
+                           long long ldo, cudaStream_t stream);
+SX_API int sx_argmax_rows(const void* rows, int row_kind, long long ld, int V, int n, int* out, cudaStream_t stream);
+/* sample (sampling.py:101-113) from n warped fp64 rows with uniforms u[n] */
+SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u, int n, int* out,
+                          cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,4 +1,44 @@
-"""B200-native SpecExec (arXiv 2406.02532): the reference `speckit` generator /
-engine API over hand-written sm_100a CUDA kernels behind a C ABI."""
+"""B200-native SpecExec (arXiv 2406.02532).
+
+Drop-in for the hot path of the reference `speckit` package: the same
+generator / engine API (`BuilderParams`, `SamplingConfig`, `CounterRng`,
+`DraftTree`, `flatten`, `build_sssp`, `precompute`, `generate_specexec`,
+`generate_sequential`, `GenStats`, `ProbCache`, `LanguageModel`, ...) over
+hand-written sm_100a CUDA kernels behind the C ABI in include/specexec_b200.h.
+There is no CPU fallback: without the built library or a CUDA device every
+device call raises.
+"""
+
+from .engine import GenStats, ProbCache, generate_sequential, generate_specexec, precompute, stats_record
+from .models import LanguageModel, MarkovModel, TabularModel, make_synthetic, model_from_json
+from .rng import CounterRng
+from .sampling import SamplingConfig, apply_warp, sample, validate_distribution
+from .tree import ROOT, BuilderParams, DraftNode, DraftTree, FlattenedTree, build_sssp, flatten
 
 __version__ = "0.1.0"
+
+__all__ = [
+    "ROOT",
+    "BuilderParams",
+    "CounterRng",
+    "DraftNode",
+    "DraftTree",
+    "FlattenedTree",
+    "GenStats",
+    "LanguageModel",
+    "MarkovModel",
+    "ProbCache",
+    "SamplingConfig",
+    "TabularModel",
+    "apply_warp",
+    "build_sssp",
+    "flatten",
+    "generate_sequential",
+    "generate_specexec",
+    "make_synthetic",
+    "model_from_json",
+    "precompute",
+    "sample",
+    "stats_record",
+    "validate_distribution",
+]

@@ -16,6 +16,7 @@ LIB_PATH = _HERE / "libspecexec_b200.so"
 
 _c_int = ctypes.c_int
 _c_ll = ctypes.c_longlong
+_c_dbl = ctypes.c_double
 _vp = ctypes.c_void_p
 _ip = ctypes.POINTER(ctypes.c_int)
 _llp = ctypes.POINTER(ctypes.c_longlong)
@@ -29,7 +30,35 @@ SIGNATURES: dict[str, tuple] = {
         _c_int,
         [_vp, _vp, _vp, _vp, _vp, _c_ll, _c_int, _c_int, _c_int, _c_ll, _c_int, _c_int, _vp],
     ),
+    "sx_tree_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_int, _c_int]),
+    "sx_tree_offsets": (_c_int, [_c_int, _c_int, _c_int, _c_int, _llp, _c_int]),
+    "sx_tree_begin": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "sx_tree_round": (
+        _c_int,
+        [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl, _vp, _vp],
+    ),
+    "sx_tree_finalize": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "sx_markov_rows": (
+        _c_int,
+        [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_ll, _vp],
+    ),
+    "sx_row_scratch_bytes": (_c_ll, [_c_int]),
+    "sx_verify_walk": (
+        _c_int,
+        [_vp, _c_int, _c_ll, _c_int, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_dbl, _c_dbl, _vp, _vp, _vp],
+    ),
+    "sx_warp_scratch_bytes": (_c_ll, [_c_int, _c_int]),
+    "sx_warp_rows": (
+        _c_int,
+        [_vp, _c_int, _c_ll, _c_int, _vp, _c_int, _c_dbl, _c_dbl, _vp, _c_ll, _vp, _vp],
+    ),
+    "sx_softmax_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _c_ll, _vp]),
+    "sx_argmax_rows": (_c_int, [_vp, _c_int, _c_ll, _c_int, _c_int, _vp, _vp]),
+    "sx_sample_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _vp]),
 }
+
+ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1
+SCORE_RAW, SCORE_ARGMAX, SCORE_WARP = 0, 1, 2
 
 EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16 = 0, 1, 2, 3
 

@@ -1,0 +1,711 @@
+// KT1-KT3: stage-1 draft-tree construction on the GPU (build_sssp,
+// pkg/src/speckit/tree.py:240-327).
+//
+// State kept in one device workspace (tree_layout.h):
+//   materialized  : the <= K best candidates so far, SORTED by the reference key
+//                   (nll asc, depth asc, path-lex asc) (tree.py:235-237, :270-278),
+//                   double-buffered; each node carries its parent index, token,
+//                   edge log-prob, draft-KV slot (if expanded) and its rank in
+//                   path-lex order among same-depth nodes (`lex`).
+//   batch         : the <= B nodes expanded by the next draft call (tree.py:282-295)
+//   survivors     : this round's children whose key beats the threshold
+//
+// Key encoding: hi = bit pattern of nll (>= 0, so unsigned order == numeric
+// order); lo = depth << 56 | lex(parent) << 32 | token. For two same-depth
+// paths, lexicographic order == (lex rank of parent, token), so (hi, lo) is the
+// reference's total order.
+//
+// Per round (one draft call):
+//   sx_tree_score  : canonical float64 probabilities of every batch row (from
+//                    fp32 logits, fp64 probabilities, or a warped row), edge =
+//                    sx_log(p), nll = parent_nll - edge, keep key < threshold.
+//   sx_tree_update : ONE CTA. Radix-select (8-bit digits over the 128-bit key)
+//                    of the K best of materialized U survivors, bitonic sort in
+//                    shared memory, parent remap, lex-rank recompute (sort by lo),
+//                    new threshold = K-th key, next batch = first B unexpanded
+//                    nodes with depth < D and key < threshold, their draft-KV
+//                    slots and ancestor-slot lists.
+#include "capi_util.h"
+#include "common.cuh"
+#include "specexec_b200.h"
+#include "sxmath.cuh"
+#include "tree_layout.h"
+#include "warp_rows.cuh"
+
+namespace sx {
+
+template <typename T>
+SX_DEV T* at(uint8_t* ws, long long off) {
+  return reinterpret_cast<T*>(ws + off);
+}
+
+SX_DEV unsigned long long make_lo(int depth, int plex, int token) {
+  return ((unsigned long long)depth << 56) | ((unsigned long long)(unsigned)plex << 32) | (unsigned)token;
+}
+SX_DEV int lo_depth(unsigned long long lo) { return (int)(lo >> 56); }
+SX_DEV int lo_token(unsigned long long lo) { return (int)(lo & 0xffffffffu); }
+
+SX_DEV bool key_less(unsigned long long ah, unsigned long long al, unsigned long long bh, unsigned long long bl) {
+  return ah < bh || (ah == bh && al < bl);
+}
+
+// --------------------------------------------------------------------------
+__global__ void tree_begin_kernel(uint8_t* ws, TreeLayout L, int root_slot) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  c->cur = 0;
+  c->count = 0;
+  c->has_thr = 0;
+  c->rounds = 0;
+  c->slot_next = root_slot + 1;
+  c->batch_n = 1;
+  c->n_surv = 0;
+  c->root_slot = root_slot;
+  c->err = 0;
+  c->thr_nll = 0.0;
+  c->thr_lo = 0ull;
+  at<int>(ws, L.b_node)[0] = -1;
+  at<double>(ws, L.b_nll)[0] = 0.0;
+  at<int>(ws, L.b_depth)[0] = 0;
+  at<int>(ws, L.b_lex)[0] = 0;
+  at<int>(ws, L.b_slot)[0] = root_slot;
+  at<int>(ws, L.b_token)[0] = -1;
+  at<int>(ws, L.b_anc)[0] = root_slot;
+  at<int>(ws, L.b_anc_len)[0] = 1;
+}
+
+// --------------------------------------------------------------------------
+// Canonical warp of each batch row (t > 0 scoring): w_rows[b] = apply_warp(row b).
+__global__ void __launch_bounds__(kRowThreads) tree_warp_rows_kernel(uint8_t* ws, TreeLayout L, const void* rows,
+                                                                       int row_kind, long long ld, double temperature,
+                                                                       double top_p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int b = blockIdx.x;
+  if (b >= c->batch_n) return;
+  const int V = L.V;
+  const float* z = row_kind == SX_ROWS_LOGITS_F32 ? reinterpret_cast<const float*>(rows) + b * ld : nullptr;
+  const double* p = row_kind == SX_ROWS_PROBS_F64 ? reinterpret_cast<const double*>(rows) + b * ld : nullptr;
+  double* out = at<double>(ws, L.w_rows) + (long long)b * V;
+  unsigned long long* k1 = at<unsigned long long>(ws, L.w_keys) + (long long)b * V;
+  unsigned long long* k2 = at<unsigned long long>(ws, L.w_keys2) + (long long)b * V;
+  int* i1 = at<int>(ws, L.w_idx) + (long long)b * V;
+  int* i2 = at<int>(ws, L.w_idx2) + (long long)b * V;
+  warp_row(sm, z, p, V, temperature, top_p, out, k1, i1, k2, i2);
+}
+
+// --------------------------------------------------------------------------
+// Row statistics for logits rows: max and canonical sum of exp(z - max).
+__global__ void __launch_bounds__(kRowThreads) tree_row_stats_kernel(uint8_t* ws, TreeLayout L, const float* rows,
+                                                                       long long ld) {
+  __shared__ RowSmemLite sm;
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int b = blockIdx.x;
+  if (b >= c->batch_n) return;
+  const float* z = rows + b * ld;
+  float m;
+  double S;
+  row_stats_lite(sm, z, L.V, m, S);
+  if (threadIdx.x == 0) {
+    at<float>(ws, L.r_max)[b] = m;
+    at<double>(ws, L.r_sum)[b] = S;
+  }
+}
+
+// Argmax rows (t = 0 warped scoring): one child per row with p = 1, edge = log(1) = 0.
+__global__ void __launch_bounds__(kRowThreads) tree_argmax_score_kernel(uint8_t* ws, TreeLayout L, const void* rows,
+                                                                          int row_kind, long long ld) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int b = blockIdx.x;
+  if (b >= c->batch_n) return;
+  double bv = -CUDART_INF;
+  int bi = 0x7fffffff;
+  for (int v = threadIdx.x; v < L.V; v += kRowThreads) {
+    const double x = row_kind == SX_ROWS_LOGITS_F32 ? (double)reinterpret_cast<const float*>(rows)[b * ld + v]
+                                                    : reinterpret_cast<const double*>(rows)[b * ld + v];
+    if (x > bv) {
+      bv = x;
+      bi = v;
+    }
+  }
+  const int best = block_argmax(sm, bv, bi);
+  if (threadIdx.x == 0) {
+    const double parent_nll = at<double>(ws, L.b_nll)[b];
+    const double nll = dsub(parent_nll, 0.0);
+    const unsigned long long hi = (unsigned long long)__double_as_longlong(nll);
+    const unsigned long long lo = make_lo(at<int>(ws, L.b_depth)[b] + 1, at<int>(ws, L.b_lex)[b], best);
+    if (!c->has_thr || key_less(hi, lo, (unsigned long long)__double_as_longlong(c->thr_nll), c->thr_lo)) {
+      const int k = atomicAdd(&c->n_surv, 1);
+      at<double>(ws, L.s_nll)[k] = nll;
+      at<unsigned long long>(ws, L.s_lo)[k] = lo;
+      at<double>(ws, L.s_edge)[k] = 0.0;
+      at<int>(ws, L.s_row)[k] = b;
+    }
+  }
+}
+
+// Score every (row, token): grid (chunks, B). mode: probabilities (fp64 rows or the
+// warped rows) or logits (fp32 + row stats).
+__global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout L, const void* rows, int row_kind,
+                                                           long long ld) {
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int b = blockIdx.y;
+  if (b >= c->batch_n) return;
+  const int V = L.V;
+  const double parent_nll = at<double>(ws, L.b_nll)[b];
+  const int depth = at<int>(ws, L.b_depth)[b] + 1;
+  const int plex = at<int>(ws, L.b_lex)[b];
+  const bool has_thr = c->has_thr;
+  const unsigned long long th = (unsigned long long)__double_as_longlong(c->thr_nll);
+  const unsigned long long tl = c->thr_lo;
+  float m = 0.f;
+  double S = 1.0;
+  const float* z = nullptr;
+  const double* p = nullptr;
+  if (row_kind == SX_ROWS_LOGITS_F32) {
+    z = reinterpret_cast<const float*>(rows) + b * ld;
+    m = at<float>(ws, L.r_max)[b];
+    S = at<double>(ws, L.r_sum)[b];
+  } else if (row_kind == SX_ROWS_PROBS_F64) {
+    p = reinterpret_cast<const double*>(rows) + b * ld;
+  } else {
+    p = at<double>(ws, L.w_rows) + (long long)b * V;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int v0 = blockIdx.x * blockDim.x; v0 < V; v0 += gridDim.x * blockDim.x) {
+    const int v = v0 + threadIdx.x;
+    bool keep = false;
+    double nll = 0.0, edge = 0.0;
+    unsigned long long lo = 0;
+    if (v < V) {
+      const double pv = z ? ddiv(sx_exp(dsub((double)z[v], (double)m)), S) : p[v];
+      if (pv > 0.0) {
+        edge = sx_log(pv);
+        nll = dsub(parent_nll, edge);
+        lo = make_lo(depth, plex, v);
+        keep = !has_thr || key_less((unsigned long long)__double_as_longlong(nll), lo, th, tl);
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffff, keep);
+    if (mask) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&c->n_surv, __popc(mask));
+      base = __shfl_sync(0xffffffff, base, 0);
+      if (keep) {
+        const long long k = base + __popc(mask & ((1u << lane) - 1));
+        if (k < L.cap) {
+          at<double>(ws, L.s_nll)[k] = nll;
+          at<unsigned long long>(ws, L.s_lo)[k] = lo;
+          at<double>(ws, L.s_edge)[k] = edge;
+          at<int>(ws, L.s_row)[k] = b;
+        } else {
+          c->err = 1;
+        }
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// The single-CTA update: select, sort, relabel, threshold, next batch.
+constexpr int kUpdThreads = 1024;
+
+struct UpdSmem {
+  int hist[256];
+  int bin;
+  int rank;
+  int done;
+  int sel_n;
+  int elig_total;
+  int scan[kUpdThreads];
+  int depth_start[256];
+};
+
+SX_DEV void get_key(uint8_t* ws, const TreeLayout& L, int cur, int n_old, int i, unsigned long long& h,
+                    unsigned long long& l) {
+  if (i < n_old) {
+    h = (unsigned long long)__double_as_longlong(at<double>(ws, L.m_nll[cur])[i]);
+    l = at<unsigned long long>(ws, L.m_lo[cur])[i];
+  } else {
+    h = (unsigned long long)__double_as_longlong(at<double>(ws, L.s_nll)[i - n_old]);
+    l = at<unsigned long long>(ws, L.s_lo)[i - n_old];
+  }
+}
+
+SX_DEV int digit_of(unsigned long long h, unsigned long long l, int d) {
+  return d < 8 ? (int)((h >> (56 - 8 * d)) & 255) : (int)((l >> (56 - 8 * (d - 8))) & 255);
+}
+// compare top (d+1) digits of key against prefix digits: -1, 0, +1
+SX_DEV int cmp_prefix(unsigned long long h, unsigned long long l, unsigned long long ph, unsigned long long pl,
+                      int ndig) {
+  if (ndig <= 8) {
+    const int sh = 64 - 8 * ndig;
+    const unsigned long long a = sh >= 64 ? 0 : (h >> sh), b = sh >= 64 ? 0 : (ph >> sh);
+    return a < b ? -1 : (a > b ? 1 : 0);
+  }
+  if (h != ph) return h < ph ? -1 : 1;
+  const int sh = 64 - 8 * (ndig - 8);
+  const unsigned long long a = sh >= 64 ? 0 : (l >> sh), b = sh >= 64 ? 0 : (pl >> sh);
+  return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+SX_DEV void bitonic_sort_128(unsigned long long* kh, unsigned long long* kl, int* kv, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool asc = (i & k) == 0;
+          const bool gt = key_less(kh[ixj], kl[ixj], kh[i], kl[i]);
+          if (gt == asc) {
+            unsigned long long th = kh[i], tl = kl[i];
+            int tv = kv[i];
+            kh[i] = kh[ixj];
+            kl[i] = kl[ixj];
+            kv[i] = kv[ixj];
+            kh[ixj] = th;
+            kl[ixj] = tl;
+            kv[ixj] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+SX_DEV void bitonic_sort_64(unsigned long long* kk, int* kv, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool asc = (i & k) == 0;
+          if ((kk[i] > kk[ixj]) == asc) {
+            unsigned long long t = kk[i];
+            int tv = kv[i];
+            kk[i] = kk[ixj];
+            kv[i] = kv[ixj];
+            kk[ixj] = t;
+            kv[ixj] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// block-wide exclusive scan of one int per thread; returns the total
+SX_DEV int block_excl_scan(UpdSmem& sm, int v, int& excl) {
+  const int t = threadIdx.x;
+  sm.scan[t] = v;
+  __syncthreads();
+  for (int off = 1; off < kUpdThreads; off <<= 1) {
+    const int add = t >= off ? sm.scan[t - off] : 0;
+    __syncthreads();
+    sm.scan[t] += add;
+    __syncthreads();
+  }
+  const int incl = sm.scan[t];
+  const int total = sm.scan[kUpdThreads - 1];
+  __syncthreads();
+  excl = incl - v;
+  return total;
+}
+
+__global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws, TreeLayout L) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
+  unsigned long long* sk_h = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(UpdSmem) + 15) & ~size_t(15)));
+  unsigned long long* sk_l = sk_h + L.kpad;
+  int* sk_v = reinterpret_cast<int*>(sk_l + L.kpad);
+
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int tid = threadIdx.x;
+  const int K = L.K;
+  const int cur = c->cur, nxt = cur ^ 1;
+  const int n_old = c->count;
+  const int n_new = min((long long)c->n_surv, L.cap);
+  const int n = n_old + n_new;
+
+  // ---- 1. select the K smallest keys (radix select over 16 8-bit digits) ----
+  unsigned long long ph = 0, pl = 0;
+  int ndig = 0;  // digits fixed in the prefix
+  bool select_all = n <= K;
+  if (!select_all) {
+    if (tid == 0) {
+      sm.rank = K;
+      sm.done = 0;
+    }
+    __syncthreads();
+    for (int d = 0; d < 16; ++d) {
+      for (int i = tid; i < 256; i += kUpdThreads) sm.hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < n; i += kUpdThreads) {
+        unsigned long long h, l;
+        get_key(ws, L, cur, n_old, i, h, l);
+        if (cmp_prefix(h, l, ph, pl, d) == 0) atomicAdd(&sm.hist[digit_of(h, l, d)], 1);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int r = sm.rank, acc = 0, b = 0;
+        for (; b < 256; ++b) {
+          if (acc + sm.hist[b] >= r) break;
+          acc += sm.hist[b];
+        }
+        sm.bin = b;
+        sm.rank = r - acc;
+        sm.done = (sm.hist[b] == r - acc);
+      }
+      __syncthreads();
+      const unsigned long long bd = (unsigned long long)sm.bin;
+      if (d < 8)
+        ph |= bd << (56 - 8 * d);
+      else
+        pl |= bd << (56 - 8 * (d - 8));
+      ndig = d + 1;
+      const int done = sm.done;
+      __syncthreads();
+      if (done) break;
+    }
+  }
+
+  // ---- 2. gather the selected keys into shared memory ----
+  if (tid == 0) sm.sel_n = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kUpdThreads) {
+    unsigned long long h, l;
+    get_key(ws, L, cur, n_old, i, h, l);
+    if (select_all || cmp_prefix(h, l, ph, pl, ndig) <= 0) {
+      const int k = atomicAdd(&sm.sel_n, 1);
+      sk_h[k] = h;
+      sk_l[k] = l;
+      sk_v[k] = i;
+    }
+  }
+  __syncthreads();
+  const int sel = sm.sel_n;  // == min(n, K)
+  int np2 = 1;
+  while (np2 < sel) np2 <<= 1;
+  for (int i = sel + tid; i < np2; i += kUpdThreads) {
+    sk_h[i] = ~0ull;
+    sk_l[i] = ~0ull;
+    sk_v[i] = -1;
+  }
+  __syncthreads();
+  bitonic_sort_128(sk_h, sk_l, sk_v, np2);
+
+  // ---- 3. write the new materialized list (sorted), remap old -> new ----
+  int* remap = at<int>(ws, L.remap);
+  const int* b_node = at<int>(ws, L.b_node);
+  for (int pos = tid; pos < sel; pos += kUpdThreads) {
+    const int src = sk_v[pos];
+    if (src < n_old) remap[src] = pos;
+  }
+  __syncthreads();
+  for (int pos = tid; pos < sel; pos += kUpdThreads) {
+    const int src = sk_v[pos];
+    int parent_old, slot;
+    double edge;
+    if (src < n_old) {
+      parent_old = at<int>(ws, L.m_parent[cur])[src];
+      slot = at<int>(ws, L.m_slot[cur])[src];
+      edge = at<double>(ws, L.m_edge[cur])[src];
+    } else {
+      const int j = src - n_old;
+      parent_old = b_node[at<int>(ws, L.s_row)[j]];
+      slot = -1;
+      edge = at<double>(ws, L.s_edge)[j];
+    }
+    at<double>(ws, L.m_nll[nxt])[pos] = __longlong_as_double((long long)sk_h[pos]);
+    at<unsigned long long>(ws, L.m_lo[nxt])[pos] = sk_l[pos];
+    at<double>(ws, L.m_edge[nxt])[pos] = edge;
+    at<int>(ws, L.m_parent[nxt])[pos] = parent_old < 0 ? -1 : remap[parent_old];
+    at<int>(ws, L.m_slot[nxt])[pos] = slot;
+  }
+  __syncthreads();
+
+  // ---- 4. lex ranks within depth: sort the lo keys (depth | lex(parent) | token) ----
+  for (int pos = tid; pos < np2; pos += kUpdThreads) {
+    sk_l[pos] = pos < sel ? at<unsigned long long>(ws, L.m_lo[nxt])[pos] : ~0ull;
+    sk_v[pos] = pos;
+  }
+  for (int i = tid; i < 256; i += kUpdThreads) sm.depth_start[i] = 0x7fffffff;
+  __syncthreads();
+  bitonic_sort_64(sk_l, sk_v, np2);
+  for (int r = tid; r < sel; r += kUpdThreads) {
+    const int d = lo_depth(sk_l[r]);
+    if (r == 0 || lo_depth(sk_l[r - 1]) != d) sm.depth_start[d] = r;
+  }
+  __syncthreads();
+  int* lex = at<int>(ws, L.m_lex[nxt]);
+  for (int r = tid; r < sel; r += kUpdThreads) lex[sk_v[r]] = r - sm.depth_start[lo_depth(sk_l[r])];
+  __syncthreads();
+  const int* par = at<int>(ws, L.m_parent[nxt]);
+  unsigned long long* lo_arr = at<unsigned long long>(ws, L.m_lo[nxt]);
+  for (int pos = tid; pos < sel; pos += kUpdThreads) {
+    const unsigned long long lo = lo_arr[pos];
+    const int p = par[pos];
+    lo_arr[pos] = make_lo(lo_depth(lo), p < 0 ? 0 : lex[p], lo_token(lo));
+  }
+  __syncthreads();
+
+  // ---- 5. threshold ----
+  const bool has_thr = sel >= K;
+  const unsigned long long th = has_thr ? (unsigned long long)__double_as_longlong(at<double>(ws, L.m_nll[nxt])[K - 1]) : 0;
+  const unsigned long long tl = has_thr ? lo_arr[K - 1] : 0;
+
+  // ---- 6. next batch: first B unexpanded nodes with depth < D and key < threshold ----
+  const int per = (sel + kUpdThreads - 1) / kUpdThreads;
+  const int p0 = min(sel, tid * per), p1 = min(sel, p0 + per);
+  const double* nll_arr = at<double>(ws, L.m_nll[nxt]);
+  int* slot_arr = at<int>(ws, L.m_slot[nxt]);
+  auto eligible = [&](int pos) -> bool {
+    if (slot_arr[pos] >= 0) return false;
+    const unsigned long long lo = lo_arr[pos];
+    if (lo_depth(lo) >= L.D) return false;
+    if (!has_thr) return true;
+    return key_less((unsigned long long)__double_as_longlong(nll_arr[pos]), lo, th, tl);
+  };
+  int cnt = 0;
+  for (int pos = p0; pos < p1; ++pos) cnt += eligible(pos);
+  int excl;
+  const int total = block_excl_scan(sm, cnt, excl);
+  const int batch_n = min(total, L.B);
+  const int slot_base = c->slot_next;
+  int rank = excl;
+  for (int pos = p0; pos < p1 && rank < batch_n; ++pos) {
+    if (!eligible(pos)) continue;
+    const int b = rank++;
+    const int slot = slot_base + b;
+    slot_arr[pos] = slot;
+    const unsigned long long lo = lo_arr[pos];
+    const int depth = lo_depth(lo);
+    at<int>(ws, L.b_node)[b] = pos;
+    at<double>(ws, L.b_nll)[b] = nll_arr[pos];
+    at<int>(ws, L.b_depth)[b] = depth;
+    at<int>(ws, L.b_lex)[b] = lex[pos];
+    at<int>(ws, L.b_slot)[b] = slot;
+    at<int>(ws, L.b_token)[b] = lo_token(lo);
+  }
+  __syncthreads();
+  // ancestor-slot lists, root first: [root_slot, slot(depth 1), ..., slot(self)]
+  for (int b = tid; b < batch_n; b += kUpdThreads) {
+    const int pos = at<int>(ws, L.b_node)[b];
+    const int depth = lo_depth(lo_arr[pos]);
+    int* anc = at<int>(ws, L.b_anc) + b * (L.D + 1);
+    int q = pos;
+    for (int k = depth; k >= 1; --k) {
+      anc[k] = slot_arr[q];
+      q = par[q];
+    }
+    anc[0] = c->root_slot;
+    at<int>(ws, L.b_anc_len)[b] = depth + 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    c->cur = nxt;
+    c->count = sel;
+    c->has_thr = has_thr;
+    c->thr_nll = __longlong_as_double((long long)th);
+    c->thr_lo = tl;
+    c->batch_n = batch_n;
+    c->slot_next = slot_base + batch_n;
+    c->n_surv = 0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Final tables for the target pass over the tree: row 0 = root (anchor's last
+// token), row i+1 = node i. anc[row] = rows of the root path, root first, self last.
+__global__ void tree_final_kernel(uint8_t* ws, TreeLayout L, int* out_parent, int* out_token, double* out_edge,
+                                  int* out_depth) {
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int cur = c->cur, n = c->count;
+  const int* par = at<int>(ws, L.m_parent[cur]);
+  const unsigned long long* lo = at<unsigned long long>(ws, L.m_lo[cur]);
+  const double* edge = at<double>(ws, L.m_edge[cur]);
+  int* f_anc = at<int>(ws, L.f_anc);
+  int* f_len = at<int>(ws, L.f_anc_len);
+  int* f_depth = at<int>(ws, L.f_depth);
+  int* f_tok = at<int>(ws, L.f_token);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += gridDim.x * blockDim.x) {
+    int* anc = f_anc + (long long)r * (L.D + 1);
+    if (r == 0) {
+      anc[0] = 0;
+      f_len[0] = 1;
+      f_depth[0] = 0;
+      continue;
+    }
+    const int i = r - 1;
+    const int depth = lo_depth(lo[i]);
+    f_depth[r] = depth;
+    f_tok[r] = lo_token(lo[i]);
+    f_len[r] = depth + 1;
+    int q = i;
+    for (int k = depth; k >= 1; --k) {
+      anc[k] = q + 1;
+      q = par[q];
+    }
+    anc[0] = 0;
+    if (out_parent) out_parent[i] = par[i];
+    if (out_token) out_token[i] = lo_token(lo[i]);
+    if (out_edge) out_edge[i] = edge[i];
+    if (out_depth) out_depth[i] = depth;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Exact table models on the GPU (MarkovModel / TabularModel, models.py:77-151):
+// rows for tree nodes. node_ids[i] = position in the current materialized list,
+// or -1 for the root (the anchor itself). ctx0 = anchor's last `order` tokens,
+// left-padded with 0 (models.py:127-129).
+__global__ void markov_rows_kernel(const double* __restrict__ table, int V, int order, const int* ctx0,
+                                   uint8_t* ws, TreeLayout L, const int* node_ids, int n_nodes, int from_batch,
+                                   double* out, long long ld) {
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int i = blockIdx.x;
+  const int cnt = from_batch ? c->batch_n : n_nodes;
+  if (i >= cnt) return;
+  __shared__ long long row_idx;
+  if (threadIdx.x == 0) {
+    const int cur = c->cur;
+    const int* par = at<int>(ws, L.m_parent[cur]);
+    const unsigned long long* lo = at<unsigned long long>(ws, L.m_lo[cur]);
+    int node = from_batch ? at<int>(ws, L.b_node)[i] : node_ids[i];
+    int toks[64];
+    int nt = 0;
+    while (node >= 0 && nt < order) {
+      toks[nt++] = lo_token(lo[node]);
+      node = par[node];
+    }
+    // context = (ctx0 + path)[-order:]
+    long long idx = 0;
+    for (int k = 0; k < order; ++k) {
+      const int pos_from_end = order - 1 - k;  // 0 = last token
+      const int t = pos_from_end < nt ? toks[pos_from_end] : ctx0[order - 1 - (pos_from_end - nt)];
+      idx = idx * V + t;
+    }
+    row_idx = idx;
+  }
+  __syncthreads();
+  const double* src = table + row_idx * V;
+  double* dst = out + (long long)i * ld;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) dst[v] = src[v];
+}
+
+}  // namespace sx
+
+using namespace sx;
+
+static size_t upd_smem_bytes(const TreeLayout& L) {
+  return ((sizeof(UpdSmem) + 15) & ~size_t(15)) + (size_t)L.kpad * (8 + 8 + 4) + 64;
+}
+
+extern "C" long long sx_tree_workspace_bytes(int K, int B, int V, int D) {
+  if (K < 1 || B < 1 || V < 2 || D < 1 || D > 250) return -1;
+  return tree_layout(K, B, V, D).total;
+}
+
+extern "C" int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n) {
+  TreeLayout L = tree_layout(K, B, V, D);
+  const long long vals[] = {L.ctl,     L.b_node,  L.b_nll,   L.b_depth, L.b_lex,   L.b_slot,  L.b_token,
+                            L.b_anc,   L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows,
+                            L.total};
+  const int m = (int)(sizeof(vals) / sizeof(vals[0]));
+  for (int i = 0; i < n && i < m; ++i) out[i] = vals[i];
+  return m;
+}
+
+static int check_tree_args(int K, int B, int V, int D) {
+  if (K < 1 || B < 1 || V < 2 || D < 1) return arg_error("tree: need K, B, D >= 1 and V >= 2");
+  if (K > 8192) return arg_error("tree: budget K=%d exceeds the 8192 single-CTA select/sort capacity", K);
+  if (D > 250) return arg_error("tree: max_depth %d > 250", D);
+  if (V > 262144) return arg_error("tree: vocab %d > 262144", V);
+  return SX_OK;
+}
+
+extern "C" int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, cudaStream_t stream) {
+  int st = check_tree_args(K, B, V, D);
+  if (st) return st;
+  TreeLayout L = tree_layout(K, B, V, D);
+  tree_begin_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, root_slot);
+  SX_CHECK_LAUNCH("tree_begin_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
+                             int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream) {
+  int st = check_tree_args(K, B, V, D);
+  if (st) return st;
+  if (row_kind != SX_ROWS_LOGITS_F32 && row_kind != SX_ROWS_PROBS_F64) return arg_error("tree: bad row kind");
+  if (ld < V) return arg_error("tree: row stride %lld < V %d", ld, V);
+  TreeLayout L = tree_layout(K, B, V, D);
+  uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(tree_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tree_warp_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
+    cudaFuncSetAttribute(tree_argmax_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
+    attrs = true;
+  }
+  if (score_mode == SX_SCORE_ARGMAX) {
+    tree_argmax_score_kernel<<<B, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld);
+    SX_CHECK_LAUNCH("tree_argmax_score_kernel");
+  } else if (score_mode == SX_SCORE_WARP) {
+    tree_warp_rows_kernel<<<B, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld, temperature, top_p);
+    SX_CHECK_LAUNCH("tree_warp_rows_kernel");
+    dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, B);
+    tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, nullptr, -1, V);
+    SX_CHECK_LAUNCH("tree_score_kernel");
+  } else if (score_mode == SX_SCORE_RAW) {
+    if (row_kind == SX_ROWS_LOGITS_F32) {
+      tree_row_stats_kernel<<<B, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld);
+      SX_CHECK_LAUNCH("tree_row_stats_kernel");
+    }
+    dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, B);
+    tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, rows, row_kind, ld);
+    SX_CHECK_LAUNCH("tree_score_kernel");
+  } else {
+    return arg_error("tree: bad score mode %d", score_mode);
+  }
+  const size_t smem = upd_smem_bytes(L);
+  if (smem > 227 * 1024) return arg_error("tree: update needs %zu B of shared memory", smem);
+  tree_update_kernel<<<1, kUpdThreads, smem, stream>>>(w, L);
+  SX_CHECK_LAUNCH("tree_update_kernel");
+  if (host_ctl) {
+    cudaError_t e = cudaMemcpyAsync(host_ctl, w + L.ctl, sizeof(TreeCtl), cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) return cuda_status(e, "sx_tree_round: ctl readback");
+  }
+  return SX_OK;
+}
+
+extern "C" int sx_tree_finalize(void* ws, int K, int B, int V, int D, int* out_parent, int* out_token,
+                                double* out_edge, int* out_depth, cudaStream_t stream) {
+  int st = check_tree_args(K, B, V, D);
+  if (st) return st;
+  TreeLayout L = tree_layout(K, B, V, D);
+  tree_final_kernel<<<(K + 256) / 256, 256, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, out_parent, out_token,
+                                                          out_edge, out_depth);
+  SX_CHECK_LAUNCH("tree_final_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_markov_rows(const double* table, int V, int order, const int* ctx0, void* ws, int K, int B, int D,
+                              const int* node_ids, int n_nodes, int from_batch, double* out, long long ld,
+                              cudaStream_t stream) {
+  int st = check_tree_args(K, B, V, D);
+  if (st) return st;
+  if (order < 0 || order > 64) return arg_error("markov: order %d out of range", order);
+  TreeLayout L = tree_layout(K, B, V, D);
+  const int grid = from_batch ? B : n_nodes;
+  if (grid <= 0) return SX_OK;
+  markov_rows_kernel<<<grid, 128, 0, stream>>>(table, V, order, ctx0, reinterpret_cast<uint8_t*>(ws), L, node_ids,
+                                               n_nodes, from_batch, out, ld);
+  SX_CHECK_LAUNCH("markov_rows_kernel");
+  return SX_OK;
+}

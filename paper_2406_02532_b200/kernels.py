@@ -8,6 +8,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _lib
@@ -90,4 +92,193 @@ def gemm(
         splits,
         stream_ptr(),
     )
+    return out
+
+
+# ---------------------------------------------------------------------------
+# canonical row kernels (sampling.py / engine.py semantics)
+# ---------------------------------------------------------------------------
+
+from ._lib import ROWS_LOGITS_F32, ROWS_PROBS_F64, SCORE_ARGMAX, SCORE_RAW, SCORE_WARP  # noqa: E402
+
+_scratch_cache: dict[tuple[int, str], torch.Tensor] = {}
+
+
+def scratch(nbytes: int, device: torch.device, tag: str) -> torch.Tensor:
+    key = (device.index or 0, tag)
+    buf = _scratch_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        _scratch_cache[key] = buf
+    return buf
+
+
+def row_kind(rows: torch.Tensor) -> int:
+    if rows.dtype == torch.float32:
+        return ROWS_LOGITS_F32
+    if rows.dtype == torch.float64:
+        return ROWS_PROBS_F64
+    raise ValueError(f"rows must be fp32 logits or fp64 probabilities, got {rows.dtype}")
+
+
+def warp_rows(rows: torch.Tensor, temperature: float, top_p: float, row_ids: torch.Tensor | None = None) -> torch.Tensor:
+    """apply_warp of each row (fp32 logits or fp64 probabilities) -> fp64 rows."""
+    _require_cuda(rows)
+    if rows.stride(-1) != 1:
+        rows = rows.contiguous()
+    n = rows.shape[0] if row_ids is None else row_ids.numel()
+    V = rows.shape[1]
+    out = torch.empty((n, V), dtype=torch.float64, device=rows.device)
+    lib = _lib.load()
+    sc = scratch(lib.sx_warp_scratch_bytes(n, V), rows.device, "warp")
+    call("sx_warp_rows", ptr(rows), row_kind(rows), rows.stride(0), V, ptr(row_ids), n, float(temperature), float(top_p),
+         ptr(out), V, ptr(sc), stream_ptr())
+    return out
+
+
+def sample_rows(warped: torch.Tensor, uniforms) -> torch.Tensor:
+    _require_cuda(warped)
+    n, V = warped.shape
+    u = torch.as_tensor(np.asarray(uniforms, dtype=np.float64)).to(warped.device)
+    out = torch.empty(n, dtype=torch.int32, device=warped.device)
+    call("sx_sample_rows", ptr(warped), warped.stride(0), V, ptr(u), n, ptr(out), stream_ptr())
+    return out.cpu()
+
+
+def softmax_rows(logits: torch.Tensor, row_ids: torch.Tensor | None = None) -> torch.Tensor:
+    """Canonical float64 probabilities of fp32 logits rows."""
+    _require_cuda(logits)
+    n = logits.shape[0] if row_ids is None else row_ids.numel()
+    V = logits.shape[1]
+    out = torch.empty((n, V), dtype=torch.float64, device=logits.device)
+    call("sx_softmax_rows", ptr(logits), logits.stride(0), V, ptr(row_ids), n, ptr(out), V, stream_ptr())
+    return out
+
+
+def argmax_rows(rows: torch.Tensor) -> torch.Tensor:
+    _require_cuda(rows)
+    n, V = rows.shape
+    out = torch.empty(n, dtype=torch.int32, device=rows.device)
+    call("sx_argmax_rows", ptr(rows), row_kind(rows), rows.stride(0), V, n, ptr(out), stream_ptr())
+    return out
+
+
+class WalkResult:
+    __slots__ = ("tokens", "fell_off", "cursor", "path_rows")
+
+    def __init__(self, tokens, fell_off, cursor, path_rows):
+        self.tokens = tokens
+        self.fell_off = fell_off
+        self.cursor = cursor
+        self.path_rows = path_rows
+
+
+def verify_walk(rows: torch.Tensor, parent: torch.Tensor, token: torch.Tensor, n_nodes: int, start_cursor: int,
+                uniforms: np.ndarray, max_steps: int, temperature: float, top_p: float,
+                out_host: torch.Tensor | None = None) -> WalkResult:
+    """Acceptance walk over cached target rows (engine.py:118-128) on one CTA."""
+    dev = rows.device
+    V = rows.shape[1]
+    lib = _lib.load()
+    sc = scratch(lib.sx_row_scratch_bytes(V), dev, "walk")
+    u = torch.as_tensor(np.ascontiguousarray(uniforms[:max_steps], dtype=np.float64))
+    if u.numel() < max_steps:
+        u = torch.cat([u, torch.zeros(max_steps - u.numel(), dtype=torch.float64)])
+    u = u.to(dev, non_blocking=True)
+    out = torch.empty(3 + 2 * max_steps, dtype=torch.int32, device=dev)
+    call("sx_verify_walk", ptr(rows), row_kind(rows), rows.stride(0), V, ptr(parent), ptr(token), n_nodes,
+         start_cursor, ptr(u), max_steps, float(temperature), float(top_p), ptr(out), ptr(sc), stream_ptr())
+    if out_host is None:
+        host = out.cpu()
+    else:
+        host = out_host[: out.numel()]
+        host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    h = host.tolist()
+    n = h[0]
+    return WalkResult(h[3 : 3 + n], bool(h[1]), h[2], h[3 + max_steps : 3 + max_steps + n - (1 if h[1] else 0)])
+
+
+# ---------------------------------------------------------------------------
+# stage-1 tree workspace
+# ---------------------------------------------------------------------------
+
+_OFF_NAMES = ["ctl", "b_node", "b_nll", "b_depth", "b_lex", "b_slot", "b_token", "b_anc", "b_anc_len",
+              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "total"]
+
+
+class TreeWorkspace:
+    """Device state of one draft-tree build (csrc/tree_layout.h)."""
+
+    def __init__(self, K: int, B: int, V: int, D: int, device: torch.device | None = None):
+        lib = _lib.load()
+        self.K, self.B, self.V, self.D = K, B, V, D
+        nbytes = lib.sx_tree_workspace_bytes(K, B, V, D)
+        if nbytes < 0:
+            raise ValueError("invalid tree parameters")
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        offs = (ctypes.c_longlong * len(_OFF_NAMES))()
+        lib.sx_tree_offsets(K, B, V, D, offs, len(_OFF_NAMES))
+        self.off = dict(zip(_OFF_NAMES, list(offs)))
+        self.ctl_host = torch.zeros(16, dtype=torch.int32).pin_memory()
+        self.rounds = 0
+
+    def view(self, name: str, dtype: torch.dtype, n: int) -> torch.Tensor:
+        o = self.off[name]
+        item = torch.empty((), dtype=dtype).element_size()
+        return self.buf[o : o + n * item].view(dtype)
+
+    # batch inputs of the next draft call
+    def batch_tokens(self) -> torch.Tensor:
+        return self.view("b_token", torch.int32, self.B)
+
+    def batch_depth(self) -> torch.Tensor:
+        return self.view("b_depth", torch.int32, self.B)
+
+    def batch_slots(self) -> torch.Tensor:
+        return self.view("b_slot", torch.int32, self.B)
+
+    def batch_anc(self) -> torch.Tensor:
+        return self.view("b_anc", torch.int32, self.B * (self.D + 1)).view(self.B, self.D + 1)
+
+    def batch_anc_len(self) -> torch.Tensor:
+        return self.view("b_anc_len", torch.int32, self.B)
+
+    def final_tables(self, n_rows: int):
+        anc = self.view("f_anc", torch.int32, (self.K + 1) * (self.D + 1)).view(self.K + 1, self.D + 1)[:n_rows]
+        return (anc, self.view("f_anc_len", torch.int32, self.K + 1)[:n_rows],
+                self.view("f_depth", torch.int32, self.K + 1)[:n_rows], self.view("f_token", torch.int32, self.K + 1)[:n_rows])
+
+    def begin(self, root_slot: int = 0) -> None:
+        self.rounds = 0
+        call("sx_tree_begin", ptr(self.buf), self.K, self.B, self.V, self.D, root_slot, stream_ptr())
+
+    def round(self, rows: torch.Tensor, score_mode: int, temperature: float = 1.0, top_p: float = 1.0) -> dict:
+        """Score the current batch's rows, update the tree; returns the control block."""
+        _require_cuda(rows)
+        call("sx_tree_round", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(rows), row_kind(rows), rows.stride(0),
+             score_mode, float(temperature), float(top_p), self.ctl_host.data_ptr(), stream_ptr())
+        torch.cuda.current_stream().synchronize()
+        self.rounds += 1
+        c = self.ctl_host.tolist()
+        if c[8]:
+            raise RuntimeError("tree: survivor buffer overflow")
+        return {"count": c[1], "has_thr": c[2], "slot_next": c[4], "batch_n": c[5]}
+
+    def finalize(self, n: int):
+        parent = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        token = torch.empty_like(parent)
+        depth = torch.empty_like(parent)
+        edge = torch.empty(max(n, 1), dtype=torch.float64, device=self.device)
+        call("sx_tree_finalize", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(parent), ptr(token), ptr(edge),
+             ptr(depth), stream_ptr())
+        return parent[:n], token[:n], edge[:n], depth[:n]
+
+
+def markov_rows(table: torch.Tensor, order: int, ctx0: torch.Tensor, ws: TreeWorkspace, node_ids: torch.Tensor | None,
+                n_nodes: int, from_batch: bool, out: torch.Tensor) -> torch.Tensor:
+    V = table.shape[1]
+    call("sx_markov_rows", ptr(table), V, order, ptr(ctx0), ptr(ws.buf), ws.K, ws.B, ws.D, ptr(node_ids), n_nodes,
+         int(from_batch), ptr(out), out.stride(0), stream_ptr())
     return out

@@ -1,0 +1,233 @@
+"""Language-model plugins: the reference interface over device-resident models.
+
+`LanguageModel` is the reference plugin API (pkg/src/speckit/models.py:32-63):
+`vocab_size`, `backend`, `next_distribution(prefix) -> float64[V]` and
+`next_distributions(prefixes) -> float64[n, V]`, pure and batch-consistent,
+`ValueError` on out-of-vocabulary tokens (:24-29).
+
+Every model in this package is additionally a *device model*: it keeps its
+parameters in HBM and produces next-token rows for draft-tree nodes directly on
+the GPU (no host round trip per row), which is what the GPU tree builder and
+the target pass over the tree consume:
+
+  tree_session(prefix, params) -> session with .ws (TreeWorkspace), .batch_rows(),
+                                  .advance(ctl), .finish(tree)
+  tree_rows(tree) -> device rows [len(tree)+1, V] (row 0 = anchor, row i+1 = node i)
+
+The exact table backends (`TabularModel`, `MarkovModel`, `make_synthetic`,
+models.py:77-151, 265-279) upload their float64 tables; Llama-shaped models live
+in `llama.py`.
+"""
+
+from __future__ import annotations
+
+import json
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .tree import BuilderParams
+
+Prefix = tuple[int, ...]
+
+
+def _check_prefix(prefix: Sequence[int], vocab_size: int) -> Prefix:
+    toks = tuple(int(t) for t in prefix)
+    for t in toks:
+        if not 0 <= t < vocab_size:
+            raise ValueError(f"token id {t} outside vocabulary [0, {vocab_size})")
+    return toks
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2406_02532_b200 needs a CUDA device (B200); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class LanguageModel:
+    """Interface shared by all backends (models.py:32-63)."""
+
+    vocab_size: int
+    backend: str
+
+    def next_distribution(self, prefix: Sequence[int]) -> np.ndarray:
+        return self.next_distributions([prefix])[0]
+
+    def next_distributions(self, prefixes: Iterable[Sequence[int]]) -> np.ndarray:
+        raise NotImplementedError
+
+    def to_json(self) -> str:
+        raise NotImplementedError
+
+    def decode(self, tokens: Sequence[int]) -> str:
+        return " ".join(str(int(t)) for t in tokens)
+
+    def encode(self, text: str) -> Prefix:
+        raise NotImplementedError(f"{self.backend} backend has no text mapping")
+
+
+def as_device_model(model) -> "LanguageModel":
+    if not hasattr(model, "tree_session") or not hasattr(model, "tree_rows"):
+        raise TypeError(
+            f"{type(model).__name__} is not a device model; use paper_2406_02532_b200 models "
+            "(TabularModel/MarkovModel/make_synthetic/LlamaModel)"
+        )
+    return model
+
+
+def _normalize_rows(table: np.ndarray) -> np.ndarray:
+    """models.py:66-74 (validation + one-time normalisation)."""
+    table = np.asarray(table, dtype=np.float64)
+    sums = table.sum(axis=-1, keepdims=True)
+    if np.any(table < 0) or np.any(sums <= 0):
+        raise ValueError("probability table rows must be non-negative with positive mass")
+    if np.max(np.abs(sums - 1.0)) <= 1e-9:
+        return table.copy()
+    return table / sums
+
+
+class _WorkspaceCache:
+    def __init__(self):
+        self._ws = {}
+
+    def get(self, budget: int, B: int, V: int, D: int) -> K.TreeWorkspace:
+        key = (budget, B, V, D)
+        ws = self._ws.get(key)
+        if ws is None:
+            if len(self._ws) > 4:
+                self._ws.clear()
+            ws = K.TreeWorkspace(budget, B, V, D)
+            self._ws[key] = ws
+        return ws
+
+
+_WS = _WorkspaceCache()
+
+
+class _TableSession:
+    def __init__(self, model: "MarkovModel", prefix: Prefix, params: BuilderParams):
+        self.model = model
+        self.ws = _WS.get(params.budget, params.batch_size, model.vocab_size, params.max_depth)
+        self.ws.begin(root_slot=0)
+        self.ctx0 = model._context_tensor(prefix)
+        self.rows = torch.empty((params.batch_size, model.vocab_size), dtype=torch.float64, device=self.ws.device)
+
+    def batch_rows(self) -> torch.Tensor:
+        m = self.model
+        return K.markov_rows(m.table_dev, m.order, self.ctx0, self.ws, None, 0, True, self.rows)
+
+    def advance(self, ctl) -> None:
+        pass
+
+    def finish(self, tree) -> None:
+        tree.ctx0 = self.ctx0
+
+
+class MarkovModel(LanguageModel):
+    """Order-k Markov chain over a dense table (models.py:100-151), table in HBM."""
+
+    backend = "markov"
+
+    def __init__(self, table: np.ndarray, order: int = 1, _stationary: bool = False) -> None:
+        if order < 1 and not _stationary:
+            raise ValueError(f"order must be >= 1, got {order}")
+        table = _normalize_rows(table)
+        vocab = table.shape[1]
+        if table.shape[0] != vocab**order:
+            raise ValueError(f"table has {table.shape[0]} rows, expected vocab**order = {vocab**order}")
+        self.table = table
+        self.order = order
+        self.vocab_size = vocab
+        self.table_dev = torch.as_tensor(table).to(_device())
+
+    def _row_index(self, prefix: Prefix) -> int:
+        if self.order == 0:
+            return 0
+        context = prefix[-self.order :]
+        context = (0,) * (self.order - len(context)) + context
+        idx = 0
+        for t in context:
+            idx = idx * self.vocab_size + t
+        return idx
+
+    def _context_tensor(self, prefix: Prefix) -> torch.Tensor:
+        n = max(self.order, 1)
+        ctx = (0,) * n + tuple(prefix)
+        return torch.tensor(ctx[-n:], dtype=torch.int32).to(self.table_dev.device)
+
+    def next_distributions(self, prefixes) -> np.ndarray:
+        idx = [self._row_index(_check_prefix(p, self.vocab_size)) for p in prefixes]
+        if not idx:
+            return np.empty((0, self.vocab_size))
+        sel = torch.tensor(idx, dtype=torch.long, device=self.table_dev.device)
+        return self.table_dev.index_select(0, sel).cpu().numpy()
+
+    def power_smoothed(self, power: float) -> "MarkovModel":
+        return type(self)._from_table(self.table**power, self.order)
+
+    @classmethod
+    def _from_table(cls, table, order):
+        return MarkovModel(table, order=order)
+
+    def to_json(self) -> str:
+        return json.dumps({"backend": self.backend, "vocab_size": self.vocab_size, "order": self.order,
+                           "table": self.table.tolist()})
+
+    # ---- device-model protocol ----
+    def tree_session(self, prefix: Prefix, params: BuilderParams) -> _TableSession:
+        _check_prefix(prefix, self.vocab_size)
+        return _TableSession(self, prefix, params)
+
+    def tree_rows(self, tree) -> torch.Tensor:
+        """Rows for the anchor and every node of a tree built on the GPU."""
+        n = len(tree.nodes)
+        ws = tree.workspace
+        ids = torch.arange(-1, n, dtype=torch.int32, device=ws.device)
+        out = torch.empty((n + 1, self.vocab_size), dtype=torch.float64, device=ws.device)
+        ctx0 = self._context_tensor(tree.prefix)
+        return K.markov_rows(self.table_dev, self.order, ctx0, ws, ids, n + 1, False, out)
+
+    def prefix_rows(self, prefix: Prefix) -> torch.Tensor:
+        idx = self._row_index(_check_prefix(prefix, self.vocab_size))
+        return self.table_dev[idx : idx + 1]
+
+
+class TabularModel(MarkovModel):
+    """Stationary backend: one fixed row (models.py:77-97) = an order-0 table."""
+
+    backend = "tabular"
+
+    def __init__(self, row: Sequence[float]) -> None:
+        r = _normalize_rows(np.asarray(row, dtype=np.float64)[None, :])[0]
+        super().__init__(r[None, :], order=0, _stationary=True)
+        self.row = r
+
+    def power_smoothed(self, power: float) -> "TabularModel":
+        return TabularModel(self.row**power)
+
+    def to_json(self) -> str:
+        return json.dumps({"backend": self.backend, "vocab_size": self.vocab_size, "row": self.row.tolist()})
+
+
+def make_synthetic(seed: int, vocab_size: int, sharpness: float, order: int = 1) -> MarkovModel:
+    """Random Markov model with Dirichlet rows (models.py:265-279); same draws as the reference."""
+    if vocab_size < 2:
+        raise ValueError(f"vocab_size must be >= 2, got {vocab_size}")
+    if sharpness <= 0:
+        raise ValueError(f"sharpness must be > 0, got {sharpness}")
+    gen = np.random.default_rng(seed)
+    table = gen.dirichlet(np.full(vocab_size, sharpness), size=vocab_size**order)
+    return MarkovModel(table, order=order)
+
+
+def model_from_json(document: str) -> LanguageModel:
+    data = json.loads(document)
+    backend = data.get("backend")
+    if backend == "tabular":
+        return TabularModel(data["row"])
+    if backend == "markov":
+        return MarkovModel(np.asarray(data["table"]), order=data["order"])
+    raise ValueError(f"unknown backend {backend!r}")

@@ -1,0 +1,63 @@
+"""The C-ABI library loads (no GPU needed) and exports exactly what
+include/specexec_b200.h declares; argument errors surface as ValueError without
+touching a device."""
+
+import ctypes
+import pathlib
+import re
+import subprocess
+
+import pytest
+
+from paper_2406_02532_b200 import _lib
+
+HDR = pathlib.Path(__file__).resolve().parents[1] / "include" / "specexec_b200.h"
+
+
+def header_symbols():
+    text = HDR.read_text()
+    return sorted(set(re.findall(r"SX_API\s+[\w\s\*]+?\b(sx_\w+)\s*\(", text)))
+
+
+def test_header_declares_symbols():
+    syms = header_symbols()
+    assert "sx_gemm_bf16" in syms and "sx_tree_round" in syms and "sx_verify_walk" in syms
+    assert len(syms) >= 15
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True, check=True)
+    exported = set(re.findall(r"\bT (sx_\w+)", out.stdout))
+    for s in header_symbols():
+        assert s in exported, s
+        assert hasattr(lib, s)
+    # nothing else leaks out of the C ABI
+    assert exported == set(header_symbols())
+
+
+def test_python_binding_covers_header():
+    assert set(_lib.SIGNATURES) == set(header_symbols())
+
+
+def test_version_and_errors_without_gpu():
+    lib = _lib.load()
+    assert lib.sx_abi_version() == 1
+    bn, sp, ws = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong()
+    st = lib.sx_gemm_plan(10, 10, 100, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws))
+    assert st < 0 and b"multiple of 64" in lib.sx_last_error()
+    with pytest.raises(ValueError):
+        _lib.check(st, "sx_gemm_plan")
+    assert lib.sx_tree_workspace_bytes(1024, 64, 32000, 16) > 0
+    assert lib.sx_tree_workspace_bytes(0, 64, 32000, 16) < 0
+
+
+def test_gemm_plan_tiles():
+    lib = _lib.load()
+    bn, sp, ws = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong()
+    assert lib.sx_gemm_plan(1025, 8192, 8192, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
+    assert bn.value % 16 == 0 and bn.value * ((1025 + bn.value - 1) // bn.value) < 1025 + 5 * 16
+    assert sp.value == 1
+    # a weight-streaming draft projection gets split-K to cover the SMs
+    assert lib.sx_gemm_plan(64, 4096, 4096, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
+    assert sp.value > 1 and ws.value == sp.value * 64 * 4096
