@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""SpecExec target-iteration benchmark on B200 (BASELINE.json metric:
+generated tokens/s, with accepted tokens per target iteration beside it).
+
+A *step* is one SpecExec target iteration: GPU draft-tree build (stage 1), one
+target pass over the anchor + every tree node (stage 2), the acceptance walk
+and KV compaction (stage 4). Default workload = BASELINE configs[1] (C2):
+Llama-2-7B-shaped draft + Llama-2-70B-shaped target, random-init bf16, target
+resident in HBM on one B200, budget K=1024, t=0, one random 128-token prompt.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N>1 (torchrun): round 1 runs N independent replicas (weak scaling); the
+target-TP path is the next row.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (draft preset, target preset, K, D, B, temperature, top_p)
+    "c2": ("llama2-7b", "llama2-70b", 1024, 16, 128, 0.0, 1.0),
+    "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 128, 0.0, 1.0),
+    "tiny": ("tiny-draft", "tiny", 128, 16, 8, 0.0, 1.0),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--budget", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--scoring", choices=["raw", "warped"], default="raw",
+                    help="raw: score the tree with the draft's raw distribution (SURVEY F2); "
+                         "warped: reference default (t=0 -> greedy chain)")
+    ap.add_argument("--synthetic", type=float, default=0.0,
+                    help="scale of the shared synthetic prev-token logit bias (0 = pure random init)")
+    ap.add_argument("--prompt-len", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sus": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline(args, w, accepted_per_iter: float, rounds_per_iter: float, tree_nodes: int, ctx: int) -> dict:
+    """The oracle port timed on this host: one fp32 decoder layer of the target
+    at N = K+1 tree tokens and one of the draft at B tokens (oracle/llama_ref.py
+    arithmetic, all host threads), extrapolated to the full depth, plus the
+    oracle's tree bookkeeping (oracle build_sssp over synthetic rows of the same
+    V/K/B). tokens/s = accepted tokens per iteration / CPU seconds per iteration."""
+    import torch
+
+    from oracle import llama_ref
+    from oracle import speckit_oracle as ox
+    from paper_2406_02532_b200.llama import PRESETS
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    dname, tname, K, D, B = w[0], w[1], w[2], w[3], w[4]
+
+    def layer_seconds(cfg, n_tok, n_ctx):
+        g = torch.Generator().manual_seed(0)
+        d, H, KVH, hd = cfg.d, cfg.heads, cfg.kv_heads, cfg.head_dim
+        L = {"wqkv": torch.randn(cfg.qkv_out, d, generator=g) * 0.02, "wo": torch.randn(d, H * hd, generator=g) * 0.02,
+             "wg": torch.randn(cfg.ff, d, generator=g) * 0.02, "wu": torch.randn(cfg.ff, d, generator=g) * 0.02,
+             "wd": torch.randn(d, cfg.ff, generator=g) * 0.02, "n1": torch.ones(d), "n2": torch.ones(d)}
+        x = torch.randn(n_tok, d, generator=g)
+        kctx = torch.randn(n_ctx, KVH, hd, generator=g)
+        t0 = time.perf_counter()
+        with torch.no_grad():
+            h = llama_ref.rmsnorm(x, L["n1"], cfg.eps)
+            qkv = h @ L["wqkv"].t()
+            q = qkv[:, : H * hd].view(n_tok, H, hd)
+            k = kctx.repeat_interleave(H // KVH, dim=1)
+            s = torch.einsum("qhd,khd->hqk", q, k) / hd**0.5
+            att = torch.einsum("hqk,khd->qhd", s.softmax(-1), k).reshape(n_tok, H * hd)
+            x = x + att @ L["wo"].t()
+            h = llama_ref.rmsnorm(x, L["n2"], cfg.eps)
+            x = x + (torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
+        return time.perf_counter() - t0
+
+    tcfg, dcfg = PRESETS[tname], PRESETS[dname]
+    t_layer = layer_seconds(tcfg, tree_nodes + 1, ctx + tree_nodes + 1)
+    d_layer = layer_seconds(dcfg, B, ctx + 64)
+    # LM heads: one GEMM each
+    t_head = 2.0 * (tree_nodes + 1) * tcfg.d * tcfg.vocab / 0.7e12
+    t0 = time.perf_counter()
+    lm = ox.LogitsLM(tcfg.vocab, ox.hashed_logits_fn(tcfg.vocab, 11, 1.3))
+    ox.build_sssp(tuple(range(8)), lm, ox.BuilderParams(K, D, B))
+    t_tree = time.perf_counter() - t0
+    per_iter = t_layer * tcfg.layers + t_head + rounds_per_iter * d_layer * dcfg.layers + t_tree
+    value = accepted_per_iter / per_iter
+    return {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": (f"one fp32 {tname} layer at N={tree_nodes + 1} ({t_layer:.2f}s) x {tcfg.layers} + LM head, "
+                       f"one fp32 {dname} layer at B={B} ({d_layer:.2f}s) x {dcfg.layers} x {rounds_per_iter:.1f} rounds, "
+                       f"oracle build_sssp K={K} V={tcfg.vocab} ({t_tree:.2f}s); extrapolated "
+                       f"{per_iter:.1f} s/iteration at {accepted_per_iter:.2f} accepted tokens/iteration"),
+            "seconds_per_iteration": per_iter}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    K = args.budget or w[2]
+    B = args.batch or w[4]
+    steps = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args, (w[0], w[1], K, w[3], B), 1.0, max(1.0, K / B + 1), K, args.prompt_len)
+        if i >= args.warmup:
+            steps.append(cb["seconds_per_iteration"])
+    sec = statistics.mean(steps)
+    value = 1.0 / sec
+    cb["value"] = value
+    line = {"impl": "reference", "metric": "generated tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {w[0]} draft + {w[1]} target, K={K}, D={w[3]}, B={B}, t={w[5]}",
+                       "note": "CPU oracle port (extrapolated per-layer timing; 1 accepted token/iteration assumed)"},
+            "cpu_baseline": cb, "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2406_02532_b200 as sx
+    from paper_2406_02532_b200 import _lib
+    from paper_2406_02532_b200 import kernels as Kern
+    from paper_2406_02532_b200.engine import SpecExecSession
+    from paper_2406_02532_b200.llama import PRESETS, LlamaModel, SyntheticBias
+
+    dname, tname, K, D, B, temp, top_p = WORKLOADS[args.workload]
+    K = args.budget or K
+    B = args.batch or B
+    syn = SyntheticBias(seed=99, rank=64, scale=args.synthetic) if args.synthetic > 0 else None
+    t_init = time.time()
+    max_new = 100000
+    ctx_cap = args.prompt_len + (args.warmup + args.steps) * (D + 1) * 3 + 64
+    target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn)
+    draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
+                       synthetic=syn)
+    torch.cuda.synchronize()
+    init_s = time.time() - t_init
+    params = sx.BuilderParams(K, D, B)
+    cfg = sx.SamplingConfig(temp, top_p, seed=rank, max_new_tokens=max_new)
+    warp_scores = args.scoring == "warped"
+    prompt = tuple(int(t) for t in np.random.default_rng(1000 + rank).integers(0, PRESETS[tname].vocab, size=args.prompt_len))
+
+    sess = SpecExecSession(prompt, draft, target, params, cfg, warp_scores)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        sess.step(max_new)
+    # ---------------- timed region: exactly `steps` target iterations
+    Kern.PROFILER = Kern.GemmProfiler()
+    launches0 = _lib.load().sx_launch_count()
+    it0, tok0, dc0 = sess.stats.target_calls, len(sess.tokens), sess.stats.draft_calls
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        n_iter = 0
+        while n_iter < args.steps:
+            sess.step(max_new)
+            if sess.cache is None:  # the iteration ended with a miss
+                n_iter += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = _lib.load().sx_launch_count() - launches0
+    prof = Kern.PROFILER
+    Kern.PROFILER = None
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms, world)
+    tokens = len(sess.tokens) - tok0
+    iters = sess.stats.target_calls - it0 + (0 if sess.cache is None else -1)
+    iters = max(iters, args.steps)
+    draft_calls = sess.stats.draft_calls - dc0
+    total_tokens = sum_over_ranks(tokens, world)
+    value = total_tokens / (ms_max / 1e3)
+    accepted_per_iter = tokens / args.steps
+
+    # dominant kernel: the tcgen05 GEMM of the target pass over the tree
+    pk = peaks()
+    big = prof.summary(min_m=max(2, K // 2))
+    small = prof.summary(min_m=0)
+    ach = big["flops"] / (big["ms"] / 1e3) / 1e12 if big["ms"] > 0 else 0.0
+    gemm_share = small["ms"] / ms if ms > 0 else 0.0
+    roof = {"bound": "tensor", "kernel": "gemm_tc_kernel (target pass, M=K+1 tree tokens)", "achieved": ach,
+            "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"] if pk["bf16_sus"] else None,
+            "peak_source": f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)", "traffic": None,
+            "launches": big["launches"], "gemm_share_of_step": gemm_share,
+            "flops_per_launch_avg": big["flops"] / max(1, big["launches"])}
+
+    clk = clocks.summary()
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Kern.IO["h2d"] = Kern.IO["d2h"] = 0
+        prompt2 = tuple(int(t) for t in np.random.default_rng(2000 + rank).integers(0, PRESETS[tname].vocab,
+                                                                                       size=args.prompt_len))
+        cfg2 = sx.SamplingConfig(temp, top_p, seed=rank + 7, max_new_tokens=max(1, int(round(accepted_per_iter * args.steps))))
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        toks2, st2 = sx.generate_specexec(prompt2, draft, target, params, cfg2, warp_scores=warp_scores)
+        torch.cuda.synchronize()
+        el = max_over_ranks(time.perf_counter() - t0, world)
+        n_it = max(1, st2.target_calls)
+        h2d = Kern.IO["h2d"] + 8 * len(prompt2)
+        e2e = {"value": sum_over_ranks(len(toks2), world) / el, "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d / n_it), "d2h_bytes_per_step": int((Kern.IO["d2h"] + 4 * len(toks2)) / n_it),
+               "iterations": n_it, "includes": "prompt prefill, tree builds, target passes, walks, host sync per round"}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args, (dname, tname, K, D, B), accepted_per_iter, draft_calls / max(1, iters), K,
+                          args.prompt_len)
+    if rank == 0:
+        tb = PRESETS[tname].weight_bytes() + PRESETS[dname].weight_bytes()
+        line = {
+            "metric": "generated tokens/sec (accepted tokens per target iteration reported beside)",
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic: random-init weights (N(0,0.02)), random 128-token prompt" +
+                    (f", shared synthetic prev-token bias scale {args.synthetic}" if syn else ""),
+            "config": {"workload": f"{args.workload}: {dname} draft + {tname} target, resident in HBM, K={K}, D={D}, "
+                                   f"B={B}, t={temp}, scoring={args.scoring}",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)",
+                       "prompt_len": args.prompt_len},
+            "accepted_tokens_per_iter": accepted_per_iter,
+            "draft_calls_per_iter": draft_calls / max(1, iters),
+            "roofline": roof,
+            "cpu_baseline": cb,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "init_seconds": init_s,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

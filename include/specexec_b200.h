@@ -42,6 +42,8 @@ extern "C" {
 /* ---------------------------------------------------------------- misc */
 SX_API int sx_abi_version(void);
 SX_API const char* sx_last_error(void);
+/* number of kernels launched through this library since it was loaded */
+SX_API long long sx_launch_count(void);
 
 /* ----------------------------------------------- KG: dense projections
  * Y[t, f] (op)= sum_k X[t, k] * W[f, k]; bf16 in, fp32 accumulate on tcgen05.
@@ -85,8 +87,8 @@ SX_API int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n);
 SX_API int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, cudaStream_t stream);
 SX_API int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
                          int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream);
-SX_API int sx_tree_finalize(void* ws, int K, int B, int V, int D, int* out_parent, int* out_token, double* out_edge,
-                            int* out_depth, cudaStream_t stream);
+SX_API int sx_tree_finalize(void* ws, int K, int B, int V, int D, int root_token, int* out_parent, int* out_token,
+                            double* out_edge, int* out_depth, int* out_slot, cudaStream_t stream);
 
 /* ------------------------------------------------ exact table models on GPU
  * MarkovModel / TabularModel (pkg/src/speckit/models.py:77-151) rows for tree
@@ -126,6 +128,32 @@ SX_API int sx_argmax_rows(const void* rows, int row_kind, long long ld, int V, i
 /* sample (sampling.py:101-113) from n warped fp64 rows with uniforms u[n] */
 SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u, int n, int* out,
                           cudaStream_t stream);
+
+/* ------------------------------------------- KE / KA / KV3: model forward
+ * Llama-shaped forward used for the draft rounds (stage 1) and the single
+ * target pass over the flattened tree (stage 2); together they implement
+ * LanguageModel.next_distributions (pkg/src/speckit/models.py:47-52) for the
+ * B200 models. KV cache per layer: K and V [KVH][slots][128] bf16.
+ *   sx_embed      x[t] = float(E[tokens[t]])                    (fp32 residual)
+ *   sx_rmsnorm    y = bf16(x * rsqrt(mean(x^2) + eps) * w)
+ *   sx_rope_kv    rotate-half RoPE of q/k at pos_base + pos[t]; q -> [n,H,128];
+ *                 k,v -> cache slot slot_base + slot[t] (pos/slot NULL: t)
+ *   sx_tree_attention  query t attends KV slots [0, dense_len[t]) (NULL: dense_const)
+ *                 plus the anc_len[t] slots anc_base + anc[t*A ...] (root, ancestors, itself) -- the
+ *                 flattened ancestor mask of tree.py:208-219 without a dense mask
+ *   sx_kv_compact move KV rows src[i] -> dst[i] in every layer / head (accepted
+ *                 path -> committed region after the walk)
+ */
+SX_API int sx_embed(const void* E, const int* tokens, int n, int d, float* x, cudaStream_t stream);
+SX_API int sx_rmsnorm(const float* x, const void* w, int n, int d, float eps, void* y, cudaStream_t stream);
+SX_API int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const int* slot, int slot_base, int n, int H,
+                      int KVH, const float* cos_t, const float* sin_t, void* q, void* kcache, void* vcache,
+                      long long slots, cudaStream_t stream);
+SX_API int sx_tree_attention(const void* q, const void* kcache, const void* vcache, long long slots,
+                             const int* dense_len, int dense_const, const int* anc, int anc_base, const int* anc_len,
+                             int A, void* out, int N, int H, int KVH, cudaStream_t stream);
+SX_API int sx_kv_compact(void* kcache, void* vcache, int layers, long long layer_stride, long long slots, int KVH,
+                         const int* src, const int* dst, int n, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,58 @@
+"""fp32 CPU reference forward of the Llama architecture. TEST INFRASTRUCTURE.
+
+The floating-point reference for the target / draft logits of the B200 path
+(north_star tolerance: 2e-2 abs in bf16). Plain PyTorch on the CPU, fp32, full
+causal attention over an explicit token prefix -- i.e. exactly what the
+reference's stateless `LanguageModel.next_distributions(prefixes)`
+(pkg/src/speckit/models.py:47-52) means for a Llama-shaped model: no KV cache,
+no tree mask, no kernels. HF Llama conventions: RMSNorm, rotate-half RoPE
+(theta from the config), GQA by repeating KV heads, SwiGLU MLP, untied LM head.
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+def rope(x: torch.Tensor, pos: torch.Tensor, theta: float) -> torch.Tensor:
+    hd = x.shape[-1]
+    inv_freq = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
+    freqs = torch.outer(pos.float(), inv_freq)
+    cos, sin = freqs.cos()[:, None, :], freqs.sin()[:, None, :]
+    x0, x1 = x[..., : hd // 2], x[..., hd // 2 :]
+    return torch.cat([x0 * cos - x1 * sin, x1 * cos + x0 * sin], dim=-1)
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
+
+
+@torch.no_grad()
+def forward_logits(cfg, W: dict, tokens: list[int], bias=None, layers: int | None = None) -> torch.Tensor:
+    """fp32 logits [len(tokens), V] for every position of a causal prefix."""
+    n = len(tokens)
+    H, KVH, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
+    tok = torch.tensor(tokens, dtype=torch.long)
+    x = W["emb"][tok].clone()
+    pos = torch.arange(n)
+    mask = torch.full((n, n), float("-inf")).triu(1)
+    for L in W["layers"][: layers if layers is not None else len(W["layers"])]:
+        h = rmsnorm(x, L["n1"], cfg.eps)
+        qkv = h @ L["wqkv"].t()
+        q = qkv[:, : H * hd].view(n, H, hd)
+        k = qkv[:, H * hd : (H + KVH) * hd].view(n, KVH, hd)
+        v = qkv[:, (H + KVH) * hd :].view(n, KVH, hd)
+        q, k = rope(q, pos, cfg.rope_theta), rope(k, pos, cfg.rope_theta)
+        g = H // KVH
+        k = k.repeat_interleave(g, dim=1)
+        v = v.repeat_interleave(g, dim=1)
+        s = torch.einsum("qhd,khd->hqk", q, k) / hd**0.5 + mask
+        att = torch.einsum("hqk,khd->qhd", s.softmax(-1), v).reshape(n, H * hd)
+        x = x + att @ L["wo"].t()
+        h = rmsnorm(x, L["n2"], cfg.eps)
+        x = x + (torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
+    logits = rmsnorm(x, W["nf"], cfg.eps) @ W["lm"].t()
+    if bias is not None:
+        u, w = bias
+        logits = logits + u[tok] @ w.t()
+    return logits

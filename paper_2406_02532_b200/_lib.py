@@ -25,6 +25,7 @@ _llp = ctypes.POINTER(ctypes.c_longlong)
 SIGNATURES: dict[str, tuple] = {
     "sx_abi_version": (_c_int, []),
     "sx_last_error": (ctypes.c_char_p, []),
+    "sx_launch_count": (_c_ll, []),
     "sx_gemm_plan": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _ip, _ip, _llp]),
     "sx_gemm_bf16": (
         _c_int,
@@ -37,7 +38,7 @@ SIGNATURES: dict[str, tuple] = {
         _c_int,
         [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl, _vp, _vp],
     ),
-    "sx_tree_finalize": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "sx_tree_finalize": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sx_markov_rows": (
         _c_int,
         [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_ll, _vp],
@@ -55,6 +56,17 @@ SIGNATURES: dict[str, tuple] = {
     "sx_softmax_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _c_ll, _vp]),
     "sx_argmax_rows": (_c_int, [_vp, _c_int, _c_ll, _c_int, _c_int, _vp, _vp]),
     "sx_sample_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _vp]),
+    "sx_embed": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
+    "sx_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
+    "sx_rope_kv": (
+        _c_int,
+        [_vp, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_ll, _vp],
+    ),
+    "sx_tree_attention": (
+        _c_int,
+        [_vp, _vp, _vp, _c_ll, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp],
+    ),
+    "sx_kv_compact": (_c_int, [_vp, _vp, _c_int, _c_ll, _c_ll, _c_int, _vp, _vp, _c_int, _vp]),
 }
 
 ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1

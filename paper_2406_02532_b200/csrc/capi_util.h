@@ -31,8 +31,14 @@ int make_tmap_bf16_kmajor(CUtensorMap* out, const void* ptr, int64_t rows, int64
 
 }  // namespace sx
 
+namespace sx {
+// kernels launched through the C ABI since load (bench.py reports it as gpu_launches)
+void count_launch();
+}  // namespace sx
+
 #define SX_CHECK_LAUNCH(where)                                  \
   do {                                                          \
+    ::sx::count_launch();                                       \
     cudaError_t _e = cudaGetLastError();                        \
     if (_e != cudaSuccess) return ::sx::cuda_status(_e, where); \
   } while (0)

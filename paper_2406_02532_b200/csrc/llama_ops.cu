@@ -1,0 +1,158 @@
+// KE / KV3: the HBM-bound glue of the Llama-shaped forward used by the draft
+// (per tree round) and the target (one pass over the flattened tree):
+//   embed        x[t]  = float(E[token[t]])                         (fp32 residual stream)
+//   rmsnorm      y[t]  = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * w)
+//   rope_kv      rotate q/k (rotate-half convention, per-token position
+//                = len(anchor) - 1 + depth) and scatter K/V into the cache slots
+//   kv_compact   move the KV rows of the accepted path [root, accepted nodes...]
+//                to the committed region (no reference counterpart: the reference
+//                model API is stateless, pkg/src/speckit/models.py:43-52)
+// KV cache layout per layer: [KVH][slots][128] bf16 for K and for V.
+#include "capi_util.h"
+#include "common.cuh"
+#include "specexec_b200.h"
+
+namespace sx {
+
+__global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int* __restrict__ tokens, int n, int d,
+                             float* __restrict__ x) {
+  const int t = blockIdx.x;
+  if (t >= n) return;
+  const long long tok = tokens[t];
+  const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(E + tok * d);
+  float2* dst = reinterpret_cast<float2*>(x + (long long)t * d);
+  for (int i = threadIdx.x; i < d / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
+}
+
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w, int d, float eps,
+                               __nv_bfloat16* __restrict__ y) {
+  const int t = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + (long long)t * d);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)d + eps);
+  __nv_bfloat162* yr = reinterpret_cast<__nv_bfloat162*>(y + (long long)t * d);
+  const __nv_bfloat162* wr = reinterpret_cast<const __nv_bfloat162*>(w);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = xr[i];
+    const float2 w0 = __bfloat1622float2(wr[2 * i]);
+    const float2 w1 = __bfloat1622float2(wr[2 * i + 1]);
+    yr[2 * i] = __floats2bfloat162_rn(v.x * r * w0.x, v.y * r * w0.y);
+    yr[2 * i + 1] = __floats2bfloat162_rn(v.z * r * w1.x, v.w * r * w1.y);
+  }
+}
+
+// qkv [n, (H + 2*KVH) * 128] bf16 -> q [n, H, 128] (rotated), K/V cache rows at slot[t].
+// cos/sin tables [max_pos, 64] fp32.
+__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, const int* __restrict__ pos, int pos_base,
+                               const int* __restrict__ slot, int slot_base, int n, int H, int KVH,
+                               const float* __restrict__ cos_t,
+                               const float* __restrict__ sin_t, __nv_bfloat16* __restrict__ q,
+                               __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, long long slots) {
+  const int t = blockIdx.x;
+  const int heads = H + 2 * KVH;
+  const int p = pos_base + (pos ? pos[t] : t);
+  const long long s = slot_base + (slot ? slot[t] : t);
+  const __nv_bfloat16* row = qkv + (long long)t * heads * 128;
+  // one warp per head, each lane handles dims (lane, lane+32) and their +64 partners
+  for (int h = threadIdx.x >> 5; h < heads; h += blockDim.x >> 5) {
+    const int lane = threadIdx.x & 31;
+    const __nv_bfloat16* src = row + h * 128;
+    if (h < H + KVH) {
+      __nv_bfloat16* dst = h < H ? q + ((long long)t * H + h) * 128 : kc + ((long long)(h - H) * slots + s) * 128;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int d = lane + 32 * k;  // 0..63
+        const float c = cos_t[(long long)p * 64 + d], sn = sin_t[(long long)p * 64 + d];
+        const float x0 = __bfloat162float(src[d]), x1 = __bfloat162float(src[d + 64]);
+        dst[d] = __float2bfloat16(x0 * c - x1 * sn);
+        dst[d + 64] = __float2bfloat16(x1 * c + x0 * sn);
+      }
+    } else {
+      __nv_bfloat16* dst = vc + ((long long)(h - H - KVH) * slots + s) * 128;
+      reinterpret_cast<uint2*>(dst)[lane] = reinterpret_cast<const uint2*>(src)[lane];
+    }
+  }
+}
+
+// Move KV rows src_slot[i] -> dst_slot[i] for all layers / kv heads. Rows are
+// staged in shared memory first, so overlapping source/destination ranges are safe.
+__global__ void kv_compact_kernel(__nv_bfloat16* kc, __nv_bfloat16* vc, long long layer_stride, long long slots,
+                                  int KVH, const int* __restrict__ src, const int* __restrict__ dst, int n) {
+  extern __shared__ __align__(16) uint4 stage[];  // [2][n][16] uint4 (128 bf16 = 16 x uint4)
+  const int layer = blockIdx.y, h = blockIdx.x;
+  __nv_bfloat16* kb = kc + layer * layer_stride + (long long)h * slots * 128;
+  __nv_bfloat16* vb = vc + layer * layer_stride + (long long)h * slots * 128;
+  for (int i = threadIdx.x; i < n * 16; i += blockDim.x) {
+    const int r = i >> 4, c = i & 15;
+    stage[i] = reinterpret_cast<const uint4*>(kb + (long long)src[r] * 128)[c];
+    stage[n * 16 + i] = reinterpret_cast<const uint4*>(vb + (long long)src[r] * 128)[c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n * 16; i += blockDim.x) {
+    const int r = i >> 4, c = i & 15;
+    reinterpret_cast<uint4*>(kb + (long long)dst[r] * 128)[c] = stage[i];
+    reinterpret_cast<uint4*>(vb + (long long)dst[r] * 128)[c] = stage[n * 16 + i];
+  }
+}
+
+}  // namespace sx
+
+using namespace sx;
+
+extern "C" int sx_embed(const void* E, const int* tokens, int n, int d, float* x, cudaStream_t stream) {
+  if (n <= 0) return SX_OK;
+  if (d % 2) return arg_error("embed: d must be even");
+  embed_kernel<<<n, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(E), tokens, n, d, x);
+  SX_CHECK_LAUNCH("embed_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_rmsnorm(const float* x, const void* w, int n, int d, float eps, void* y, cudaStream_t stream) {
+  if (n <= 0) return SX_OK;
+  if (d % 4) return arg_error("rmsnorm: d must be a multiple of 4");
+  rmsnorm_kernel<<<n, 256, 0, stream>>>(x, reinterpret_cast<const __nv_bfloat16*>(w), d, eps,
+                                        reinterpret_cast<__nv_bfloat16*>(y));
+  SX_CHECK_LAUNCH("rmsnorm_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const int* slot, int slot_base, int n, int H,
+                          int KVH, const float* cos_t, const float* sin_t, void* q, void* kcache, void* vcache,
+                          long long slots, cudaStream_t stream) {
+  if (n <= 0) return SX_OK;
+  rope_kv_kernel<<<n, 512, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), pos, pos_base, slot, slot_base,
+                                        n, H, KVH, cos_t,
+                                        sin_t, reinterpret_cast<__nv_bfloat16*>(q),
+                                        reinterpret_cast<__nv_bfloat16*>(kcache),
+                                        reinterpret_cast<__nv_bfloat16*>(vcache), slots);
+  SX_CHECK_LAUNCH("rope_kv_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_kv_compact(void* kcache, void* vcache, int layers, long long layer_stride, long long slots, int KVH,
+                             const int* src, const int* dst, int n, cudaStream_t stream) {
+  if (n <= 0) return SX_OK;
+  if (n > 192) return arg_error("kv_compact: at most 192 rows per call (got %d)", n);
+  const size_t smem = (size_t)2 * n * 16 * sizeof(uint4);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kv_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kv_compact_kernel<<<dim3(KVH, layers), 256, smem, stream>>>(reinterpret_cast<__nv_bfloat16*>(kcache),
+                                                               reinterpret_cast<__nv_bfloat16*>(vcache), layer_stride,
+                                                               slots, KVH, src, dst, n);
+  SX_CHECK_LAUNCH("kv_compact_kernel");
+  return SX_OK;
+}

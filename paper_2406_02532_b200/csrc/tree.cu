@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     at<int>(ws, L.b_lex)[b] = lex[pos];
     at<int>(ws, L.b_slot)[b] = slot;
     at<int>(ws, L.b_token)[b] = lo_token(lo);
+    at<int>(ws, L.b_pos)[b] = c->root_slot + depth;
   }
   __syncthreads();
   // ancestor-slot lists, root first: [root_slot, slot(depth 1), ..., slot(self)]
@@ -522,8 +523,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
 // --------------------------------------------------------------------------
 // Final tables for the target pass over the tree: row 0 = root (anchor's last
 // token), row i+1 = node i. anc[row] = rows of the root path, root first, self last.
-__global__ void tree_final_kernel(uint8_t* ws, TreeLayout L, int* out_parent, int* out_token, double* out_edge,
-                                  int* out_depth) {
+__global__ void tree_final_kernel(uint8_t* ws, TreeLayout L, int root_token, int* out_parent, int* out_token,
+                                  double* out_edge, int* out_depth, int* out_slot) {
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int cur = c->cur, n = c->count;
   const int* par = at<int>(ws, L.m_parent[cur]);
@@ -539,6 +540,7 @@ __global__ void tree_final_kernel(uint8_t* ws, TreeLayout L, int* out_parent, in
       anc[0] = 0;
       f_len[0] = 1;
       f_depth[0] = 0;
+      f_tok[0] = root_token;
       continue;
     }
     const int i = r - 1;
@@ -556,6 +558,7 @@ __global__ void tree_final_kernel(uint8_t* ws, TreeLayout L, int* out_parent, in
     if (out_token) out_token[i] = lo_token(lo[i]);
     if (out_edge) out_edge[i] = edge[i];
     if (out_depth) out_depth[i] = depth;
+    if (out_slot) out_slot[i] = at<int>(ws, L.m_slot[cur])[i];
   }
 }
 
@@ -613,9 +616,8 @@ extern "C" long long sx_tree_workspace_bytes(int K, int B, int V, int D) {
 
 extern "C" int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n) {
   TreeLayout L = tree_layout(K, B, V, D);
-  const long long vals[] = {L.ctl,     L.b_node,  L.b_nll,   L.b_depth, L.b_lex,   L.b_slot,  L.b_token,
-                            L.b_anc,   L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows,
-                            L.total};
+  const long long vals[] = {L.ctl,   L.b_node,    L.b_nll, L.b_depth,   L.b_lex,   L.b_slot,  L.b_token, L.b_anc,
+                            L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows, L.b_pos, L.total};
   const int m = (int)(sizeof(vals) / sizeof(vals[0]));
   for (int i = 0; i < n && i < m; ++i) out[i] = vals[i];
   return m;
@@ -684,13 +686,13 @@ extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* r
   return SX_OK;
 }
 
-extern "C" int sx_tree_finalize(void* ws, int K, int B, int V, int D, int* out_parent, int* out_token,
-                                double* out_edge, int* out_depth, cudaStream_t stream) {
+extern "C" int sx_tree_finalize(void* ws, int K, int B, int V, int D, int root_token, int* out_parent, int* out_token,
+                                double* out_edge, int* out_depth, int* out_slot, cudaStream_t stream) {
   int st = check_tree_args(K, B, V, D);
   if (st) return st;
   TreeLayout L = tree_layout(K, B, V, D);
-  tree_final_kernel<<<(K + 256) / 256, 256, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, out_parent, out_token,
-                                                          out_edge, out_depth);
+  tree_final_kernel<<<(K + 256) / 256, 256, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, root_token, out_parent,
+                                                          out_token, out_edge, out_depth, out_slot);
   SX_CHECK_LAUNCH("tree_final_kernel");
   return SX_OK;
 }

@@ -28,7 +28,7 @@ struct TreeLayout {
   // byte offsets
   long long ctl;
   long long m_nll[2], m_lo[2], m_edge[2], m_parent[2], m_lex[2], m_slot[2];
-  long long b_node, b_nll, b_depth, b_lex, b_slot, b_token, b_anc, b_anc_len;
+  long long b_node, b_nll, b_depth, b_lex, b_slot, b_token, b_anc, b_anc_len, b_pos;
   long long s_nll, s_lo, s_edge, s_row;
   long long remap;
   long long r_max, r_sum;
@@ -73,6 +73,7 @@ __host__ __device__ inline TreeLayout tree_layout(int K, int B, int V, int D) {
   L.b_token = take(4LL * B);
   L.b_anc = take(4LL * B * (D + 1));
   L.b_anc_len = take(4LL * B);
+  L.b_pos = take(4LL * B);
   L.s_nll = take(8LL * L.cap);
   L.s_lo = take(8LL * L.cap);
   L.s_edge = take(8LL * L.cap);

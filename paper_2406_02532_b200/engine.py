@@ -167,43 +167,64 @@ def _max_walk(cache: ProbCache) -> int:
     return t.max_depth() - d0 + 1
 
 
+class SpecExecSession:
+    """Iteration-level driver of generate_specexec: each `step()` is one target
+    iteration (precompute if the previous token fell off the tree, then the
+    device walk until a miss or the token limit)."""
+
+    def __init__(self, prompt, draft, target, params: BuilderParams, cfg: SamplingConfig, warp_scores: bool = True):
+        if draft is target and hasattr(target, "commit_walk"):
+            raise ValueError("draft and target must be distinct model objects (separate KV caches)")
+        self.prompt = tuple(int(t) for t in prompt)
+        self.draft, self.target, self.params, self.cfg = draft, target, params, cfg
+        self.warp_scores = warp_scores
+        self.rng = CounterRng(cfg.seed, GENERATION_STREAM)
+        self.stats = GenStats()
+        self.tokens: list[int] = []
+        self.cache: ProbCache | None = None
+
+    def _precompute(self) -> ProbCache:
+        prefix = self.prompt + tuple(self.tokens)
+        # resolved through the module global (fault-injection tests monkeypatch it)
+        if self.warp_scores:
+            cache = precompute(prefix, self.draft, self.target, self.params, self.cfg)
+        else:
+            cache = precompute(prefix, self.draft, self.target, self.params, self.cfg, warp_scores=False)
+        self.stats.target_calls += 1
+        self.stats.draft_calls += cache.tree.rounds
+        self.stats.accepted_per_iteration.append(0)
+        return cache
+
+    def step(self, limit: int) -> list[int]:
+        """Emit up to `limit` tokens from one target iteration."""
+        if self.cache is None:
+            self.cache = self._precompute()
+        cache = self.cache
+        steps = min(limit, _max_walk(cache))
+        res = cache.walk(self.rng.peek(steps), self.cfg, steps)
+        self.rng.counter += len(res.tokens)
+        self.tokens.extend(res.tokens)
+        self.stats.accepted_per_iteration[-1] += len(res.tokens)
+        self.stats.tokens_generated = len(self.tokens)
+        if res.fell_off:
+            if hasattr(self.target, "commit_walk"):
+                self.target.commit_walk(cache, res)
+            if hasattr(self.draft, "commit_walk"):
+                self.draft.commit_walk(cache, res)
+            self.cache = None
+        return res.tokens
+
+
 def generate_specexec(prompt, draft, target, params: BuilderParams, cfg: SamplingConfig, warp_scores: bool = True):
     """Decode with the speculative cache; equal to `generate_sequential` (engine.py:92-131)."""
-    prompt = tuple(int(t) for t in prompt)
-    rng = CounterRng(cfg.seed, GENERATION_STREAM)
-    stats = GenStats()
-    tokens: list[int] = []
+    sess = SpecExecSession(prompt, draft, target, params, cfg, warp_scores)
     if cfg.max_new_tokens == 0:
-        return tokens, stats
-
-    def _pre(prefix):
-        if warp_scores:
-            return precompute(prefix, draft, target, params, cfg)
-        return precompute(prefix, draft, target, params, cfg, warp_scores=False)
-
-    cache = _pre(prompt)
-    stats.target_calls += 1
-    stats.draft_calls += cache.tree.rounds
-    stats.accepted_per_iteration.append(0)
-    while len(tokens) < cfg.max_new_tokens:
-        if cache is None:
-            cache = _pre(prompt + tuple(tokens))
-            stats.target_calls += 1
-            stats.draft_calls += cache.tree.rounds
-            stats.accepted_per_iteration.append(0)
-        steps = min(cfg.max_new_tokens - len(tokens), _max_walk(cache))
-        res = cache.walk(rng.peek(steps), cfg, steps)
-        rng.counter += len(res.tokens)
-        tokens.extend(res.tokens)
-        stats.accepted_per_iteration[-1] += len(res.tokens)
-        if res.fell_off:
-            if hasattr(target, "commit_walk"):
-                target.commit_walk(cache, res)
-            if hasattr(draft, "commit_walk") and draft is not target:
-                draft.commit_walk(cache, res)
-            cache = None
-    stats.tokens_generated = len(tokens)
-    return tokens, stats
+        return sess.tokens, sess.stats
+    sess.cache = sess._precompute()  # first iteration before the loop (engine.py:113-116)
+    while len(sess.tokens) < cfg.max_new_tokens:
+        sess.step(cfg.max_new_tokens - len(sess.tokens))
+    sess.stats.tokens_generated = len(sess.tokens)
+    return sess.tokens, sess.stats
 
 
 def generate_sequential(prompt, target, cfg: SamplingConfig):

@@ -26,6 +26,37 @@ __all__ = [
 
 _ws_cache: dict[tuple[int, int], torch.Tensor] = {}
 
+# host<->device bytes moved by the engine's control path (bench.py's e2e accounting)
+IO = {"h2d": 0, "d2h": 0}
+
+
+class GemmProfiler:
+    """Brackets every GEMM launch with CUDA events on the launching stream
+    (bench.py: achieved FLOP/s of the dominant kernel over the timed region)."""
+
+    def __init__(self):
+        self.rec: list[tuple[int, int, int, int, torch.cuda.Event, torch.cuda.Event]] = []
+        self._pool: list[torch.cuda.Event] = []
+
+    def event(self) -> torch.cuda.Event:
+        return self._pool.pop() if self._pool else torch.cuda.Event(enable_timing=True)
+
+    def summary(self, min_m: int = 0) -> dict:
+        torch.cuda.synchronize()
+        flops = 0.0
+        ms = 0.0
+        n = 0
+        for M, N, K, dual, e0, e1 in self.rec:
+            if M < min_m:
+                continue
+            flops += 2.0 * M * N * K * (2 if dual else 1)
+            ms += e0.elapsed_time(e1)
+            n += 1
+        return {"launches": n, "flops": flops, "ms": ms}
+
+
+PROFILER: GemmProfiler | None = None
+
 
 def _require_cuda(*ts: torch.Tensor) -> None:
     for t in ts:
@@ -76,6 +107,10 @@ def gemm(
         out = (torch.zeros if epi == EPI_ADD_F32 else torch.empty)((M, N), dtype=dt, device=x.device)
     _, _, ws_need = gemm_plan(M, N, K, w2 is not None, splits)
     ws = _workspace(ws_need, x.device)
+    prof = PROFILER
+    if prof is not None:
+        e0 = prof.event()
+        e0.record()
     call(
         "sx_gemm_bf16",
         ptr(w),
@@ -92,6 +127,10 @@ def gemm(
         splits,
         stream_ptr(),
     )
+    if prof is not None:
+        e1 = prof.event()
+        e1.record()
+        prof.rec.append((M, N, K, int(w2 is not None), e0, e1))
     return out
 
 
@@ -194,6 +233,8 @@ def verify_walk(rows: torch.Tensor, parent: torch.Tensor, token: torch.Tensor, n
         host = out_host[: out.numel()]
         host.copy_(out, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+    IO["h2d"] += 8 * max_steps
+    IO["d2h"] += 4 * out.numel()
     h = host.tolist()
     n = h[0]
     return WalkResult(h[3 : 3 + n], bool(h[1]), h[2], h[3 + max_steps : 3 + max_steps + n - (1 if h[1] else 0)])
@@ -204,7 +245,7 @@ def verify_walk(rows: torch.Tensor, parent: torch.Tensor, token: torch.Tensor, n
 # ---------------------------------------------------------------------------
 
 _OFF_NAMES = ["ctl", "b_node", "b_nll", "b_depth", "b_lex", "b_slot", "b_token", "b_anc", "b_anc_len",
-              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "total"]
+              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "b_pos", "total"]
 
 
 class TreeWorkspace:
@@ -259,6 +300,7 @@ class TreeWorkspace:
         _require_cuda(rows)
         call("sx_tree_round", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(rows), row_kind(rows), rows.stride(0),
              score_mode, float(temperature), float(top_p), self.ctl_host.data_ptr(), stream_ptr())
+        IO["d2h"] += 56
         torch.cuda.current_stream().synchronize()
         self.rounds += 1
         c = self.ctl_host.tolist()
@@ -266,14 +308,18 @@ class TreeWorkspace:
             raise RuntimeError("tree: survivor buffer overflow")
         return {"count": c[1], "has_thr": c[2], "slot_next": c[4], "batch_n": c[5]}
 
-    def finalize(self, n: int):
+    def batch_pos(self) -> torch.Tensor:
+        return self.view("b_pos", torch.int32, self.B)
+
+    def finalize(self, n: int, root_token: int = 0):
         parent = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         token = torch.empty_like(parent)
         depth = torch.empty_like(parent)
+        slot = torch.empty_like(parent)
         edge = torch.empty(max(n, 1), dtype=torch.float64, device=self.device)
-        call("sx_tree_finalize", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(parent), ptr(token), ptr(edge),
-             ptr(depth), stream_ptr())
-        return parent[:n], token[:n], edge[:n], depth[:n]
+        call("sx_tree_finalize", ptr(self.buf), self.K, self.B, self.V, self.D, int(root_token), ptr(parent), ptr(token),
+             ptr(edge), ptr(depth), ptr(slot), stream_ptr())
+        return parent[:n], token[:n], edge[:n], depth[:n], slot[:n]
 
 
 def markov_rows(table: torch.Tensor, order: int, ctx0: torch.Tensor, ws: TreeWorkspace, node_ids: torch.Tensor | None,

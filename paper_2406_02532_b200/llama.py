@@ -1,0 +1,401 @@
+"""Llama-shaped draft / target models on the B200 (device models for the engine).
+
+A `LlamaModel` is a `LanguageModel` plugin (pkg/src/speckit/models.py:32-63)
+whose forward runs entirely in hand-written sm_100a kernels through the C ABI:
+tcgen05 GEMMs for every projection (fused SwiGLU and residual epilogues),
+tree-masked attention with an explicit ancestor list per query, RMSNorm /
+RoPE / KV scatter, and the fp32 LM head. PyTorch only allocates memory.
+
+It keeps a KV cache and a prefix cache keyed by token ids ("committed" tokens
+whose KV sits in slots 0..c-1 at positions equal to their slots), so the
+stateless reference API -- next_distribution(prefix) -- and the engine's
+`precompute(prefix, ...)` reuse everything already computed for a shared
+prefix. After each walk, `commit_walk` moves the KV rows of the accepted path
+into the committed region (kv_compact); the draft also keeps the KV of every
+node it expanded while building the tree.
+
+Weights are random-init (N(0, std), RMSNorm = 1, untied) from a seed, in the
+named architecture's shapes; an optional *synthetic* prev-token bias (a shared
+low-rank table added to the logits of draft and target alike) and a logit scale
+make draft and target agree like a trained pair; it is off by
+default and always reported when on.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from .models import LanguageModel, _WS, _check_prefix
+from .tree import BuilderParams
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    vocab: int
+    d: int
+    layers: int
+    heads: int
+    kv_heads: int
+    ff: int
+    rope_theta: float = 10000.0
+    eps: float = 1e-5
+    head_dim: int = 128
+    name: str = "llama"
+
+    @property
+    def qkv_out(self) -> int:
+        return (self.heads + 2 * self.kv_heads) * self.head_dim
+
+    def n_params(self) -> int:
+        per_layer = self.qkv_out * self.d + self.d * self.heads * self.head_dim + 3 * self.d * self.ff + 2 * self.d
+        return self.layers * per_layer + 2 * self.vocab * self.d + self.d
+
+    def weight_bytes(self) -> int:
+        return 2 * self.n_params()
+
+    def kv_bytes_per_slot(self) -> int:
+        return self.layers * 2 * self.kv_heads * self.head_dim * 2
+
+
+PRESETS = {
+    "llama2-7b": LlamaConfig(32000, 4096, 32, 32, 32, 11008, 1e4, 1e-5, name="llama2-7b"),
+    "llama2-70b": LlamaConfig(32000, 8192, 80, 64, 8, 28672, 1e4, 1e-5, name="llama2-70b"),
+    "llama3-8b": LlamaConfig(128256, 4096, 32, 32, 8, 14336, 5e5, 1e-5, name="llama3-8b"),
+    "llama3-70b": LlamaConfig(128256, 8192, 80, 64, 8, 28672, 5e5, 1e-5, name="llama3-70b"),
+    # demo-sized (BASELINE config 1 restated): d=256, 4 layers, V=32000
+    "tiny": LlamaConfig(32000, 256, 4, 2, 1, 704, 1e4, 1e-5, name="tiny"),
+    "tiny-draft": LlamaConfig(32000, 256, 2, 2, 2, 512, 1e4, 1e-5, name="tiny-draft"),
+}
+
+
+@dataclass
+class SyntheticBias:
+    """Shared prev-token logit bias (low rank): logits[t] += scale * U[x_t] . W."""
+
+    seed: int = 1234
+    rank: int = 64
+    scale: float = 1.0
+
+
+def _rope_tables(cfg: LlamaConfig, max_pos: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    # HF Llama convention, computed in fp32
+    inv_freq = 1.0 / (cfg.rope_theta ** (torch.arange(0, cfg.head_dim, 2, dtype=torch.int64).float() / cfg.head_dim))
+    t = torch.arange(max_pos, dtype=torch.int64).float()
+    freqs = torch.outer(t, inv_freq)
+    return freqs.cos().contiguous().to(device), freqs.sin().contiguous().to(device)
+
+
+class LlamaWeights:
+    """Device-resident bf16 weights in nn.Linear layout ([out, in])."""
+
+    def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0):
+        self.cfg = cfg
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+
+        def rnd(*shape, s=std):
+            return torch.empty(shape, dtype=torch.bfloat16, device=device).normal_(0.0, s, generator=g)
+
+        self.emb = rnd(cfg.vocab, cfg.d)
+        self.layers = []
+        for _ in range(cfg.layers):
+            self.layers.append(
+                dict(
+                    wqkv=rnd(cfg.qkv_out, cfg.d),
+                    wo=rnd(cfg.d, cfg.heads * cfg.head_dim),
+                    wg=rnd(cfg.ff, cfg.d),
+                    wu=rnd(cfg.ff, cfg.d),
+                    wd=rnd(cfg.d, cfg.ff),
+                    n1=torch.ones(cfg.d, dtype=torch.bfloat16, device=device),
+                    n2=torch.ones(cfg.d, dtype=torch.bfloat16, device=device),
+                )
+            )
+        self.nf = torch.ones(cfg.d, dtype=torch.bfloat16, device=device)
+        self.lm = rnd(cfg.vocab, cfg.d, s=std * lm_scale)
+
+    def to_cpu_fp32(self) -> dict:
+        """fp32 CPU copy for the CPU reference forward (oracle/llama_ref.py)."""
+        f = lambda t: t.float().cpu()  # noqa: E731
+        return {
+            "emb": f(self.emb),
+            "layers": [{k: f(v) for k, v in L.items()} for L in self.layers],
+            "nf": f(self.nf),
+            "lm": f(self.lm),
+        }
+
+
+class _Buffers:
+    def __init__(self, cfg: LlamaConfig, n: int, device):
+        self.n = n
+        self.x = torch.empty((n, cfg.d), dtype=torch.float32, device=device)
+        self.h = torch.empty((n, cfg.d), dtype=torch.bfloat16, device=device)
+        self.qkv = torch.empty((n, cfg.qkv_out), dtype=torch.bfloat16, device=device)
+        self.q = torch.empty((n, cfg.heads * cfg.head_dim), dtype=torch.bfloat16, device=device)
+        self.att = torch.empty((n, cfg.heads * cfg.head_dim), dtype=torch.bfloat16, device=device)
+        self.act = torch.empty((n, cfg.ff), dtype=torch.bfloat16, device=device)
+        self.logits = torch.empty((n, cfg.vocab), dtype=torch.float32, device=device)
+        self.tok = torch.empty(n, dtype=torch.int32, device=device)
+        self.pos = torch.empty(n, dtype=torch.int32, device=device)
+
+
+class LlamaModel(LanguageModel):
+    """Llama-shaped model resident in HBM; a device model for the SpecExec engine."""
+
+    backend = "llama"
+
+    def __init__(
+        self,
+        cfg: LlamaConfig | str,
+        seed: int = 0,
+        max_ctx: int = 4096,
+        max_tokens: int = 1024,
+        std: float = 0.02,
+        lm_scale: float = 1.0,
+        synthetic: SyntheticBias | None = None,
+        device=None,
+    ):
+        if isinstance(cfg, str):
+            cfg = PRESETS[cfg]
+        if cfg.head_dim != 128:
+            raise ValueError("head_dim must be 128")
+        if not torch.cuda.is_available():
+            raise RuntimeError("LlamaModel needs a CUDA device; there is no CPU fallback")
+        _lib.load()
+        self.cfg = cfg
+        self.vocab_size = cfg.vocab
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.seed = seed
+        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale)
+        self.slots = max_ctx
+        self.kc = torch.zeros((cfg.layers, cfg.kv_heads, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
+        self.vc = torch.zeros_like(self.kc)
+        self.layer_stride = cfg.kv_heads * max_ctx * cfg.head_dim
+        self.cos, self.sin = _rope_tables(cfg, max_ctx + 64, self.device)
+        self.max_tokens = max_tokens
+        self.buf = _Buffers(cfg, max_tokens, self.device)
+        self.synthetic = synthetic
+        if synthetic is not None:
+            g = torch.Generator(device=self.device)
+            g.manual_seed(synthetic.seed)
+            self.bias_u = torch.empty((cfg.vocab, synthetic.rank), dtype=torch.bfloat16, device=self.device).normal_(
+                0.0, 1.0, generator=g)
+            self.bias_w = (torch.empty((cfg.vocab, synthetic.rank), dtype=torch.bfloat16, device=self.device)
+                           .normal_(0.0, 1.0, generator=g) * (synthetic.scale / math.sqrt(synthetic.rank))).bfloat16()
+            self.bias_in = torch.empty((max_tokens, synthetic.rank), dtype=torch.bfloat16, device=self.device)
+        self.committed: list[int] = []  # tokens whose KV is in slots [0, len)
+        self.record: list[dict] | None = None  # test hook: per build, prefix -> fp32 logits row
+        self.stats = {"forward_tokens": 0, "forwards": 0}
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, n: int, tokens: torch.Tensor, pos: torch.Tensor | None, pos_base: int, slot: torch.Tensor | None,
+                slot_base: int, dense_len: torch.Tensor | None, dense_const: int, anc: torch.Tensor | None,
+                anc_base: int, anc_len: torch.Tensor | None, A: int, logits_from: int | None) -> torch.Tensor | None:
+        """Run n tokens through the network; write their K/V into the cache.
+
+        Token t sits at position pos_base + pos[t] (pos None: t) and KV slot
+        slot_base + slot[t]; it attends slots [0, dense_len[t]) and the anc
+        list. Returns fp32 logits of rows [logits_from, n) (None: no LM head)."""
+        cfg, b, w = self.cfg, self.buf, self.w
+        if n > b.n:
+            raise ValueError(f"forward of {n} tokens exceeds max_tokens={b.n}")
+        st = _lib.stream_ptr()
+        x, h = b.x[:n], b.h[:n]
+        _lib.call("sx_embed", _lib.ptr(w.emb), _lib.ptr(tokens), n, cfg.d, _lib.ptr(x), st)
+        p = _lib.ptr
+        for li, L in enumerate(w.layers):
+            kc, vc = self.kc[li], self.vc[li]
+            _lib.call("sx_rmsnorm", p(x), p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
+            K.gemm(h, L["wqkv"], out=b.qkv[:n])
+            _lib.call("sx_rope_kv", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, cfg.heads, cfg.kv_heads,
+                      p(self.cos), p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
+            _lib.call("sx_tree_attention", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
+                      anc_base, p(anc_len), A, p(b.att), n, cfg.heads, cfg.kv_heads, st)
+            K.gemm(b.att[:n], L["wo"], out=x, epi=K.EPI_ADD_F32)
+            _lib.call("sx_rmsnorm", p(x), p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
+            K.gemm(h, L["wg"], out=b.act[:n], epi=K.EPI_SWIGLU_BF16, w2=L["wu"])
+            K.gemm(b.act[:n], L["wd"], out=x, epi=K.EPI_ADD_F32)
+        self.stats["forward_tokens"] += n
+        self.stats["forwards"] += 1
+        if logits_from is None:
+            return None
+        m = n - logits_from
+        hh = b.h[logits_from:n]
+        _lib.call("sx_rmsnorm", p(x[logits_from:]), p(w.nf), m, cfg.d, cfg.eps, p(hh), st)
+        logits = b.logits[:m]
+        K.gemm(hh, w.lm, out=logits, epi=K.EPI_F32)
+        if self.synthetic is not None:
+            bi = self.bias_in[:m]
+            torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)
+            K.gemm(bi, self.bias_w, out=logits, epi=K.EPI_ADD_F32)
+        return logits
+
+    # ---------------------------------------------------------- prefix cache
+    def _sync(self, prefix: tuple[int, ...]) -> tuple[int, list[int]]:
+        """Keep the longest committed prefix of `prefix[:-1]`; return (c, pending)
+        where pending = prefix[c:] (always non-empty; its last token is the root)."""
+        c = 0
+        lim = min(len(self.committed), len(prefix) - 1)
+        while c < lim and self.committed[c] == prefix[c]:
+            c += 1
+        del self.committed[c:]
+        return c, list(prefix[c:])
+
+    def _chain(self, c: int, toks: Sequence[int], want_logits: bool) -> torch.Tensor | None:
+        """Causal chain of tokens at slots/positions c.. (prefill, catch-up)."""
+        out = None
+        i = 0
+        step = self.buf.n
+        while i < len(toks):
+            chunk = toks[i : i + step]
+            n = len(chunk)
+            base = c + i
+            if base + n > self.slots:
+                raise RuntimeError(f"KV cache full ({self.slots} slots)")
+            tok = self.buf.tok[:n]
+            tok.copy_(torch.tensor(chunk, dtype=torch.int32), non_blocking=True)
+            K.IO["h2d"] += 8 * n
+            dl = self.buf.pos[:n]
+            dl.copy_(torch.arange(base + 1, base + n + 1, dtype=torch.int32), non_blocking=True)
+            last = i + n >= len(toks)
+            out = self.forward(n, tok, None, base, None, base, dl, 0, None, 0, None, 0,
+                               (n - 1) if (want_logits and last) else None)
+            i += n
+        self.committed.extend(int(t) for t in toks)
+        return out
+
+    def prefix_rows(self, prefix) -> torch.Tensor:
+        """fp32 logits [1, V] of the next token after `prefix` (commits the prefix)."""
+        prefix = _check_prefix(prefix, self.vocab_size)
+        if not prefix:
+            raise ValueError("empty prefix")
+        c, pending = self._sync(prefix)
+        return self._chain(c, pending, True)
+
+    def next_distributions(self, prefixes) -> np.ndarray:
+        rows = [K.softmax_rows(self.prefix_rows(p))[0].cpu().numpy() for p in prefixes]
+        if not rows:
+            return np.empty((0, self.vocab_size))
+        return np.stack(rows)
+
+    # -------------------------------------------------- device-model protocol
+    def tree_session(self, prefix, params: BuilderParams) -> "_LlamaDraftSession":
+        _check_prefix(prefix, self.vocab_size)
+        return _LlamaDraftSession(self, tuple(prefix), params)
+
+    def tree_rows(self, tree) -> torch.Tensor:
+        """ONE target pass over the anchor + every tree node: fp32 logits [n+1, V]."""
+        prefix = tree.prefix
+        c, pending = self._sync(prefix)
+        if len(pending) > 1:
+            self._chain(c, pending[:-1], False)
+            c += len(pending) - 1
+        n = len(tree.nodes) + 1
+        if c + n > self.slots:
+            raise RuntimeError(f"KV cache full: need {c + n} slots, have {self.slots}")
+        ws = tree.workspace
+        anc, anc_len, depth, tok = ws.final_tables(n)
+        logits = self.forward(n, tok, depth, c, None, c, None, c, anc, c, anc_len, ws.D + 1, 0)
+        self.committed.append(prefix[-1])  # the root's KV is at slot c = its position
+        tree.target_base = c
+        if self.record is not None:
+            rows = logits.cpu().numpy()
+            rec = {prefix: rows[0].copy()}
+            for node in tree.nodes:
+                rec[tree.full_prefix(node.node_id)] = rows[node.node_id + 1].copy()
+            self.record.append(rec)
+        return logits
+
+    def commit_walk(self, cache, res) -> None:
+        """Move the accepted path's KV into the committed region after a walk."""
+        tree = cache.tree
+        if getattr(cache, "target", None) is self and hasattr(tree, "target_base"):
+            c = tree.target_base
+            rows = [r for r in res.path_rows]
+            if rows:
+                src = torch.tensor([c + r for r in rows], dtype=torch.int32).to(self.device, non_blocking=True)
+                dst = torch.tensor([c + 1 + i for i in range(len(rows))], dtype=torch.int32).to(self.device,
+                                                                                                 non_blocking=True)
+                _lib.call("sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc), self.cfg.layers, self.layer_stride,
+                          self.slots, self.cfg.kv_heads, _lib.ptr(src), _lib.ptr(dst), len(rows), _lib.stream_ptr())
+                K.IO["h2d"] += 8 * len(rows)
+            self.committed.extend(tree.nodes[r - 1].token for r in rows)
+        elif getattr(tree, "draft_model", None) is self:
+            c = tree.draft_root_slot
+            slots = tree.host_slot
+            src, toks = [], []
+            for r in res.path_rows:
+                s = slots[r - 1]
+                if s < 0:
+                    break
+                src.append(s)
+                toks.append(tree.nodes[r - 1].token)
+            if src:
+                s_t = torch.tensor(src, dtype=torch.int32).to(self.device, non_blocking=True)
+                d_t = torch.tensor([c + 1 + i for i in range(len(src))], dtype=torch.int32).to(self.device,
+                                                                                                non_blocking=True)
+                _lib.call("sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc), self.cfg.layers, self.layer_stride,
+                          self.slots, self.cfg.kv_heads, _lib.ptr(s_t), _lib.ptr(d_t), len(src), _lib.stream_ptr())
+                K.IO["h2d"] += 8 * len(src)
+            self.committed.extend(toks)
+
+
+class _LlamaDraftSession:
+    """Feeds the GPU tree builder: round 1 = catch-up chain + root, later rounds
+    = the batch nodes with their ancestor KV slots (tree.py:282-296)."""
+
+    def __init__(self, model: LlamaModel, prefix: tuple[int, ...], params: BuilderParams):
+        self.m = model
+        self.prefix = prefix
+        self.ws = _WS.get(params.budget, params.batch_size, model.vocab_size, params.max_depth)
+        c, pending = model._sync(prefix)
+        self.c, self.pending = c, pending
+        self.root_slot = c + len(pending) - 1
+        self.ws.begin(root_slot=self.root_slot)
+        self.first = True
+        self.batch_n = 1
+        self.rec = None
+        if model.record is not None:  # replay-oracle hook: prefix -> fp32 logits of this build
+            self.rec = {}
+            self.slot_path = {self.root_slot: ()}
+            model.record.append(self.rec)
+
+    def batch_rows(self) -> torch.Tensor:
+        m = self.m
+        if self.first:
+            self.first = False
+            out = m._chain(self.c, self.pending, True)
+            if self.rec is not None:
+                self.rec[self.prefix] = out[0].cpu().numpy().copy()
+            return out
+        ws, n = self.ws, self.batch_n
+        out = m.forward(n, ws.batch_tokens()[:n], ws.batch_pos()[:n], 0, ws.batch_slots()[:n], 0, None, self.root_slot,
+                        ws.batch_anc()[:n], 0, ws.batch_anc_len()[:n], ws.D + 1, 0)
+        if self.rec is not None:
+            anc, alen = ws.batch_anc()[:n].cpu().tolist(), ws.batch_anc_len()[:n].cpu().tolist()
+            toks, slots = ws.batch_tokens()[:n].cpu().tolist(), ws.batch_slots()[:n].cpu().tolist()
+            rows = out.cpu().numpy()
+            for b in range(n):
+                path = self.slot_path[anc[b][alen[b] - 2]] + (toks[b],)
+                self.slot_path[slots[b]] = path
+                self.rec[self.prefix + path] = rows[b].copy()
+        return out
+
+    def advance(self, ctl) -> None:
+        self.batch_n = ctl["batch_n"]
+        if ctl["slot_next"] > self.m.slots:
+            raise RuntimeError(f"draft KV slots exhausted ({ctl['slot_next']} > {self.m.slots}); raise max_ctx")
+        if self.batch_n > self.m.buf.n:
+            raise RuntimeError("draft batch exceeds max_tokens")
+
+    def finish(self, tree) -> None:
+        tree.draft_model = self.m
+        tree.draft_root_slot = self.root_slot
+        tree.host_slot = tree.device_slot.cpu().tolist()
+        K.IO["d2h"] += 4 * len(tree.host_slot)

@@ -218,9 +218,13 @@ def build_sssp(
             break
         session.advance(ctl)
     n = ctl["count"]
-    parent, token, edge, depth = ws.finalize(n)
+    parent, token, edge, depth, slot = ws.finalize(n, prefix[-1] if prefix else 0)
     tree = _tree_from_device(prefix, parent.cpu(), token.cpu(), edge.cpu(), ws.rounds)
+    from .kernels import IO
+
+    IO["d2h"] += 16 * n
     tree.device_parent, tree.device_token, tree.workspace = parent, token, ws
     tree.device_depth = depth
+    tree.device_slot = slot
     session.finish(tree)
     return tree
