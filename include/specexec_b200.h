@@ -62,6 +62,8 @@ enum {
   SX_EPI_ADD_F32 = 2,     /* out fp32 += acc (residual stream)     */
   SX_EPI_SWIGLU_BF16 = 3  /* out bf16  = silu(acc(W)) * acc(W2)    */
 };
+/* 0 = auto (CTA-pair cta_group::2 tiles for M >= 256), 1 = single-CTA only, 2 = pair when legal */
+SX_API int sx_gemm_set_pair_mode(int mode);
 SX_API int sx_gemm_plan(int M, int N, int K, int dual, int splits_req, int* bn_out, int* splits_out,
                  long long* ws_floats_out);
 SX_API int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* out, float* ws, long long ws_floats,
@@ -84,7 +86,8 @@ enum { SX_ROWS_LOGITS_F32 = 0, SX_ROWS_PROBS_F64 = 1 };
 enum { SX_SCORE_RAW = 0, SX_SCORE_ARGMAX = 1, SX_SCORE_WARP = 2 };
 SX_API long long sx_tree_workspace_bytes(int K, int B, int V, int D);
 SX_API int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n);
-SX_API int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, cudaStream_t stream);
+SX_API int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, int pad_slot,
+                         cudaStream_t stream);
 SX_API int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
                          int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream);
 SX_API int sx_tree_finalize(void* ws, int K, int B, int V, int D, int root_token, int* out_parent, int* out_token,

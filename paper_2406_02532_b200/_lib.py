@@ -26,6 +26,7 @@ SIGNATURES: dict[str, tuple] = {
     "sx_abi_version": (_c_int, []),
     "sx_last_error": (ctypes.c_char_p, []),
     "sx_launch_count": (_c_ll, []),
+    "sx_gemm_set_pair_mode": (_c_int, [_c_int]),
     "sx_gemm_plan": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _ip, _ip, _llp]),
     "sx_gemm_bf16": (
         _c_int,
@@ -33,7 +34,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "sx_tree_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_int, _c_int]),
     "sx_tree_offsets": (_c_int, [_c_int, _c_int, _c_int, _c_int, _llp, _c_int]),
-    "sx_tree_begin": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "sx_tree_begin": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
     "sx_tree_round": (
         _c_int,
         [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl, _vp, _vp],

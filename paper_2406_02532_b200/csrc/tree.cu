@@ -50,7 +50,7 @@ SX_DEV bool key_less(unsigned long long ah, unsigned long long al, unsigned long
 }
 
 // --------------------------------------------------------------------------
-__global__ void tree_begin_kernel(uint8_t* ws, TreeLayout L, int root_slot) {
+__global__ void tree_begin_kernel(uint8_t* ws, TreeLayout L, int root_slot, int pad_slot) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   c->cur = 0;
@@ -61,6 +61,7 @@ __global__ void tree_begin_kernel(uint8_t* ws, TreeLayout L, int root_slot) {
   c->batch_n = 1;
   c->n_surv = 0;
   c->root_slot = root_slot;
+  c->pad_slot = pad_slot;
   c->err = 0;
   c->thr_nll = 0.0;
   c->thr_lo = 0ull;
@@ -506,6 +507,18 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     }
     anc[0] = c->root_slot;
     at<int>(ws, L.b_anc_len)[b] = depth + 1;
+    at<int>(ws, L.b_dense)[b] = c->root_slot;
+  }
+  // padded rows [batch_n, B): a fixed-shape draft forward (CUDA graph) may run
+  // them; they write only the scratch KV slot and see just the committed prefix
+  for (int b = batch_n + tid; b < L.B; b += kUpdThreads) {
+    at<int>(ws, L.b_node)[b] = -1;
+    at<int>(ws, L.b_token)[b] = 0;
+    at<int>(ws, L.b_pos)[b] = c->root_slot;
+    at<int>(ws, L.b_slot)[b] = c->pad_slot;
+    at<int>(ws, L.b_anc_len)[b] = 0;
+    at<int>(ws, L.b_anc)[b * (L.D + 1)] = c->pad_slot;
+    at<int>(ws, L.b_dense)[b] = c->root_slot;
   }
   __syncthreads();
   if (tid == 0) {
@@ -617,7 +630,7 @@ extern "C" long long sx_tree_workspace_bytes(int K, int B, int V, int D) {
 extern "C" int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n) {
   TreeLayout L = tree_layout(K, B, V, D);
   const long long vals[] = {L.ctl,   L.b_node,    L.b_nll, L.b_depth,   L.b_lex,   L.b_slot,  L.b_token, L.b_anc,
-                            L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows, L.b_pos, L.total};
+                            L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows, L.b_pos, L.b_dense, L.total};
   const int m = (int)(sizeof(vals) / sizeof(vals[0]));
   for (int i = 0; i < n && i < m; ++i) out[i] = vals[i];
   return m;
@@ -631,11 +644,11 @@ static int check_tree_args(int K, int B, int V, int D) {
   return SX_OK;
 }
 
-extern "C" int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, cudaStream_t stream) {
+extern "C" int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, int pad_slot, cudaStream_t stream) {
   int st = check_tree_args(K, B, V, D);
   if (st) return st;
   TreeLayout L = tree_layout(K, B, V, D);
-  tree_begin_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, root_slot);
+  tree_begin_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, root_slot, pad_slot);
   SX_CHECK_LAUNCH("tree_begin_kernel");
   return SX_OK;
 }

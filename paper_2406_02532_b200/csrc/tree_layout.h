@@ -17,7 +17,7 @@ struct TreeCtl {
   int n_surv;      // candidates appended by the scorer this round
   int root_slot;   // draft-KV slot of the root (anchor's last token)
   int err;         // 1 = survivor buffer overflow
-  int pad_;
+  int pad_slot;    // KV slot that padded batch rows (b >= batch_n) write to
   double thr_nll;
   unsigned long long thr_lo;
 };
@@ -28,7 +28,7 @@ struct TreeLayout {
   // byte offsets
   long long ctl;
   long long m_nll[2], m_lo[2], m_edge[2], m_parent[2], m_lex[2], m_slot[2];
-  long long b_node, b_nll, b_depth, b_lex, b_slot, b_token, b_anc, b_anc_len, b_pos;
+  long long b_node, b_nll, b_depth, b_lex, b_slot, b_token, b_anc, b_anc_len, b_pos, b_dense;
   long long s_nll, s_lo, s_edge, s_row;
   long long remap;
   long long r_max, r_sum;
@@ -74,6 +74,7 @@ __host__ __device__ inline TreeLayout tree_layout(int K, int B, int V, int D) {
   L.b_anc = take(4LL * B * (D + 1));
   L.b_anc_len = take(4LL * B);
   L.b_pos = take(4LL * B);
+  L.b_dense = take(4LL * B);
   L.s_nll = take(8LL * L.cap);
   L.s_lo = take(8LL * L.cap);
   L.s_edge = take(8LL * L.cap);

@@ -79,9 +79,14 @@ def _workspace(n_floats: int, device: torch.device) -> torch.Tensor | None:
     key = (device.index or 0, 0)
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < n_floats:
-        ws = torch.empty(max(n_floats, 1 << 20), dtype=torch.float32, device=device)
+        if ws is not None:
+            _keep_alive.append(ws)  # captured CUDA graphs may still point at it
+        ws = torch.empty(max(n_floats, 1 << 22), dtype=torch.float32, device=device)
         _ws_cache[key] = ws
     return ws
+
+
+_keep_alive: list[torch.Tensor] = []
 
 
 def gemm(
@@ -147,6 +152,8 @@ def scratch(nbytes: int, device: torch.device, tag: str) -> torch.Tensor:
     key = (device.index or 0, tag)
     buf = _scratch_cache.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            _keep_alive.append(buf)
         buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
         _scratch_cache[key] = buf
     return buf
@@ -245,7 +252,7 @@ def verify_walk(rows: torch.Tensor, parent: torch.Tensor, token: torch.Tensor, n
 # ---------------------------------------------------------------------------
 
 _OFF_NAMES = ["ctl", "b_node", "b_nll", "b_depth", "b_lex", "b_slot", "b_token", "b_anc", "b_anc_len",
-              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "b_pos", "total"]
+              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "b_pos", "b_dense", "total"]
 
 
 class TreeWorkspace:
@@ -291,15 +298,25 @@ class TreeWorkspace:
         return (anc, self.view("f_anc_len", torch.int32, self.K + 1)[:n_rows],
                 self.view("f_depth", torch.int32, self.K + 1)[:n_rows], self.view("f_token", torch.int32, self.K + 1)[:n_rows])
 
-    def begin(self, root_slot: int = 0) -> None:
-        self.rounds = 0
-        call("sx_tree_begin", ptr(self.buf), self.K, self.B, self.V, self.D, root_slot, stream_ptr())
+    def batch_dense(self) -> torch.Tensor:
+        return self.view("b_dense", torch.int32, self.B)
 
-    def round(self, rows: torch.Tensor, score_mode: int, temperature: float = 1.0, top_p: float = 1.0) -> dict:
-        """Score the current batch's rows, update the tree; returns the control block."""
+    def begin(self, root_slot: int = 0, pad_slot: int = 0) -> None:
+        self.rounds = 0
+        call("sx_tree_begin", ptr(self.buf), self.K, self.B, self.V, self.D, root_slot, pad_slot, stream_ptr())
+
+    def launch_round(self, rows: torch.Tensor, score_mode: int, temperature: float = 1.0, top_p: float = 1.0) -> None:
+        """Enqueue scoring + update + control-block readback (capturable in a CUDA graph)."""
         _require_cuda(rows)
         call("sx_tree_round", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(rows), row_kind(rows), rows.stride(0),
              score_mode, float(temperature), float(top_p), self.ctl_host.data_ptr(), stream_ptr())
+
+    def round(self, rows: torch.Tensor, score_mode: int, temperature: float = 1.0, top_p: float = 1.0) -> dict:
+        """Score the current batch's rows, update the tree; returns the control block."""
+        self.launch_round(rows, score_mode, temperature, top_p)
+        return self.read_ctl()
+
+    def read_ctl(self) -> dict:
         IO["d2h"] += 56
         torch.cuda.current_stream().synchronize()
         self.rounds += 1

@@ -149,6 +149,7 @@ class LlamaModel(LanguageModel):
     """Llama-shaped model resident in HBM; a device model for the SpecExec engine."""
 
     backend = "llama"
+    _serial = 0
 
     def __init__(
         self,
@@ -191,6 +192,9 @@ class LlamaModel(LanguageModel):
             self.bias_in = torch.empty((max_tokens, synthetic.rank), dtype=torch.bfloat16, device=self.device)
         self.committed: list[int] = []  # tokens whose KV is in slots [0, len)
         self.record: list[dict] | None = None  # test hook: per build, prefix -> fp32 logits row
+        self.use_graphs = True  # draft rounds as CUDA graphs (fixed B rows)
+        LlamaModel._serial += 1
+        self._uid = LlamaModel._serial
         self.stats = {"forward_tokens": 0, "forwards": 0}
 
     # ------------------------------------------------------------------ forward
@@ -357,7 +361,7 @@ class _LlamaDraftSession:
         c, pending = model._sync(prefix)
         self.c, self.pending = c, pending
         self.root_slot = c + len(pending) - 1
-        self.ws.begin(root_slot=self.root_slot)
+        self.ws.begin(root_slot=self.root_slot, pad_slot=model.slots - 1)
         self.first = True
         self.batch_n = 1
         self.rec = None
@@ -387,10 +391,63 @@ class _LlamaDraftSession:
                 self.rec[self.prefix + path] = rows[b].copy()
         return out
 
+    # -- fused round: fixed-shape draft forward over all B batch rows (rows past
+    # batch_n are padding that writes only the scratch slot) + scoring + update,
+    # replayed as one CUDA graph per (model, workspace, scoring mode).
+    def run_round(self, mode: int, temp: float, top_p: float) -> dict:
+        m, ws = self.m, self.ws
+        if self.first or not m.use_graphs or ws.B > m.buf.n:
+            rows = self.batch_rows()
+            return ws.round(rows, mode, temp, top_p)
+        snap = self._snapshot() if self.rec is not None else None
+        if not hasattr(ws, "_graphs"):
+            ws._graphs = {}
+        key = (m._uid, mode, temp, top_p)
+        g = ws._graphs.get(key)
+        if g is None:
+            if key not in getattr(ws, "_graph_warm", set()):
+                # one eager fixed-shape round first (sets kernel attributes, tensor maps, scratch)
+                ws._graph_warm = getattr(ws, "_graph_warm", set()) | {key}
+                self._fixed_forward()
+                ws.launch_round(m.buf.logits[: ws.B], mode, temp, top_p)
+                ctl = ws.read_ctl()
+                self._record(snap)
+                return ctl
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._fixed_forward()
+                ws.launch_round(m.buf.logits[: ws.B], mode, temp, top_p)
+            ws._graphs[key] = g
+        g.replay()
+        ctl = ws.read_ctl()
+        self._record(snap)
+        return ctl
+
+    def _snapshot(self):
+        ws, n = self.ws, self.batch_n
+        return (ws.batch_anc()[:n].cpu().tolist(), ws.batch_anc_len()[:n].cpu().tolist(),
+                ws.batch_tokens()[:n].cpu().tolist(), ws.batch_slots()[:n].cpu().tolist())
+
+    def _record(self, snap) -> None:
+        if snap is None:
+            return
+        anc, alen, toks, slots = snap
+        rows = self.m.buf.logits[: len(toks)].cpu().numpy()
+        for b in range(len(toks)):
+            path = self.slot_path[anc[b][alen[b] - 2]] + (toks[b],)
+            self.slot_path[slots[b]] = path
+            self.rec[self.prefix + path] = rows[b].copy()
+
+    def _fixed_forward(self) -> None:
+        ws, B = self.ws, self.ws.B
+        self.m.forward(B, ws.batch_tokens(), ws.batch_pos(), 0, ws.batch_slots(), 0, ws.batch_dense(), 0,
+                       ws.batch_anc(), 0, ws.batch_anc_len(), ws.D + 1, 0)
+
     def advance(self, ctl) -> None:
         self.batch_n = ctl["batch_n"]
-        if ctl["slot_next"] > self.m.slots:
-            raise RuntimeError(f"draft KV slots exhausted ({ctl['slot_next']} > {self.m.slots}); raise max_ctx")
+        if ctl["slot_next"] >= self.m.slots:
+            raise RuntimeError(f"draft KV slots exhausted ({ctl['slot_next']} >= {self.m.slots}); raise max_ctx")
         if self.batch_n > self.m.buf.n:
             raise RuntimeError("draft batch exceeds max_tokens")
 

@@ -211,9 +211,13 @@ def build_sssp(
     session = dm.tree_session(prefix, params)
     mode, temp, top_p = score_mode(warp, warp_scores)
     ws = session.ws
+    run_round = getattr(session, "run_round", None)
     while True:
-        rows = session.batch_rows()
-        ctl = ws.round(rows, mode, temp, top_p)
+        if run_round is not None:  # the session fuses draft forward + round (CUDA graph)
+            ctl = run_round(mode, temp, top_p)
+        else:
+            rows = session.batch_rows()
+            ctl = ws.round(rows, mode, temp, top_p)
         if ctl["batch_n"] == 0:
             break
         session.advance(ctl)

@@ -57,6 +57,32 @@ def test_gemm_swiglu_dual(cuda, M, splits):
     assert (y.float() - ref).abs().max().item() < 2e-2 * max(1.0, ref.abs().max().item())
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("M,N,Kd", [(256, 256, 64), (1025, 1280, 512), (300, 1000, 192), (64, 512, 256)])
+def test_gemm_pair_vs_single(cuda, mode, M, N, Kd):
+    from paper_2406_02532_b200 import _lib
+
+    _lib.call("sx_gemm_set_pair_mode", mode)
+    try:
+        g = torch.Generator(device=cuda).manual_seed(M + N)
+        x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+        w = (torch.randn(N, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+        w2 = (torch.randn(N, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+        ref = _ref(x, w)
+        y32 = K.gemm(x, w, epi=K.EPI_F32, splits=1)
+        resid = torch.randn(M, N, generator=g, device=cuda)
+        exp_r = resid + ref
+        K.gemm(x, w, out=resid, epi=K.EPI_ADD_F32, splits=1)
+        sw = K.gemm(x, w, epi=K.EPI_SWIGLU_BF16, w2=w2, splits=1)
+        torch.cuda.synchronize()
+        assert (y32 - ref).abs().max().item() < 1e-3 * Kd ** 0.5
+        assert (resid - exp_r).abs().max().item() < 1e-3 * Kd ** 0.5
+        ref_sw = torch.nn.functional.silu(ref) * _ref(x, w2)
+        assert (sw.float() - ref_sw).abs().max().item() < 2e-2 * max(1.0, ref_sw.abs().max().item())
+    finally:
+        _lib.call("sx_gemm_set_pair_mode", 0)
+
+
 def test_gemm_large_perf_smoke(cuda):
     # 70B-shaped projection over a K=1024 tree (N = K+1 = 1025 tokens).
     M, N, Kd = 1025, 8192, 8192
