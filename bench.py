@@ -31,8 +31,8 @@ sys.path.insert(0, str(ROOT))
 
 WORKLOADS = {
     # name: (draft preset, target preset, K, D, B, temperature, top_p)
-    "c2": ("llama2-7b", "llama2-70b", 1024, 16, 128, 0.0, 1.0),
-    "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 128, 0.0, 1.0),
+    "c2": ("llama2-7b", "llama2-70b", 1024, 16, 256, 0.0, 1.0),
+    "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 256, 0.0, 1.0),
     "tiny": ("tiny-draft", "tiny", 128, 16, 8, 0.0, 1.0),
 }
 

@@ -62,7 +62,7 @@ enum {
   SX_EPI_ADD_F32 = 2,     /* out fp32 += acc (residual stream)     */
   SX_EPI_SWIGLU_BF16 = 3  /* out bf16  = silu(acc(W)) * acc(W2)    */
 };
-/* 0 = auto (CTA-pair cta_group::2 tiles for M >= 256), 1 = single-CTA only, 2 = pair when legal */
+/* 0 = auto (CTA-pair cta_group::2 tiles for M >= 256), 1 = single-CTA only (default), 2 = pair when legal */
 SX_API int sx_gemm_set_pair_mode(int mode);
 SX_API int sx_gemm_plan(int M, int N, int K, int dual, int splits_req, int* bn_out, int* splits_out,
                  long long* ws_floats_out);

@@ -17,12 +17,18 @@
 // Accumulators are double-buffered in TMEM when they fit so the epilogue of one
 // tile overlaps the main loop of the next.
 //
+// Scheduling: whole output tiles round-robin over the CTAs when that fills the
+// machine evenly, otherwise STREAM-K: the (tile, k-block) iteration space is cut
+// into 148 equal contiguous ranges, one per CTA. A tile split across CTAs is
+// finished by the CTA holding its first k-block (the "owner", which reaches it
+// last); the others publish fp32 partials + a flag, and the owner adds them in
+// CTA order -- deterministic, no atomics on data. This removes the wave tail of
+// shapes like 320 tiles on 148 SMs (o / down projections at K+1 = 1025 tokens)
+// and replaces split-K for the weight-streaming draft shapes.
+//
 // Epilogues: bf16 store, fp32 store (logits), fp32 residual add, and a fused
 // SwiGLU "dual" mode where a second weight matrix (up-projection) is multiplied
 // into a second accumulator and the epilogue writes silu(gate) * up.
-// Split-K (for small-token, weight-streaming shapes that would otherwise leave
-// SMs idle) writes fp32 partials that `splitk_reduce` sums in a fixed order
-// (deterministic) before applying the same epilogue.
 #include "capi_util.h"
 #include "common.cuh"
 #include "specexec_b200.h"
@@ -32,7 +38,10 @@ namespace sx {
 struct GemmArgs {
   int M, Nf, K;
   int BN;
-  int tiles_f, tiles_t, splits, kb_per_split, kb_total, units;
+  int tiles_f, tiles_t, kb_total, tiles;
+  int streamk;      // 1: stream-K ranges, 0: whole tiles round-robin
+  long long work;   // tiles * kb_total
+  int ctas;         // grid size (stream-K partition count)
   int epi, dual, stages;
   uint32_t stage_bytes, a_bytes, b_bytes;
   uint32_t acc_cols;  // TMEM columns per accumulator buffer
@@ -40,64 +49,147 @@ struct GemmArgs {
   uint32_t tmem_cols;
   void* out;
   long long ldo;
-  float* ws;
+  int* flags;      // stream-K partial-ready flags [ctas]
+  float* part;     // stream-K partials [ctas][dual?2:1][BN][128]
+  int debug_no_tma;  // SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
 };
 
 constexpr int kGemmThreads = 192;
+constexpr int kFlagFloats = 1024;  // workspace prefix reserved for the stream-K flags
 
 SX_DEV float silu(float x) { return x / (1.0f + __expf(-x)); }
 
+// ---- work segments: (tile, kb0, kb1) in processing order for CTA c ----------
+struct SegIter {
+  long long pos, end;
+  int t, step;
+  bool sk;
+  SX_DEV SegIter(const GemmArgs& g, int c) {
+    sk = g.streamk;
+    if (sk) {
+      pos = (g.work * c) / g.ctas;
+      end = (g.work * (c + 1)) / g.ctas;
+    } else {
+      t = c;
+      step = g.ctas;
+    }
+  }
+  SX_DEV bool next(const GemmArgs& g, int& tile, int& kb0, int& kb1) {
+    if (sk) {
+      if (pos >= end) return false;
+      tile = (int)(pos / g.kb_total);
+      kb0 = (int)(pos % g.kb_total);
+      kb1 = (int)min((long long)g.kb_total, kb0 + (end - pos));
+      pos += kb1 - kb0;
+      return true;
+    }
+    if (t >= g.tiles) return false;
+    tile = t;
+    kb0 = 0;
+    kb1 = g.kb_total;
+    t += step;
+    return true;
+  }
+};
+
+SX_DEV long long sk_start(const GemmArgs& g, int c) { return (g.work * c) / g.ctas; }
+// CTA whose range contains linear k-block k
+SX_DEV int sk_cta_of(const GemmArgs& g, long long k) {
+  int c = (int)((k * g.ctas) / g.work);
+  while (c + 1 < g.ctas && sk_start(g, c + 1) <= k) ++c;
+  while (c > 0 && sk_start(g, c) > k) --c;
+  return c;
+}
+
+SX_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+SX_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SX_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+
+// Final epilogue of one 16-column chunk (values already summed over K).
+SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float (&v2)[16], int f, bool fok, int t0) {
+  if (g.epi == SX_EPI_BF16) {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + f] = __float2bfloat16(v[j]);
+  } else if (g.epi == SX_EPI_F32) {
+    float* o = reinterpret_cast<float*>(g.out);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + f] = v[j];
+  } else if (g.epi == SX_EPI_ADD_F32) {
+    float* o = reinterpret_cast<float*>(g.out);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + f] += v[j];
+  } else {  // SX_EPI_SWIGLU_BF16
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + f] = __float2bfloat16(silu(v[j]) * v2[j]);
+  }
+}
+
 // TMEM accumulator (this thread's lane = feature f, BN token columns) -> global.
-SX_DEV void epilogue_tile(const GemmArgs& g, uint32_t tbase, int f, bool fok, int tt, int split) {
+//   mode 0: whole tile          -> final epilogue
+//   mode 1: helper segment      -> fp32 partial in slot `slot`, then publish flag
+//   mode 2: owner of split tile -> add partials of CTAs [h0, h1] in order, final epilogue
+SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool fok, int tt, int mode, int slot,
+                         int h0, int h1) {
+  const long long pstride = (long long)(g.dual ? 2 : 1) * g.BN * 128;
+  if (mode == 2) {
+    if (threadIdx.x == 64)
+      for (int h = h0; h <= h1; ++h) {
+        while (ld_acquire(&g.flags[h]) == 0) {
+        }
+      }
+    epi_bar();
+  }
   for (int c = 0; c < g.BN; c += 16) {
     uint32_t r[16];
     uint32_t r2[16];
     tmem_ld16(tbase + c, r);
     if (g.dual) tmem_ld16(tbase + g.BN + c, r2);
     tmem_ld_wait();
-    const int t0 = tt * g.BN + c;
-    if (g.splits > 1) {
-      float* ws = g.ws + ((long long)split * (g.dual ? 2 : 1) * g.M) * g.Nf;
+    float v[16], v2[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      v[j] = __uint_as_float(r[j]);
+      v2[j] = g.dual ? __uint_as_float(r2[j]) : 0.f;
+    }
+    if (mode == 1) {
+      float* p = g.part + slot * pstride;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int t = t0 + j;
-        if (t < g.M && fok) {
-          ws[(long long)t * g.Nf + f] = __uint_as_float(r[j]);
-          if (g.dual) ws[((long long)g.M + t) * g.Nf + f] = __uint_as_float(r2[j]);
-        }
+        p[(long long)(c + j) * 128 + fl] = v[j];
+        if (g.dual) p[(long long)g.BN * 128 + (long long)(c + j) * 128 + fl] = v2[j];
       }
-    } else if (g.epi == SX_EPI_BF16) {
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
+      continue;
+    }
+    if (mode == 2) {
+      for (int h = h0; h <= h1; ++h) {
+        const float* p = g.part + h * pstride;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = t0 + j;
-        if (t < g.M && fok) o[(long long)t * g.ldo + f] = __float2bfloat16(__uint_as_float(r[j]));
-      }
-    } else if (g.epi == SX_EPI_F32) {
-      float* o = reinterpret_cast<float*>(g.out);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = t0 + j;
-        if (t < g.M && fok) o[(long long)t * g.ldo + f] = __uint_as_float(r[j]);
-      }
-    } else if (g.epi == SX_EPI_ADD_F32) {
-      float* o = reinterpret_cast<float*>(g.out);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = t0 + j;
-        if (t < g.M && fok) o[(long long)t * g.ldo + f] += __uint_as_float(r[j]);
-      }
-    } else {  // SX_EPI_SWIGLU_BF16
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = t0 + j;
-        if (t < g.M && fok) {
-          const float gv = __uint_as_float(r[j]);
-          o[(long long)t * g.ldo + f] = __float2bfloat16(silu(gv) * __uint_as_float(r2[j]));
+        for (int j = 0; j < 16; ++j) {
+          v[j] += __ldcg(p + (long long)(c + j) * 128 + fl);
+          if (g.dual) v2[j] += __ldcg(p + (long long)g.BN * 128 + (long long)(c + j) * 128 + fl);
         }
       }
     }
+    epilogue_store(g, v, v2, f, fok, tt * g.BN + c);
+  }
+  if (mode == 1) {
+    __threadfence();
+    epi_bar();
+    if (threadIdx.x == 64) st_release(&g.flags[slot], 1);
+  } else if (mode == 2) {
+    epi_bar();  // every thread finished reading the partials
+    if (threadIdx.x == 64)
+      for (int h = h0; h <= h1; ++h) g.flags[h] = 0;  // re-arm for the next launch / graph replay
   }
 }
 
@@ -115,6 +207,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  const int cta = blockIdx.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapA);
@@ -142,20 +235,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_w = policy_evict_first();  // weights stream through once per token tile group
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-        const int split = u % g.splits;
-        const int rest = u / g.splits;
-        const int tt = rest % g.tiles_t;
-        const int tf = rest / g.tiles_t;
-        const int kb0 = split * g.kb_per_split;
-        const int kb1 = min(g.kb_total, kb0 + g.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      int issued = 0;
+      SegIter it(g, cta);
+      int tile, kb0, kb1;
+      while (it.next(g, tile, kb0, kb1)) {
+        const int tt = tile % g.tiles_t;
+        const int tf = tile / g.tiles_t;
+        for (int kb = kb0; kb < kb1; ++kb, ++issued) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * g.stage_bytes;
-          mbar_arrive_expect_tx(&full_bar[stage], g.stage_bytes);
-          tma_load_2d_hint(sa, &mapA, &full_bar[stage], kb * 64, tf * 128, pol_w);
-          if (g.dual) tma_load_2d_hint(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, tf * 128, pol_w);
-          tma_load_2d(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64, tt * g.BN);
+          if (g.debug_no_tma && issued >= g.stages) {  // measurement mode: MMA on stale tiles
+            mbar_arrive(&full_bar[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], g.stage_bytes);
+            tma_load_2d_hint(sa, &mapA, &full_bar[stage], kb * 64, tf * 128, pol_w);
+            if (g.dual) tma_load_2d_hint(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, tf * 128, pol_w);
+            tma_load_2d(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64, tt * g.BN);
+          }
           if (++stage == g.stages) {
             stage = 0;
             phase ^= 1;
@@ -171,10 +267,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-        const int split = u % g.splits;
-        const int kb0 = split * g.kb_per_split;
-        const int kb1 = min(g.kb_total, kb0 + g.kb_per_split);
+      SegIter it(g, cta);
+      int tile, kb0, kb1;
+      while (it.next(g, tile, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * g.acc_cols;
@@ -208,19 +303,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int fl = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      const int split = u % g.splits;
-      const int rest = u / g.splits;
-      const int tt = rest % g.tiles_t;
-      const int tf = rest / g.tiles_t;
-      const int f = tf * 128 + quarter * 32 + lane;
+    SegIter it(g, cta);
+    int tile, kb0, kb1;
+    while (it.next(g, tile, kb0, kb1)) {
+      const int tt = tile % g.tiles_t;
+      const int tf = tile / g.tiles_t;
+      const int f = tf * 128 + fl;
       const bool fok = f < g.Nf;
+      int mode = 0, h0 = 0, h1 = -1;
+      if (kb0 > 0) {
+        mode = 1;  // helper: this CTA's range starts inside the tile
+      } else if (kb1 < g.kb_total) {
+        mode = 2;  // owner: the rest of the tile lives in the next CTA(s)
+        h0 = cta + 1;
+        h1 = sk_cta_of(g, (long long)tile * g.kb_total + g.kb_total - 1);
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_tile(g, tbase, f, fok, tt, split);
+      epilogue_seg(g, tbase, f, fl, fok, tt, mode, cta, h0, h1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -242,9 +346,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // ----------------------------------------------------------------------------
 // CTA-pair variant (tcgen05 cta_group::2, M = 256 features per pair): each CTA
 // stages its 128 weight rows and half of the BN token rows; the leader issues
-// the pair MMA, so every token tile fetched from L2 feeds 256 features instead
-// of 128 (operand traffic per FLOP drops ~1.5x: the single-CTA kernel is
-// L2-bandwidth bound at M = 128). Used for the compute-bound target pass.
+// the pair MMA. Kept behind sx_gemm_set_pair_mode(2): on B200 it measured ~7%
+// slower than the single-CTA kernel on every target-pass shape
+// (tools/gemm_micro3.py).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
                     const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
@@ -289,19 +393,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < g.units; u += npairs) {
-        const int rest = u / g.splits;
-        const int tt = rest % g.tiles_t;
-        const int tf = rest / g.tiles_t;
+      for (int u = pair; u < g.tiles; u += npairs) {
+        const int tt = u % g.tiles_t;
+        const int tf = u / g.tiles_t;
         for (int kb = 0; kb < g.kb_total; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * g.stage_bytes;
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * g.stage_bytes);
-          const int frow = tf * 256 + (int)rank * 128;
-          tma_load_2d_2sm(sa, &mapA, &full_bar[stage], kb * 64, frow, pol_w);
-          if (g.dual) tma_load_2d_2sm(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, frow, pol_w);
-          tma_load_2d_2sm(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64,
-                          tt * g.BN + (int)rank * half, pol_x);
+          if (g.debug_no_tma && kb >= g.stages) {
+            if (rank == 0) mbar_arrive(&full_bar[stage]);
+          } else {
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * g.stage_bytes);
+            const int frow = tf * 256 + (int)rank * 128;
+            tma_load_2d_2sm(sa, &mapA, &full_bar[stage], kb * 64, frow, pol_w);
+            if (g.dual) tma_load_2d_2sm(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, frow, pol_w);
+            tma_load_2d_2sm(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64,
+                            tt * g.BN + (int)rank * half, pol_x);
+          }
           if (++stage == g.stages) {
             stage = 0;
             phase ^= 1;
@@ -316,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = pair; u < g.units; u += npairs) {
+      for (int u = pair; u < g.tiles; u += npairs) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * g.acc_cols;
@@ -348,18 +455,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
+    const int fl = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < g.units; u += npairs) {
-      const int rest = u / g.splits;
-      const int tt = rest % g.tiles_t;
-      const int tf = rest / g.tiles_t;
-      const int f = tf * 256 + (int)rank * 128 + quarter * 32 + lane;
+    for (int u = pair; u < g.tiles; u += npairs) {
+      const int tt = u % g.tiles_t;
+      const int tf = u / g.tiles_t;
+      const int f = tf * 256 + (int)rank * 128 + fl;
       const bool fok = f < g.Nf;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_tile(g, tbase, f, fok, tt, 0);
+      epilogue_seg(g, tbase, f, fl, fok, tt, 0, 0, 0, -1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
@@ -379,36 +486,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-// Deterministic split-K reduction: partial planes are summed in split order,
-// then the epilogue of the GEMM is applied.
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, void* out, long long ldo, int M, int Nf,
-                                     int splits, int epi, int dual) {
-  const long long total = (long long)M * Nf;
-  const long long plane = (long long)(dual ? 2 : 1) * total;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(i / Nf);
-    const int f = (int)(i % Nf);
-    float s = 0.f, s2 = 0.f;
-    for (int k = 0; k < splits; ++k) {
-      s += ws[k * plane + i];
-      if (dual) s2 += ws[k * plane + total + i];
-    }
-    const long long o = (long long)t * ldo + f;
-    if (epi == SX_EPI_BF16) {
-      reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16(s);
-    } else if (epi == SX_EPI_F32) {
-      reinterpret_cast<float*>(out)[o] = s;
-    } else if (epi == SX_EPI_ADD_F32) {
-      reinterpret_cast<float*>(out)[o] += s;
-    } else {
-      reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16(silu(s) * s2);
-    }
-  }
-}
-
-// 0 = auto (pair for M >= 256), 1 = single-CTA only, 2 = pair whenever legal
-static int g_pair_mode = 0;
+// 0 = auto (pair for M >= 256), 1 = single-CTA only, 2 = pair whenever legal.
+// Default single: measured on B200 the pair kernel is ~7% slower on every
+// target-pass shape (tools/gemm_micro3.py).
+static int g_pair_mode = 1;
 
 // tuning overrides (read once): SX_GEMM_BN_CAP (token-tile cap), SX_GEMM_STAGES (max pipeline depth)
 static int env_int(const char* name, int dflt) {
@@ -432,6 +513,29 @@ static int pick_bn(int M, int cap) {
   return bn;
 }
 
+struct Plan {
+  int bn, tiles_f, tiles_t, tiles, kb_total, ctas, streamk;
+  long long ws_floats;
+};
+
+// sched_req: 1 = whole tiles only; otherwise auto (stream-K when whole-tile
+// waves would leave more than 5% of the CTA-slots idle).
+static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
+  Plan p{};
+  p.bn = pick_bn(M, dual ? 128 : bn_cap_single());
+  p.tiles_f = (Nf + 127) / 128;
+  p.tiles_t = (M + p.bn - 1) / p.bn;
+  p.tiles = p.tiles_f * p.tiles_t;
+  p.kb_total = K / 64;
+  const int waves = (p.tiles + kNumSMs - 1) / kNumSMs;
+  const double eff = (double)p.tiles / ((double)waves * kNumSMs);
+  p.streamk = (sched_req != 1 && eff < 0.95) ? 1 : 0;
+  p.ctas = p.streamk ? kNumSMs : (p.tiles < kNumSMs ? p.tiles : kNumSMs);
+  if (p.streamk && (long long)p.tiles * p.kb_total < p.ctas) p.ctas = (int)((long long)p.tiles * p.kb_total);
+  p.ws_floats = p.streamk ? kFlagFloats + (long long)p.ctas * (dual ? 2 : 1) * p.bn * 128 : 0;
+  return p;
+}
+
 }  // namespace sx
 
 using namespace sx;
@@ -446,24 +550,10 @@ extern "C" int sx_gemm_plan(int M, int Nf, int K, int dual, int splits_req, int*
                             long long* ws_floats_out) {
   if (M <= 0 || Nf <= 0 || K <= 0 || (K % 64) != 0)
     return arg_error("sx_gemm: need M,N > 0 and K a positive multiple of 64 (M=%d N=%d K=%d)", M, Nf, K);
-  const int bn = pick_bn(M, dual ? 128 : bn_cap_single());
-  const int tiles_t = (M + bn - 1) / bn;
-  const int tiles_f = (Nf + 127) / 128;
-  const int kb_total = K / 64;
-  int splits = splits_req;
-  if (splits <= 0) {
-    const int units = tiles_t * tiles_f;
-    splits = 1;
-    // weight-streaming shapes: split K until the grid covers the SMs,
-    // keeping at least 8 k-blocks (512 of K) per split.
-    while (units * splits < (kNumSMs * 3) / 4 && kb_total / (splits * 2) >= 8) splits *= 2;
-  }
-  if (splits > kb_total) splits = kb_total;
-  const int kps = (kb_total + splits - 1) / splits;
-  splits = (kb_total + kps - 1) / kps;
-  *bn_out = bn;
-  *splits_out = splits;
-  *ws_floats_out = splits > 1 ? (long long)splits * (dual ? 2 : 1) * M * (long long)Nf : 0;
+  Plan p = make_plan(M, Nf, K, dual, splits_req);
+  *bn_out = p.bn;
+  *splits_out = p.streamk ? p.ctas : 1;  // >1: number of stream-K ranges
+  *ws_floats_out = p.ws_floats;
   return SX_OK;
 }
 
@@ -474,23 +564,18 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   if (dual != (epi == SX_EPI_SWIGLU_BF16)) return arg_error("sx_gemm: SWIGLU epilogue needs W2 and vice versa");
   if (epi < 0 || epi > SX_EPI_SWIGLU_BF16) return arg_error("sx_gemm: bad epilogue %d", epi);
   if (ldo < Nf) return arg_error("sx_gemm: ldo (%lld) < N (%d)", ldo, Nf);
-  int bn, splits;
-  long long need;
-  int st = sx_gemm_plan(M, Nf, K, dual, splits_req, &bn, &splits, &need);
-  if (st) return st;
-  if (need > 0 && (ws == nullptr || ws_floats < need))
-    return arg_error("sx_gemm: split-K workspace needs %lld floats, got %lld", need, ws_floats);
+  if (M <= 0 || Nf <= 0 || K <= 0 || (K % 64) != 0)
+    return arg_error("sx_gemm: need M,N > 0 and K a positive multiple of 64 (M=%d N=%d K=%d)", M, Nf, K);
+  int st;
 
-  // CTA-pair (cta_group::2) path for the compute-bound shapes
-  const bool pair = splits == 1 && Nf >= 256 && (g_pair_mode == 2 || (g_pair_mode == 0 && M >= 256));
-  if (pair) bn = (pick_bn(M, dual ? 128 : bn_cap_single()) + 31) / 32 * 32;
-
-  CUtensorMap ma, ma2, mb;
-  if ((st = make_tmap_bf16_kmajor(&ma, W, Nf, K, K, 128))) return st;
-  if ((st = make_tmap_bf16_kmajor(&ma2, dual ? W2 : W, Nf, K, K, 128))) return st;
-  if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, pair ? bn / 2 : bn))) return st;
-
+  // CTA-pair (cta_group::2) path, opt-in
+  const bool pair = Nf >= 256 && (g_pair_mode == 2 || (g_pair_mode == 0 && M >= 256));
   if (pair) {
+    const int bn = (pick_bn(M, dual ? 128 : bn_cap_single()) + 31) / 32 * 32;
+    CUtensorMap ma, ma2, mb;
+    if ((st = make_tmap_bf16_kmajor(&ma, W, Nf, K, K, 128))) return st;
+    if ((st = make_tmap_bf16_kmajor(&ma2, dual ? W2 : W, Nf, K, K, 128))) return st;
+    if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, bn / 2))) return st;
     GemmArgs g{};
     g.M = M;
     g.Nf = Nf;
@@ -499,9 +584,7 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
     g.tiles_f = (Nf + 255) / 256;
     g.tiles_t = (M + bn - 1) / bn;
     g.kb_total = K / 64;
-    g.splits = 1;
-    g.kb_per_split = g.kb_total;
-    g.units = g.tiles_f * g.tiles_t;
+    g.tiles = g.tiles_f * g.tiles_t;
     g.epi = epi;
     g.dual = dual;
     g.a_bytes = 128 * 64 * 2;
@@ -516,47 +599,56 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
     g.tmem_cols = cols;
     g.out = out;
     g.ldo = ldo;
-    g.ws = nullptr;
+    g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
     const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + (2 * g.stages + 4) * 8 + 16;
     static bool attr2 = false;
     if (!attr2) {
       cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr2 = true;
     }
-    const int pairs = g.units < kNumSMs / 2 ? g.units : kNumSMs / 2;
+    const int pairs = g.tiles < kNumSMs / 2 ? g.tiles : kNumSMs / 2;
     gemm_tc2_kernel<<<2 * pairs, kGemmThreads, smem, stream>>>(ma, ma2, mb, g);
     SX_CHECK_LAUNCH("gemm_tc2_kernel");
     return SX_OK;
   }
 
+  Plan p = make_plan(M, Nf, K, dual, splits_req);
+  if (p.ws_floats > 0 && (ws == nullptr || ws_floats < p.ws_floats))
+    return arg_error("sx_gemm: stream-K workspace needs %lld floats, got %lld", p.ws_floats, ws_floats);
+  CUtensorMap ma, ma2, mb;
+  if ((st = make_tmap_bf16_kmajor(&ma, W, Nf, K, K, 128))) return st;
+  if ((st = make_tmap_bf16_kmajor(&ma2, dual ? W2 : W, Nf, K, K, 128))) return st;
+  if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, p.bn))) return st;
+
   GemmArgs g{};
   g.M = M;
   g.Nf = Nf;
   g.K = K;
-  g.BN = bn;
-  g.tiles_f = (Nf + 127) / 128;
-  g.tiles_t = (M + bn - 1) / bn;
-  g.kb_total = K / 64;
-  g.splits = splits;
-  g.kb_per_split = (g.kb_total + splits - 1) / splits;
-  g.units = g.tiles_f * g.tiles_t * splits;
+  g.BN = p.bn;
+  g.tiles_f = p.tiles_f;
+  g.tiles_t = p.tiles_t;
+  g.kb_total = p.kb_total;
+  g.tiles = p.tiles;
+  g.streamk = p.streamk;
+  g.work = (long long)p.tiles * p.kb_total;
+  g.ctas = p.ctas;
   g.epi = epi;
   g.dual = dual;
   g.a_bytes = 128 * 64 * 2;
-  g.b_bytes = bn * 64 * 2;
+  g.b_bytes = p.bn * 64 * 2;
   g.stage_bytes = (dual ? 2 : 1) * g.a_bytes + g.b_bytes;
-  const int smem_budget = 227 * 1024 - 1024 - 256;
-  g.stages = smem_budget / (int)g.stage_bytes;
+  g.stages = (227 * 1024 - 1024 - 256) / (int)g.stage_bytes;
   if (g.stages > max_stages()) g.stages = max_stages();
-  g.acc_cols = bn * (dual ? 2 : 1);
+  g.acc_cols = p.bn * (dual ? 2 : 1);
   g.acc_stages = (2 * g.acc_cols <= 512) ? 2 : 1;
-  uint32_t need_cols = g.acc_cols * g.acc_stages;
   uint32_t cols = 32;
-  while (cols < need_cols) cols <<= 1;
+  while (cols < g.acc_cols * (uint32_t)g.acc_stages) cols <<= 1;
   g.tmem_cols = cols;
   g.out = out;
   g.ldo = ldo;
-  g.ws = ws;
+  g.flags = p.streamk ? reinterpret_cast<int*>(ws) : nullptr;
+  g.part = p.streamk ? ws + kFlagFloats : nullptr;
+  g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
 
   const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + (2 * g.stages + 4) * 8 + 16;
   static bool attr_set = false;
@@ -564,15 +656,7 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  int grid = g.units < kNumSMs ? g.units : kNumSMs;
-  gemm_tc_kernel<<<grid, kGemmThreads, smem, stream>>>(ma, ma2, mb, g);
+  gemm_tc_kernel<<<g.ctas, kGemmThreads, smem, stream>>>(ma, ma2, mb, g);
   SX_CHECK_LAUNCH("gemm_tc_kernel");
-  if (splits > 1) {
-    long long total = (long long)M * Nf;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, out, ldo, M, Nf, splits, epi, dual);
-    SX_CHECK_LAUNCH("splitk_reduce_kernel");
-  }
   return SX_OK;
 }

@@ -81,7 +81,8 @@ def _workspace(n_floats: int, device: torch.device) -> torch.Tensor | None:
     if ws is None or ws.numel() < n_floats:
         if ws is not None:
             _keep_alive.append(ws)  # captured CUDA graphs may still point at it
-        ws = torch.empty(max(n_floats, 1 << 22), dtype=torch.float32, device=device)
+        # zero-filled: its prefix holds the stream-K partial-ready flags
+        ws = torch.zeros(max(n_floats, 1 << 22), dtype=torch.float32, device=device)
         _ws_cache[key] = ws
     return ws
 

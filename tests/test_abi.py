@@ -57,7 +57,14 @@ def test_gemm_plan_tiles():
     bn, sp, ws = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong()
     assert lib.sx_gemm_plan(1025, 8192, 8192, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
     assert bn.value % 16 == 0 and bn.value * ((1025 + bn.value - 1) // bn.value) < 1025 + 5 * 16
-    assert sp.value == 1
-    # a weight-streaming draft projection gets split-K to cover the SMs
+    # 64 x 5 = 320 tiles would leave a 2.16-wave tail on 148 SMs -> stream-K
+    assert sp.value == 148
+    # 224 x 9 = 2016 SwiGLU tiles fill 14 waves at 97% -> whole tiles
+    assert lib.sx_gemm_plan(1025, 28672, 8192, 1, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
+    assert sp.value == 1 and ws.value == 0
+    # a weight-streaming draft projection (32 tiles) is stream-K over all 148 SMs
     assert lib.sx_gemm_plan(64, 4096, 4096, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
-    assert sp.value > 1 and ws.value == sp.value * 64 * 4096
+    assert sp.value == 148 and ws.value == 1024 + 148 * 64 * 128
+    # ... unless whole tiles are requested
+    assert lib.sx_gemm_plan(64, 4096, 4096, 0, 1, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
+    assert sp.value == 1 and ws.value == 0
