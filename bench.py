@@ -284,6 +284,9 @@ def main():
         sess.step(max_new)
     # ---------------- timed region: exactly `steps` target iterations
     Kern.PROFILER = Kern.GemmProfiler()
+    from paper_2406_02532_b200 import engine as Eng
+
+    Eng.STAGES = Eng.StageTimer()
     launches0 = _lib.load().sx_launch_count()
     it0, tok0, dc0 = sess.stats.target_calls, len(sess.tokens), sess.stats.draft_calls
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -301,6 +304,8 @@ def main():
     barrier(world)
     launches = _lib.load().sx_launch_count() - launches0
     prof = Kern.PROFILER
+    stages = {k: v / args.steps for k, v in Eng.STAGES.totals().items()}
+    Eng.STAGES = None
     Kern.PROFILER = None
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms, world)
@@ -364,6 +369,7 @@ def main():
                        "prompt_len": args.prompt_len},
             "accepted_tokens_per_iter": accepted_per_iter,
             "draft_calls_per_iter": draft_calls / max(1, iters),
+            "stage_ms_per_step": stages,
             "roofline": roof,
             "cpu_baseline": cb,
             "e2e": e2e,

@@ -39,9 +39,12 @@ struct GemmArgs {
   int M, Nf, K;
   int BN;
   int tiles_f, tiles_t, kb_total, tiles;
-  int streamk;      // 1: stream-K ranges, 0: whole tiles round-robin
+  int streamk;      // 0: whole tiles round-robin, 1: stream-K ranges, 2: whole-tile waves + split tail
   long long work;   // tiles * kb_total
   int ctas;         // grid size (stream-K partition count)
+  int dp_rounds;    // mode 2: whole-tile rounds before the tail
+  int tail_tiles;   // mode 2: tiles left for the split tail
+  int tail_splits;  // mode 2: K-splits per tail tile
   int epi, dual, stages;
   uint32_t stage_bytes, a_bytes, b_bytes;
   uint32_t acc_cols;  // TMEM columns per accumulator buffer
@@ -62,11 +65,15 @@ SX_DEV float silu(float x) { return x / (1.0f + __expf(-x)); }
 // ---- work segments: (tile, kb0, kb1) in processing order for CTA c ----------
 struct SegIter {
   long long pos, end;
-  int t, step;
-  bool sk;
-  SX_DEV SegIter(const GemmArgs& g, int c) {
-    sk = g.streamk;
-    if (sk) {
+  int t, step, c, r;
+  int mode;
+  bool tail_done;
+  SX_DEV SegIter(const GemmArgs& g, int cta) {
+    mode = g.streamk;
+    c = cta;
+    r = 0;
+    tail_done = false;
+    if (mode == 1) {
       pos = (g.work * c) / g.ctas;
       end = (g.work * (c + 1)) / g.ctas;
     } else {
@@ -75,12 +82,28 @@ struct SegIter {
     }
   }
   SX_DEV bool next(const GemmArgs& g, int& tile, int& kb0, int& kb1) {
-    if (sk) {
+    if (mode == 1) {
       if (pos >= end) return false;
       tile = (int)(pos / g.kb_total);
       kb0 = (int)(pos % g.kb_total);
       kb1 = (int)min((long long)g.kb_total, kb0 + (end - pos));
       pos += kb1 - kb0;
+      return true;
+    }
+    if (mode == 2) {
+      if (r < g.dp_rounds) {  // whole tiles: in round r the CTAs cover tiles r*P .. r*P+P-1
+        tile = r * g.ctas + c;
+        kb0 = 0;
+        kb1 = g.kb_total;
+        ++r;
+        return true;
+      }
+      if (tail_done || c >= g.tail_tiles * g.tail_splits) return false;
+      tail_done = true;  // one tail item per CTA; all items run concurrently
+      const int j = c % g.tail_tiles, s = c / g.tail_tiles;
+      tile = g.dp_rounds * g.ctas + j;
+      kb0 = (int)((long long)g.kb_total * s / g.tail_splits);
+      kb1 = (int)((long long)g.kb_total * (s + 1) / g.tail_splits);
       return true;
     }
     if (t >= g.tiles) return false;
@@ -137,14 +160,14 @@ SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float 
 // TMEM accumulator (this thread's lane = feature f, BN token columns) -> global.
 //   mode 0: whole tile          -> final epilogue
 //   mode 1: helper segment      -> fp32 partial in slot `slot`, then publish flag
-//   mode 2: owner of split tile -> add partials of CTAs [h0, h1] in order, final epilogue
+//   mode 2: owner of split tile -> add partials of CTAs h0, h0+hs, ... (hn of them) in order
 SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool fok, int tt, int mode, int slot,
-                         int h0, int h1) {
+                         int h0, int hs, int hn) {
   const long long pstride = (long long)(g.dual ? 2 : 1) * g.BN * 128;
   if (mode == 2) {
     if (threadIdx.x == 64)
-      for (int h = h0; h <= h1; ++h) {
-        while (ld_acquire(&g.flags[h]) == 0) {
+      for (int i = 0; i < hn; ++i) {
+        while (ld_acquire(&g.flags[h0 + i * hs]) == 0) {
         }
       }
     epi_bar();
@@ -161,22 +184,39 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
       v[j] = __uint_as_float(r[j]);
       v2[j] = g.dual ? __uint_as_float(r2[j]) : 0.f;
     }
+    // partial layout per slot: [token/4][feature][4] floats -> one float4 per 4 tokens
     if (mode == 1) {
-      float* p = g.part + slot * pstride;
+      float4* p = reinterpret_cast<float4*>(g.part + slot * pstride) + (long long)(c >> 2) * 128 + fl;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        p[(long long)(c + j) * 128 + fl] = v[j];
-        if (g.dual) p[(long long)g.BN * 128 + (long long)(c + j) * 128 + fl] = v2[j];
+      for (int q = 0; q < 4; ++q) {
+        p[q * 128] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (g.dual)
+          p[(long long)g.BN * 32 + q * 128] = make_float4(v2[4 * q], v2[4 * q + 1], v2[4 * q + 2], v2[4 * q + 3]);
       }
       continue;
     }
     if (mode == 2) {
-      for (int h = h0; h <= h1; ++h) {
-        const float* p = g.part + h * pstride;
+      for (int i = 0; i < hn; ++i) {
+        const float4* p = reinterpret_cast<const float4*>(g.part + (h0 + i * hs) * pstride) +
+                          (long long)(c >> 2) * 128 + fl;
+        float4 a[4], b[4];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          v[j] += __ldcg(p + (long long)(c + j) * 128 + fl);
-          if (g.dual) v2[j] += __ldcg(p + (long long)g.BN * 128 + (long long)(c + j) * 128 + fl);
+        for (int q = 0; q < 4; ++q) {
+          a[q] = __ldcg(p + q * 128);
+          if (g.dual) b[q] = __ldcg(p + (long long)g.BN * 32 + q * 128);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[4 * q] += a[q].x;
+          v[4 * q + 1] += a[q].y;
+          v[4 * q + 2] += a[q].z;
+          v[4 * q + 3] += a[q].w;
+          if (g.dual) {
+            v2[4 * q] += b[q].x;
+            v2[4 * q + 1] += b[q].y;
+            v2[4 * q + 2] += b[q].z;
+            v2[4 * q + 3] += b[q].w;
+          }
         }
       }
     }
@@ -189,7 +229,7 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
   } else if (mode == 2) {
     epi_bar();  // every thread finished reading the partials
     if (threadIdx.x == 64)
-      for (int h = h0; h <= h1; ++h) g.flags[h] = 0;  // re-arm for the next launch / graph replay
+      for (int i = 0; i < hn; ++i) g.flags[h0 + i * hs] = 0;  // re-arm for the next launch / graph replay
   }
 }
 
@@ -313,18 +353,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int tf = tile / g.tiles_t;
       const int f = tf * 128 + fl;
       const bool fok = f < g.Nf;
-      int mode = 0, h0 = 0, h1 = -1;
+      int mode = 0, h0 = 0, hs = 1, hn = 0;
       if (kb0 > 0) {
-        mode = 1;  // helper: this CTA's range starts inside the tile
+        mode = 1;  // helper: publishes a partial for the tile's owner
       } else if (kb1 < g.kb_total) {
-        mode = 2;  // owner: the rest of the tile lives in the next CTA(s)
-        h0 = cta + 1;
-        h1 = sk_cta_of(g, (long long)tile * g.kb_total + g.kb_total - 1);
+        mode = 2;  // owner: the rest of the tile is summed by other CTAs
+        if (g.streamk == 1) {
+          h0 = cta + 1;
+          hn = sk_cta_of(g, (long long)tile * g.kb_total + g.kb_total - 1) - cta;
+        } else {
+          h0 = cta + g.tail_tiles;
+          hs = g.tail_tiles;
+          hn = g.tail_splits - 1;
+        }
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_seg(g, tbase, f, fl, fok, tt, mode, cta, h0, h1);
+      epilogue_seg(g, tbase, f, fl, fok, tt, mode, cta, h0, hs, hn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -466,7 +512,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_seg(g, tbase, f, fl, fok, tt, 0, 0, 0, -1);
+      epilogue_seg(g, tbase, f, fl, fok, tt, 0, 0, 0, 1, 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
@@ -515,24 +561,65 @@ static int pick_bn(int M, int cap) {
 
 struct Plan {
   int bn, tiles_f, tiles_t, tiles, kb_total, ctas, streamk;
+  int dp_rounds, tail_tiles, tail_splits;
   long long ws_floats;
 };
 
-// sched_req: 1 = whole tiles only; otherwise auto (stream-K when whole-tile
-// waves would leave more than 5% of the CTA-slots idle).
+// sched_req: 1 = whole tiles only, 2 = force stream-K ranges, 3 = force
+// whole-tile waves + split tail; otherwise auto:
+//  - whole tiles when the waves fill >= 95% of the CTA slots;
+//  - else, with several token tiles per weight tile, whole-tile waves plus a
+//    K-split tail (all tail items run together, so the token tiles of a weight
+//    tile still read the same k-range at the same time and share it in L2);
+//  - else (one token tile: every weight tile is read once anyway) stream-K.
 static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
   Plan p{};
   p.bn = pick_bn(M, dual ? 128 : bn_cap_single());
   p.tiles_f = (Nf + 127) / 128;
+  // Weight-streaming shapes with few weight tiles (e.g. a 4096-wide projection of
+  // the draft = 32 tiles): a single SM's TMA pulls only ~40-50 GB/s, so use
+  // narrower token tiles until ~120+ CTAs stream. The weight tile is shared by
+  // the token tiles through L2, HBM traffic is unchanged.
+  while (p.tiles_f * ((M + p.bn - 1) / p.bn) < 120 && p.bn > 32) {
+    const int half = ((p.bn / 2) + 15) / 16 * 16;
+    p.bn = pick_bn(M, half);
+  }
   p.tiles_t = (M + p.bn - 1) / p.bn;
   p.tiles = p.tiles_f * p.tiles_t;
   p.kb_total = K / 64;
-  const int waves = (p.tiles + kNumSMs - 1) / kNumSMs;
-  const double eff = (double)p.tiles / ((double)waves * kNumSMs);
-  p.streamk = (sched_req != 1 && eff < 0.95) ? 1 : 0;
-  p.ctas = p.streamk ? kNumSMs : (p.tiles < kNumSMs ? p.tiles : kNumSMs);
-  if (p.streamk && (long long)p.tiles * p.kb_total < p.ctas) p.ctas = (int)((long long)p.tiles * p.kb_total);
-  p.ws_floats = p.streamk ? kFlagFloats + (long long)p.ctas * (dual ? 2 : 1) * p.bn * 128 : 0;
+  const int P = kNumSMs;
+  const int waves = (p.tiles + P - 1) / P;
+  const double eff = (double)p.tiles / ((double)waves * P);
+  int mode = 0;
+  if (sched_req == 2 || sched_req == 3) {
+    mode = sched_req - 1;
+  } else if (sched_req != 1 && eff < 0.95 && p.tiles_t > 1) {
+    // (pure stream-K measured slower than whole tiles on the one-token-tile
+    // draft shapes, tools/gemm_bench.py --sched; it stays opt-in)
+    mode = 2;
+  }
+  if (mode == 2) {
+    p.dp_rounds = p.tiles / P;
+    p.tail_tiles = p.tiles - p.dp_rounds * P;
+    int s = p.tail_tiles > 0 ? P / p.tail_tiles : 1;
+    if (s > p.kb_total) s = p.kb_total;
+    if (s < 1) s = 1;
+    p.tail_splits = s;
+    if (p.tail_tiles == 0 || s == 1) mode = 0;  // nothing to balance
+    // the owner's fixup (reading s-1 partial tiles) must stay small next to a
+    // tail item: measured a loss at 21 k-blocks per item (o-proj), a gain at 64+
+    if (sched_req != 3 && p.kb_total / s < 48) mode = 0;
+  }
+  p.streamk = mode;
+  if (mode == 1) {
+    p.ctas = P;
+    if ((long long)p.tiles * p.kb_total < p.ctas) p.ctas = (int)((long long)p.tiles * p.kb_total);
+  } else if (mode == 2) {
+    p.ctas = p.dp_rounds > 0 ? P : p.tail_tiles * p.tail_splits;
+  } else {
+    p.ctas = p.tiles < P ? p.tiles : P;
+  }
+  p.ws_floats = mode ? kFlagFloats + (long long)p.ctas * (dual ? 2 : 1) * p.bn * 128 : 0;
   return p;
 }
 
@@ -632,6 +719,9 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   g.streamk = p.streamk;
   g.work = (long long)p.tiles * p.kb_total;
   g.ctas = p.ctas;
+  g.dp_rounds = p.dp_rounds;
+  g.tail_tiles = p.tail_tiles;
+  g.tail_splits = p.tail_splits;
   g.epi = epi;
   g.dual = dual;
   g.a_bytes = 128 * 64 * 2;

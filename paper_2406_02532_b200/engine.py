@@ -155,9 +155,39 @@ def precompute(
     over the anchor and every node (engine.py:73-89). `warp_scores=False`
     scores the tree with the raw draft distribution (SURVEY F2 builder flag)."""
     prefix = tuple(int(t) for t in prefix)
+    _mark("draft")
     tree = build_sssp(prefix, draft, params, warp, warp_scores)
+    _mark("target")
     rows = as_device_model(target).tree_rows(tree)
+    _mark("verify")
     return ProbCache(prefix, tree, rows, target)
+
+
+class StageTimer:
+    """CUDA events at stage boundaries on the current stream (bench.py breakdown)."""
+
+    def __init__(self):
+        self.marks: list[tuple[str, torch.cuda.Event]] = []
+
+    def mark(self, name: str) -> None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.marks.append((name, e))
+
+    def totals(self) -> dict[str, float]:
+        torch.cuda.synchronize()
+        out: dict[str, float] = {}
+        for (name, e0), (_, e1) in zip(self.marks, self.marks[1:]):
+            out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+        return out
+
+
+STAGES: StageTimer | None = None
+
+
+def _mark(name: str) -> None:
+    if STAGES is not None:
+        STAGES.mark(name)
 
 
 def _max_walk(cache: ProbCache) -> int:
@@ -212,6 +242,7 @@ class SpecExecSession:
             if hasattr(self.draft, "commit_walk"):
                 self.draft.commit_walk(cache, res)
             self.cache = None
+        _mark("host")
         return res.tokens
 
 

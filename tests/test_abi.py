@@ -57,14 +57,18 @@ def test_gemm_plan_tiles():
     bn, sp, ws = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong()
     assert lib.sx_gemm_plan(1025, 8192, 8192, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
     assert bn.value % 16 == 0 and bn.value * ((1025 + bn.value - 1) // bn.value) < 1025 + 5 * 16
-    # 64 x 5 = 320 tiles would leave a 2.16-wave tail on 148 SMs -> stream-K
-    assert sp.value == 148
+    # 64 x 5 = 320 tiles leave a 2.16-wave tail, but a 6-way split of 128 k-blocks
+    # is too short to amortise the fixup -> whole tiles; at K = 28672 -> split tail
+    assert sp.value == 1
+    assert lib.sx_gemm_plan(1025, 8192, 28672, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
+    assert sp.value == 148 and ws.value == 1024 + 148 * bn.value * 128
     # 224 x 9 = 2016 SwiGLU tiles fill 14 waves at 97% -> whole tiles
     assert lib.sx_gemm_plan(1025, 28672, 8192, 1, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
     assert sp.value == 1 and ws.value == 0
-    # a weight-streaming draft projection (32 tiles) is stream-K over all 148 SMs
+    # one token tile (draft shapes): whole tiles unless stream-K is requested (sched 2)
     assert lib.sx_gemm_plan(64, 4096, 4096, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
-    assert sp.value == 148 and ws.value == 1024 + 148 * 64 * 128
-    # ... unless whole tiles are requested
-    assert lib.sx_gemm_plan(64, 4096, 4096, 0, 1, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
     assert sp.value == 1 and ws.value == 0
+    assert lib.sx_gemm_plan(64, 4096, 4096, 0, 2, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
+    assert sp.value == 148 and ws.value == 1024 + 148 * bn.value * 128
+    # few weight tiles -> narrower token tiles so that enough SMs stream weights
+    assert bn.value == 32

@@ -83,6 +83,28 @@ def test_gemm_pair_vs_single(cuda, mode, M, N, Kd):
         _lib.call("sx_gemm_set_pair_mode", 0)
 
 
+@pytest.mark.parametrize("sched", [1, 2, 3, 0])
+@pytest.mark.parametrize("M,N,Kd,dual", [(1025, 8192, 1024, False), (1025, 4480, 512, True), (200, 3072, 2048, False),
+                                          (96, 1024, 4096, True)])
+def test_gemm_schedules_agree(cuda, sched, M, N, Kd, dual):
+    """whole tiles / stream-K / waves + split tail give the reference result;
+    repeated launches (re-armed stream-K flags) are bit-identical."""
+    g = torch.Generator(device=cuda).manual_seed(M * 3 + N)
+    x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+    w = (torch.randn(N, Kd, generator=g, device=cuda) * 0.04).bfloat16()
+    w2 = (torch.randn(N, Kd, generator=g, device=cuda) * 0.04).bfloat16() if dual else None
+    epi = K.EPI_SWIGLU_BF16 if dual else K.EPI_F32
+    a = K.gemm(x, w, epi=epi, w2=w2, splits=sched)
+    b = K.gemm(x, w, epi=epi, w2=w2, splits=sched)
+    ref = _ref(x, w)
+    if dual:
+        ref = torch.nn.functional.silu(ref) * _ref(x, w2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    tol = 2e-2 * max(1.0, ref.abs().max().item()) if dual else 1e-3 * Kd ** 0.5
+    assert (a.float() - ref).abs().max().item() < tol
+
+
 def test_gemm_large_perf_smoke(cuda):
     # 70B-shaped projection over a K=1024 tree (N = K+1 = 1025 tokens).
     M, N, Kd = 1025, 8192, 8192

@@ -17,6 +17,7 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 from paper_2406_02532_b200 import _lib  # noqa: E402
 from paper_2406_02532_b200 import kernels as K  # noqa: E402
 
+DRAFT_M = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--draft-m=")), 128))
 SHAPES = [
     # name, M (tokens), N (features), K, dual, epilogue
     ("70b.qkv", 1025, 10240, 8192, False, K.EPI_BF16),
@@ -24,11 +25,11 @@ SHAPES = [
     ("70b.gate_up", 1025, 28672, 8192, True, K.EPI_SWIGLU_BF16),
     ("70b.down", 1025, 8192, 28672, False, K.EPI_ADD_F32),
     ("70b.lm_head", 1025, 32000, 8192, False, K.EPI_F32),
-    ("7b.qkv", 128, 12288, 4096, False, K.EPI_BF16),
-    ("7b.o", 128, 4096, 4096, False, K.EPI_ADD_F32),
-    ("7b.gate_up", 128, 11008, 4096, True, K.EPI_SWIGLU_BF16),
-    ("7b.down", 128, 4096, 11008, False, K.EPI_ADD_F32),
-    ("7b.lm_head", 128, 32000, 4096, False, K.EPI_F32),
+    ("7b.qkv", DRAFT_M, 12288, 4096, False, K.EPI_BF16),
+    ("7b.o", DRAFT_M, 4096, 4096, False, K.EPI_ADD_F32),
+    ("7b.gate_up", DRAFT_M, 11008, 4096, True, K.EPI_SWIGLU_BF16),
+    ("7b.down", DRAFT_M, 4096, 11008, False, K.EPI_ADD_F32),
+    ("7b.lm_head", DRAFT_M, 32000, 4096, False, K.EPI_F32),
 ]
 
 
@@ -36,6 +37,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", type=int, default=0)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--sched", type=int, default=0, help="1 = whole tiles, 0 = auto (stream-K when waves are uneven)")
+    ap.add_argument("--draft-m", type=int, default=128)
     a = ap.parse_args()
     _lib.call("sx_gemm_set_pair_mode", a.mode)
     res = []
@@ -48,19 +51,19 @@ def main():
         dt = torch.float32 if epi in (K.EPI_F32, K.EPI_ADD_F32) else torch.bfloat16
         out = torch.zeros(M, N, dtype=dt, device="cuda")
         for i in range(3):
-            K.gemm(x, ws[i % len(ws)], out=out, epi=epi, w2=w2s[i % len(ws)] if dual else None)
+            K.gemm(x, ws[i % len(ws)], out=out, epi=epi, w2=w2s[i % len(ws)] if dual else None, splits=a.sched)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = 10
         s.record()
         for i in range(n):
-            K.gemm(x, ws[i % len(ws)], out=out, epi=epi, w2=w2s[i % len(ws)] if dual else None)
+            K.gemm(x, ws[i % len(ws)], out=out, epi=epi, w2=w2s[i % len(ws)] if dual else None, splits=a.sched)
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / n
         flops = 2.0 * M * N * Kd * (2 if dual else 1)
         wbytes = N * Kd * 2 * (2 if dual else 1)
         r = {"shape": name, "M": M, "N": N, "K": Kd, "dual": dual, "ms": ms, "tflops": flops / ms / 1e9,
-             "weight_gbs": wbytes / ms / 1e6, "plan": K.gemm_plan(M, N, Kd, dual)}
+             "weight_gbs": wbytes / ms / 1e6, "plan": K.gemm_plan(M, N, Kd, dual, a.sched)}
         res.append(r)
         print(f"{name:14s} M={M:5d} N={N:6d} K={Kd:6d} {ms:8.3f} ms {r['tflops']:7.1f} TFLOP/s "
               f"{r['weight_gbs']:7.0f} GB/s(weights) plan(bn,splits,ws)={r['plan']}")
