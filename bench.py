@@ -34,7 +34,11 @@ WORKLOADS = {
     "c2": ("llama2-7b", "llama2-70b", 1024, 16, 256, 0.0, 1.0),
     "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 256, 0.0, 1.0),
     "tiny": ("tiny-draft", "tiny", 128, 16, 8, 0.0, 1.0),
+    # C3: 70B target offloaded to pinned host RAM, streamed per layer; 7B draft resident
+    "c3": ("llama2-7b", "llama2-70b", 2048, 16, 256, 0.6, 0.9),
+    "tiny-offload": ("tiny-draft", "tiny", 128, 16, 8, 0.6, 0.9),
 }
+OFFLOAD = {"c3", "tiny-offload"}
 
 
 def parse():
@@ -46,7 +50,7 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--scoring", choices=["raw", "warped"], default="raw",
+    ap.add_argument("--scoring", choices=["raw", "warped"], default=None,
                     help="raw: score the tree with the draft's raw distribution (SURVEY F2); "
                          "warped: reference default (t=0 -> greedy chain)")
     ap.add_argument("--synthetic", type=float, default=0.0,
@@ -156,6 +160,23 @@ def barrier(world: int):
         import torch.distributed as dist
 
         dist.barrier()
+
+
+def measure_h2d(torch, nbytes: int = 1 << 30, reps: int = 5) -> float:
+    """Pinned host -> device copy bandwidth (GB/s) on this box (the host-link
+    roofline of the offloaded target; not in MEASURED_PEAKS.json)."""
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    dst.copy_(src, non_blocking=True)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    gbs = reps * nbytes / (s.elapsed_time(e) / 1e3) / 1e9
+    del src, dst
+    return gbs
 
 
 # ----------------------------------------------------------------------------- CPU baseline
@@ -268,14 +289,18 @@ def main():
     t_init = time.time()
     max_new = 100000
     ctx_cap = args.prompt_len + (args.warmup + args.steps) * (D + 1) * 3 + 64
-    target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn)
+    offload = args.workload in OFFLOAD
+    target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn,
+                        offload=offload)
     draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
                        synthetic=syn)
     torch.cuda.synchronize()
     init_s = time.time() - t_init
     params = sx.BuilderParams(K, D, B)
     cfg = sx.SamplingConfig(temp, top_p, seed=rank, max_new_tokens=max_new)
-    warp_scores = args.scoring == "warped"
+    scoring = args.scoring or ("raw" if temp == 0.0 else "warped")
+    warp_scores = scoring == "warped"
+    h2d_peak = measure_h2d(torch) if offload else None
     prompt = tuple(int(t) for t in np.random.default_rng(1000 + rank).integers(0, PRESETS[tname].vocab, size=args.prompt_len))
 
     sess = SpecExecSession(prompt, draft, target, params, cfg, warp_scores)
@@ -288,6 +313,7 @@ def main():
 
     Eng.STAGES = Eng.StageTimer()
     launches0 = _lib.load().sx_launch_count()
+    streamed0 = target.streamer.bytes if offload else 0
     it0, tok0, dc0 = sess.stats.target_calls, len(sess.tokens), sess.stats.draft_calls
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
@@ -330,6 +356,16 @@ def main():
             "flops_per_launch_avg": big["flops"] / max(1, big["launches"])}
 
     clk = clocks.summary()
+    if offload:
+        # stage 3 bound: host link. achieved = bytes streamed in the timed region / its device time
+        streamed = target.streamer.bytes - streamed0
+        h2d = streamed / (ms / 1e3) / 1e9
+        roof = {"bound": "h2d", "kernel": "per-layer weight streaming (sx_stream_copy, copy engines)", "achieved": h2d,
+                "peak": h2d_peak, "unit": "GB/s", "frac": h2d / h2d_peak if h2d_peak else None,
+                "peak_source": "pinned H2D measured in this run (1 GiB x5)", "traffic": None,
+                "bytes_per_step": streamed / args.steps,
+                "costsim_forward_s": PRESETS[tname].weight_bytes() / (h2d_peak * 1e9) if h2d_peak else None,
+                "gemm_target_pass_tflops": ach}
     # ---------------- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -363,7 +399,7 @@ def main():
             "data": "synthetic: random-init weights (N(0,0.02)), random 128-token prompt" +
                     (f", shared synthetic prev-token bias scale {args.synthetic}" if syn else ""),
             "config": {"workload": f"{args.workload}: {dname} draft + {tname} target, resident in HBM, K={K}, D={D}, "
-                                   f"B={B}, t={temp}, scoring={args.scoring}",
+                                   f"B={B}, t={temp}, scoring={scoring}" + (", target offloaded (per-layer H2D streaming)" if offload else "") + "",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)",
                        "prompt_len": args.prompt_len},

@@ -155,6 +155,14 @@ SX_API int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const int* 
 SX_API int sx_tree_attention(const void* q, const void* kcache, const void* vcache, long long slots,
                              const int* dense_len, int dense_const, const int* anc, int anc_base, const int* anc_len,
                              int A, void* out, int N, int H, int KVH, cudaStream_t stream);
+/* ------------------------------------------------ KS: weight streaming (stage 3)
+ * Async copy of `bytes` between pinned host memory and device memory on
+ * `stream` (to_device = 1: H2D), after waiting on `wait_event` (may be NULL) and
+ * recording `done_event` (may be NULL) -- the double-buffer handshake of the
+ * offloaded target (modelled by costsim.forward_time, pkg/src/speckit/costsim.py:59-65).
+ */
+SX_API int sx_stream_copy(void* dst, const void* src, long long bytes, int to_device, cudaStream_t stream,
+                          cudaEvent_t wait_event, cudaEvent_t done_event);
 SX_API int sx_kv_compact(void* kcache, void* vcache, int layers, long long layer_stride, long long slots, int KVH,
                          const int* src, const int* dst, int n, cudaStream_t stream);
 

@@ -582,7 +582,9 @@ static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
   // the token tiles through L2, HBM traffic is unchanged.
   while (p.tiles_f * ((M + p.bn - 1) / p.bn) < 120 && p.bn > 32) {
     const int half = ((p.bn / 2) + 15) / 16 * 16;
-    p.bn = pick_bn(M, half);
+    const int nb = pick_bn(M, half);
+    if (p.tiles_f * ((M + nb - 1) / nb) > kNumSMs) break;  // would spill into a second wave
+    p.bn = nb;
   }
   p.tiles_t = (M + p.bn - 1) / p.bn;
   p.tiles = p.tiles_f * p.tiles_t;

@@ -92,33 +92,66 @@ def _rope_tables(cfg: LlamaConfig, max_pos: int, device) -> tuple[torch.Tensor, 
     return freqs.cos().contiguous().to(device), freqs.sin().contiguous().to(device)
 
 
-class LlamaWeights:
-    """Device-resident bf16 weights in nn.Linear layout ([out, in])."""
+def layer_layout(cfg: LlamaConfig) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
+    """Byte offsets of one decoder layer's tensors in a contiguous buffer
+    (256-B aligned, the unit streamed in offload mode)."""
+    shapes = {
+        "wqkv": (cfg.qkv_out, cfg.d),
+        "wo": (cfg.d, cfg.heads * cfg.head_dim),
+        "wg": (cfg.ff, cfg.d),
+        "wu": (cfg.ff, cfg.d),
+        "wd": (cfg.d, cfg.ff),
+        "n1": (cfg.d,),
+        "n2": (cfg.d,),
+    }
+    out, off = {}, 0
+    for k, shp in shapes.items():
+        out[k] = (off, shp)
+        off += (math.prod(shp) * 2 + 255) // 256 * 256
+    return out, off
 
-    def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0):
+
+def layer_views(buf: torch.Tensor, layout) -> dict[str, torch.Tensor]:
+    return {k: buf[o : o + math.prod(s) * 2].view(torch.bfloat16).view(s) for k, (o, s) in layout.items()}
+
+
+class LlamaWeights:
+    """bf16 weights in nn.Linear layout ([out, in]); each decoder layer is one
+    contiguous buffer -- in HBM, or (offload) in pinned host memory."""
+
+    def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0,
+                 offload: bool = False):
         self.cfg = cfg
+        self.offload = offload
         g = torch.Generator(device=device)
         g.manual_seed(seed)
 
-        def rnd(*shape, s=std):
-            return torch.empty(shape, dtype=torch.bfloat16, device=device).normal_(0.0, s, generator=g)
+        def rnd_(t, s=std):
+            return t.normal_(0.0, s, generator=g)
 
-        self.emb = rnd(cfg.vocab, cfg.d)
+        self.emb = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device))
+        self.layout, self.layer_bytes = layer_layout(cfg)
+        self.layer_bufs: list[torch.Tensor] = []
         self.layers = []
+        tmp = torch.empty(self.layer_bytes, dtype=torch.uint8, device=device) if offload else None
         for _ in range(cfg.layers):
-            self.layers.append(
-                dict(
-                    wqkv=rnd(cfg.qkv_out, cfg.d),
-                    wo=rnd(cfg.d, cfg.heads * cfg.head_dim),
-                    wg=rnd(cfg.ff, cfg.d),
-                    wu=rnd(cfg.ff, cfg.d),
-                    wd=rnd(cfg.d, cfg.ff),
-                    n1=torch.ones(cfg.d, dtype=torch.bfloat16, device=device),
-                    n2=torch.ones(cfg.d, dtype=torch.bfloat16, device=device),
-                )
-            )
+            buf = tmp if offload else torch.empty(self.layer_bytes, dtype=torch.uint8, device=device)
+            v = layer_views(buf, self.layout)
+            for k in ("wqkv", "wo", "wg", "wu", "wd"):  # same draw order as the resident model
+                rnd_(v[k])
+            v["n1"].fill_(1.0)
+            v["n2"].fill_(1.0)
+            if offload:
+                host = torch.empty(self.layer_bytes, dtype=torch.uint8, pin_memory=True)
+                host.copy_(buf)
+                self.layer_bufs.append(host)
+                self.layers.append(layer_views(host, self.layout))
+            else:
+                self.layer_bufs.append(buf)
+                self.layers.append(v)
+        del tmp
         self.nf = torch.ones(cfg.d, dtype=torch.bfloat16, device=device)
-        self.lm = rnd(cfg.vocab, cfg.d, s=std * lm_scale)
+        self.lm = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device), std * lm_scale)
 
     def to_cpu_fp32(self) -> dict:
         """fp32 CPU copy for the CPU reference forward (oracle/llama_ref.py)."""
@@ -129,6 +162,56 @@ class LlamaWeights:
             "nf": f(self.nf),
             "lm": f(self.lm),
         }
+
+
+class LayerStreamer:
+    """Stage 3: double-buffered per-layer weight streaming from pinned host RAM.
+
+    Copies run on a dedicated stream (copy engines) through sx_stream_copy; the
+    k-th copy lands in staging buffer k % nbuf after the compute stream released
+    it. Layers are issued in cyclic order, so finishing layer L-1 of one pass
+    immediately starts loading layers 0..nbuf-1 of the next pass -- they stream
+    in while the draft builds the next tree (the paper's prefetch)."""
+
+    def __init__(self, weights: LlamaWeights, device, nbuf: int = 2):
+        self.w = weights
+        self.L = weights.cfg.layers
+        self.nbuf = nbuf
+        self.stream = torch.cuda.Stream(device)
+        self.bufs = [torch.empty(weights.layer_bytes, dtype=torch.uint8, device=device) for _ in range(nbuf)]
+        self.views = [layer_views(b, weights.layout) for b in self.bufs]
+        self.ready = [torch.cuda.Event() for _ in range(nbuf)]
+        self.free = [torch.cuda.Event() for _ in range(nbuf)]
+        for e in self.ready + self.free:  # materialise the event handles
+            e.record(self.stream)
+        self.pending: list[tuple[int, int]] = []  # (layer, buffer) copies issued, FIFO
+        self.k = 0
+        self.next_layer = 0
+        self.bytes = 0
+        torch.cuda.synchronize(device)
+
+    def _issue(self) -> None:
+        li, b = self.next_layer, self.k % self.nbuf
+        _lib.call("sx_stream_copy", _lib.ptr(self.bufs[b]), self.w.layer_bufs[li].data_ptr(), self.w.layer_bytes, 1,
+                  int(self.stream.cuda_stream), self.free[b].cuda_event, self.ready[b].cuda_event)
+        self.pending.append((li, b))
+        self.bytes += self.w.layer_bytes
+        self.k += 1
+        self.next_layer = (li + 1) % self.L
+
+    def acquire(self, li: int) -> dict[str, torch.Tensor]:
+        while len(self.pending) < self.nbuf:
+            self._issue()
+        layer, b = self.pending[0]
+        if layer != li:
+            raise RuntimeError(f"layer streamer out of order: expected {layer}, got {li}")
+        torch.cuda.current_stream().wait_event(self.ready[b])
+        return self.views[b]
+
+    def release(self, li: int) -> None:
+        _, b = self.pending.pop(0)
+        self.free[b].record(torch.cuda.current_stream())
+        self._issue()  # refill the freed buffer with the next layer in cyclic order
 
 
 class _Buffers:
@@ -161,6 +244,7 @@ class LlamaModel(LanguageModel):
         lm_scale: float = 1.0,
         synthetic: SyntheticBias | None = None,
         device=None,
+        offload: bool = False,
     ):
         if isinstance(cfg, str):
             cfg = PRESETS[cfg]
@@ -173,7 +257,8 @@ class LlamaModel(LanguageModel):
         self.vocab_size = cfg.vocab
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.seed = seed
-        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale)
+        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload)
+        self.streamer = LayerStreamer(self.w, self.device) if offload else None
         self.slots = max_ctx
         self.kc = torch.zeros((cfg.layers, cfg.kv_heads, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
         self.vc = torch.zeros_like(self.kc)
@@ -213,7 +298,8 @@ class LlamaModel(LanguageModel):
         x, h = b.x[:n], b.h[:n]
         _lib.call("sx_embed", _lib.ptr(w.emb), _lib.ptr(tokens), n, cfg.d, _lib.ptr(x), st)
         p = _lib.ptr
-        for li, L in enumerate(w.layers):
+        for li in range(cfg.layers):
+            L = self.streamer.acquire(li) if self.streamer is not None else w.layers[li]
             kc, vc = self.kc[li], self.vc[li]
             _lib.call("sx_rmsnorm", p(x), p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
             K.gemm(h, L["wqkv"], out=b.qkv[:n])
@@ -225,6 +311,8 @@ class LlamaModel(LanguageModel):
             _lib.call("sx_rmsnorm", p(x), p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
             K.gemm(h, L["wg"], out=b.act[:n], epi=K.EPI_SWIGLU_BF16, w2=L["wu"])
             K.gemm(b.act[:n], L["wd"], out=x, epi=K.EPI_ADD_F32)
+            if self.streamer is not None:
+                self.streamer.release(li)
         self.stats["forward_tokens"] += n
         self.stats["forwards"] += 1
         if logits_from is None:

@@ -139,3 +139,19 @@ def test_specexec_equals_sequential_greedy(pair):
     got, _ = sx.generate_specexec(prompt, draft, target, sx.BuilderParams(64, 8, 16), cfg, warp_scores=False)
     seq, _ = sx.generate_sequential(prompt, target, cfg)
     assert got == seq
+
+
+def test_offloaded_target_matches_resident(pair):
+    """Stage 3: the same weights streamed per layer from pinned host memory give
+    bit-identical logits and tokens (same kernels, same order of operations)."""
+    draft, _ = pair
+    syn = SyntheticBias(seed=7, rank=64, scale=4.0)
+    res = LlamaModel("tiny", seed=11, max_ctx=2048, max_tokens=512, synthetic=syn)
+    off = LlamaModel("tiny", seed=11, max_ctx=2048, max_tokens=512, synthetic=syn, offload=True)
+    prefix = tuple(range(300, 340))
+    assert torch.equal(res.prefix_rows(prefix), off.prefix_rows(prefix))
+    cfg = sx.SamplingConfig(0.6, 0.9, seed=5, max_new_tokens=30)
+    a, sa = sx.generate_specexec((5, 6, 7, 8), draft, res, sx.BuilderParams(64, 8, 16), cfg)
+    b, sb = sx.generate_specexec((5, 6, 7, 8), draft, off, sx.BuilderParams(64, 8, 16), cfg)
+    assert a == b and sa.accepted_per_iteration == sb.accepted_per_iteration
+    assert off.streamer.bytes >= off.w.layer_bytes * off.cfg.layers * sb.target_calls
