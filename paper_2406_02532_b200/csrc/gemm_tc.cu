@@ -55,6 +55,9 @@ struct GemmArgs {
   int* flags;      // stream-K partial-ready flags [ctas]
   float* part;     // stream-K partials [ctas][dual?2:1][BN][128]
   int debug_no_tma;  // SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
+  int a_tmem;        // 1: stage the weight operand in TMEM (tcgen05.cp) and issue TS MMAs
+  uint32_t a_col0;   // first TMEM column of the A buffers
+  uint32_t a_cols;   // columns per A buffer (32 per weight tile per k-block)
 };
 
 constexpr int kGemmThreads = 192;
@@ -270,20 +273,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_base_smem;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      const uint64_t pol_w = policy_evict_first();  // weights stream through once per token tile group
-      int stage = 0;
-      uint32_t phase = 0;
-      int issued = 0;
-      SegIter it(g, cta);
-      int tile, kb0, kb1;
-      while (it.next(g, tile, kb0, kb1)) {
-        const int tt = tile % g.tiles_t;
-        const int tf = tile / g.tiles_t;
-        for (int kb = kb0; kb < kb1; ++kb, ++issued) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * g.stage_bytes;
+    // ---------------- TMA producer (warp-uniform loop, one elected lane issues) ----------------
+    const uint64_t pol_w = policy_evict_first();  // weights stream through once per token tile group
+    int stage = 0;
+    uint32_t phase = 0;
+    int issued = 0;
+    SegIter it(g, cta);
+    int tile, kb0, kb1;
+    while (it.next(g, tile, kb0, kb1)) {
+      const int tt = tile % g.tiles_t;
+      const int tf = tile / g.tiles_t;
+      for (int kb = kb0; kb < kb1; ++kb, ++issued) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * g.stage_bytes;
+        if (elect_one()) {
           if (g.debug_no_tma && issued >= g.stages) {  // measurement mode: MMA on stale tiles
             mbar_arrive(&full_bar[stage]);
           } else {
@@ -292,52 +295,81 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (g.dual) tma_load_2d_hint(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, tf * 128, pol_w);
             tma_load_2d(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64, tt * g.BN);
           }
-          if (++stage == g.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == g.stages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      const uint32_t idesc = idesc_bf16_f32(128, g.BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      SegIter it(g, cta);
-      int tile, kb0, kb1;
-      while (it.next(g, tile, kb0, kb1)) {
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+    // ---------------- MMA issuer ----------------
+    // The whole warp walks the (warp-uniform) loop so descriptors and counters
+    // live in uniform registers; one elected lane issues tcgen05.mma/commit.
+    // (A lane-0-only loop measured ~850 cycles of issue overhead per k-block.)
+    const uint32_t idesc = idesc_bf16_f32(128, g.BN);
+    const uint32_t smem_base = smem_u32(smem);
+    // descriptor of stage 0; stage s adds s * stage_bytes >> 4 to the start-address field
+    const uint64_t desc0 = smem_desc_k_sw128(smem);
+    const uint32_t a2_off = g.a_bytes >> 4;
+    const uint32_t b_off = ((g.dual ? 2 : 1) * g.a_bytes) >> 4;
+    const uint32_t stage_off = g.stage_bytes >> 4;
+    (void)smem_base;
+    int ts_buf = 0;  // A-operand TMEM buffer (ping-pong) in TS mode
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    SegIter it(g, cta);
+    int tile, kb0, kb1;
+    while (it.next(g, tile, kb0, kb1)) {
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + acc * g.acc_cols;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * g.acc_cols;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          uint8_t* sa = smem + stage * g.stage_bytes;
-          const uint64_t da = smem_desc_k_sw128(sa);
-          const uint64_t da2 = smem_desc_k_sw128(sa + g.a_bytes);
-          const uint64_t db = smem_desc_k_sw128(sa + (g.dual ? 2 : 1) * g.a_bytes);
+        const uint64_t da = desc0 + (uint64_t)(stage * stage_off);
+        const uint64_t db = da + b_off;
+        if (elect_one()) {
+          if (g.a_tmem) {
+            // weights -> TMEM (tcgen05.cp), then TS MMAs read only the token tile from smem
+            const uint32_t ab = tmem_base + g.a_col0 + (uint32_t)(ts_buf * g.a_cols);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            // advance 16 bf16 = 32 B along K inside the swizzle atom (>>4 => +2)
-            const uint32_t acc_flag = (kb > kb0 || k > 0) ? 1u : 0u;
-            tc_mma_bf16(d0, da + 2 * k, db + 2 * k, idesc, acc_flag);
-            if (g.dual) tc_mma_bf16(d0 + g.BN, da2 + 2 * k, db + 2 * k, idesc, acc_flag);
+            for (int k = 0; k < 4; ++k) {
+              tc_cp_128x256b(ab + 8 * k, da + 2 * k);
+              if (g.dual) tc_cp_128x256b(ab + 32 + 8 * k, da + a2_off + 2 * k);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t acc_flag = (kb > kb0 || k > 0) ? 1u : 0u;
+              tc_mma_bf16_ts(d0, ab + 8 * k, db + 2 * k, idesc, acc_flag);
+              if (g.dual) tc_mma_bf16_ts(d0 + g.BN, ab + 32 + 8 * k, db + 2 * k, idesc, acc_flag);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              // advance 16 bf16 = 32 B along K inside the swizzle atom (>>4 => +2)
+              const uint32_t acc_flag = (kb > kb0 || k > 0) ? 1u : 0u;
+              tc_mma_bf16(d0, da + 2 * k, db + 2 * k, idesc, acc_flag);
+              if (g.dual) tc_mma_bf16(d0 + g.BN, da + a2_off + 2 * k, db + 2 * k, idesc, acc_flag);
+            }
           }
           tc_commit(&empty_bar[stage]);
-          if (++stage == g.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        tc_commit(&tfull_bar[acc]);
-        if (++acc == g.acc_stages) {
-          acc = 0;
-          acc_phase ^= 1;
+        ts_buf ^= 1;
+        __syncwarp();
+        if (++stage == g.stages) {
+          stage = 0;
+          phase ^= 1;
         }
+      }
+      if (elect_one()) tc_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == g.acc_stages) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else {
@@ -550,6 +582,11 @@ static int max_stages() {
   static int v = env_int("SX_GEMM_STAGES", 8);
   return v;
 }
+// SX_GEMM_TS=1: weight operand staged in TMEM (tcgen05.cp + TS-form MMA)
+static int ts_mode() {
+  static int v = env_int("SX_GEMM_TS", 0);
+  return v;
+}
 
 static int pick_bn(int M, int cap) {
   int tiles = (M + cap - 1) / cap;
@@ -595,10 +632,15 @@ static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
   int mode = 0;
   if (sched_req == 2 || sched_req == 3) {
     mode = sched_req - 1;
-  } else if (sched_req != 1 && eff < 0.95 && p.tiles_t > 1) {
-    // (pure stream-K measured slower than whole tiles on the one-token-tile
-    // draft shapes, tools/gemm_bench.py --sched; it stays opt-in)
-    mode = 2;
+  } else if (sched_req != 1 && eff < 0.95) {
+    // several token tiles: waves + K-split tail (keeps the weight tile shared in
+    // L2). One token tile: stream-K pays off only for thin token tiles (M <= 128:
+    // 34 -> 19 us on a 4096 x 4096 projection at M = 2, 216 -> 104 us at M = 64,
+    // K = 32768; neutral-to-worse at M = 256, tools/gemm_sched_micro.py).
+    if (p.tiles_t > 1)
+      mode = 2;
+    else if (M <= 128)
+      mode = 1;
   }
   if (mode == 2) {
     p.dp_rounds = p.tiles / P;
@@ -732,9 +774,17 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   g.stages = (227 * 1024 - 1024 - 256) / (int)g.stage_bytes;
   if (g.stages > max_stages()) g.stages = max_stages();
   g.acc_cols = p.bn * (dual ? 2 : 1);
-  g.acc_stages = (2 * g.acc_cols <= 512) ? 2 : 1;
+  g.a_tmem = ts_mode();
+  g.a_cols = g.a_tmem ? 32u * (dual ? 2 : 1) : 0u;  // 4 K=16 slices x 8 columns per weight tile
+  const uint32_t a_need = 2 * g.a_cols;               // ping-pong
+  g.acc_stages = (2 * g.acc_cols + a_need <= 512) ? 2 : 1;
+  if (g.acc_cols + a_need > 512) {  // no room for the A buffers: SS mode
+    g.a_tmem = 0;
+    g.a_cols = 0;
+  }
+  g.a_col0 = g.acc_cols * g.acc_stages;
   uint32_t cols = 32;
-  while (cols < g.acc_cols * (uint32_t)g.acc_stages) cols <<= 1;
+  while (cols < g.a_col0 + 2 * g.a_cols) cols <<= 1;
   g.tmem_cols = cols;
   g.out = out;
   g.ldo = ldo;
