@@ -10,8 +10,11 @@ resident in HBM on one B200, budget K=1024, t=0, one random 128-token prompt.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N>1 (torchrun): round 1 runs N independent replicas (weak scaling); the
-target-TP path is the next row.
+N>1 (torchrun): the 70B target is tensor-parallel over the N GPUs (NCCL
+all-reduce over NVLink after the o / down projections, all-gathered
+vocab-parallel logits; tp.py), the draft / tree build / walk are replicas on
+every rank -- one generation stream, strong scaling. `--parallel replicas`
+runs N independent streams instead (weak scaling).
 """
 
 from __future__ import annotations
@@ -33,6 +36,8 @@ WORKLOADS = {
     # name: (draft preset, target preset, K, D, B, temperature, top_p)
     "c2": ("llama2-7b", "llama2-70b", 1024, 16, 256, 0.0, 1.0),
     "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 256, 0.0, 1.0),
+    # C4: 70B target tensor-parallel over the N GPUs (--gpus N), K=4096
+    "c4": ("llama2-7b", "llama2-70b", 4096, 16, 256, 0.0, 1.0),
     "tiny": ("tiny-draft", "tiny", 128, 16, 8, 0.0, 1.0),
     # C3: 70B target offloaded to pinned host RAM, streamed per layer; 7B draft resident
     "c3": ("llama2-7b", "llama2-70b", 2048, 16, 256, 0.6, 0.9),
@@ -58,6 +63,9 @@ def parse():
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--parallel", choices=["tp", "replicas"], default="tp",
+                    help="N>1: tensor-parallel target (one stream) or N independent replicas")
+    ap.add_argument("--reduce", choices=["bf16", "fp32"], default="bf16", help="TP all-reduce precision")
     return ap.parse_args()
 
 
@@ -286,22 +294,29 @@ def main():
     K = args.budget or K
     B = args.batch or B
     syn = SyntheticBias(seed=99, rank=64, scale=args.synthetic) if args.synthetic > 0 else None
+    tp = world > 1 and args.parallel == "tp"
+    comm = None
+    if tp:
+        from paper_2406_02532_b200.tp import NcclComm
+
+        comm = NcclComm()
+    srank = 0 if tp else rank  # TP ranks share one generation stream (same prompt and seed)
     t_init = time.time()
     max_new = 100000
     ctx_cap = args.prompt_len + (args.warmup + args.steps) * (D + 1) * 3 + 64
     offload = args.workload in OFFLOAD
     target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn,
-                        offload=offload)
+                        offload=offload, tp=comm, reduce_bf16=args.reduce == "bf16")
     draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
                        synthetic=syn)
     torch.cuda.synchronize()
     init_s = time.time() - t_init
     params = sx.BuilderParams(K, D, B)
-    cfg = sx.SamplingConfig(temp, top_p, seed=rank, max_new_tokens=max_new)
+    cfg = sx.SamplingConfig(temp, top_p, seed=srank, max_new_tokens=max_new)
     scoring = args.scoring or ("raw" if temp == 0.0 else "warped")
     warp_scores = scoring == "warped"
     h2d_peak = measure_h2d(torch) if offload else None
-    prompt = tuple(int(t) for t in np.random.default_rng(1000 + rank).integers(0, PRESETS[tname].vocab, size=args.prompt_len))
+    prompt = tuple(int(t) for t in np.random.default_rng(1000 + srank).integers(0, PRESETS[tname].vocab, size=args.prompt_len))
 
     sess = SpecExecSession(prompt, draft, target, params, cfg, warp_scores)
     stream = torch.cuda.current_stream()
@@ -339,12 +354,13 @@ def main():
     iters = sess.stats.target_calls - it0 + (0 if sess.cache is None else -1)
     iters = max(iters, args.steps)
     draft_calls = sess.stats.draft_calls - dc0
-    total_tokens = sum_over_ranks(tokens, world)
+    total_tokens = tokens if tp else sum_over_ranks(tokens, world)
     value = total_tokens / (ms_max / 1e3)
     accepted_per_iter = tokens / args.steps
 
     # dominant kernel: the tcgen05 GEMM of the target pass over the tree
     pk = peaks()
+    gemm_shapes = prof.by_shape(steps=args.steps)
     big = prof.summary(min_m=max(2, K // 2))
     small = prof.summary(min_m=0)
     ach = big["flops"] / (big["ms"] / 1e3) / 1e12 if big["ms"] > 0 else 0.0
@@ -370,9 +386,10 @@ def main():
     e2e = None
     if not args.no_e2e:
         Kern.IO["h2d"] = Kern.IO["d2h"] = 0
-        prompt2 = tuple(int(t) for t in np.random.default_rng(2000 + rank).integers(0, PRESETS[tname].vocab,
-                                                                                       size=args.prompt_len))
-        cfg2 = sx.SamplingConfig(temp, top_p, seed=rank + 7, max_new_tokens=max(1, int(round(accepted_per_iter * args.steps))))
+        prompt2 = tuple(int(t) for t in np.random.default_rng(2000 + srank).integers(0, PRESETS[tname].vocab,
+                                                                                        size=args.prompt_len))
+        cfg2 = sx.SamplingConfig(temp, top_p, seed=srank + 7,
+                                 max_new_tokens=max(1, int(round(accepted_per_iter * args.steps))))
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -381,7 +398,7 @@ def main():
         el = max_over_ranks(time.perf_counter() - t0, world)
         n_it = max(1, st2.target_calls)
         h2d = Kern.IO["h2d"] + 8 * len(prompt2)
-        e2e = {"value": sum_over_ranks(len(toks2), world) / el, "unit": "tokens/s",
+        e2e = {"value": (len(toks2) if tp else sum_over_ranks(len(toks2), world)) / el, "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d / n_it), "d2h_bytes_per_step": int((Kern.IO["d2h"] + 4 * len(toks2)) / n_it),
                "iterations": n_it, "includes": "prompt prefill, tree builds, target passes, walks, host sync per round"}
 
@@ -394,18 +411,21 @@ def main():
         line = {
             "metric": "generated tokens/sec (accepted tokens per target iteration reported beside)",
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong" if tp else "weak",
+            "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic: random-init weights (N(0,0.02)), random 128-token prompt" +
                     (f", shared synthetic prev-token bias scale {args.synthetic}" if syn else ""),
             "config": {"workload": f"{args.workload}: {dname} draft + {tname} target, resident in HBM, K={K}, D={D}, "
                                    f"B={B}, t={temp}, scoring={scoring}" + (", target offloaded (per-layer H2D streaming)" if offload else "") + "",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"tp{world} target (NCCL, {args.reduce} all-reduce), draft replicated"
+                                       if tp else f"replicas x{world}") if world > 1 else "1 GPU",
                        "l2": f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)",
                        "prompt_len": args.prompt_len},
             "accepted_tokens_per_iter": accepted_per_iter,
             "draft_calls_per_iter": draft_calls / max(1, iters),
             "stage_ms_per_step": stages,
+            "gemm_shapes": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in gemm_shapes],
             "roofline": roof,
             "cpu_baseline": cb,
             "e2e": e2e,

@@ -62,7 +62,7 @@ enum {
   SX_EPI_ADD_F32 = 2,     /* out fp32 += acc (residual stream)     */
   SX_EPI_SWIGLU_BF16 = 3  /* out bf16  = silu(acc(W)) * acc(W2)    */
 };
-/* 0 = auto (CTA-pair cta_group::2 tiles for M >= 256), 1 = single-CTA only (default), 2 = pair when legal */
+/* 0 = auto (default: CTA-pair cta_group::2 tiles for M >= 256 tokens), 1 = single-CTA only, 2 = pair when legal */
 SX_API int sx_gemm_set_pair_mode(int mode);
 SX_API int sx_gemm_plan(int M, int N, int K, int dual, int splits_req, int* bn_out, int* splits_out,
                  long long* ws_floats_out);
@@ -139,6 +139,8 @@ SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u,
  * B200 models. KV cache per layer: K and V [KVH][slots][128] bf16.
  *   sx_embed      x[t] = float(E[tokens[t]])                    (fp32 residual)
  *   sx_rmsnorm    y = bf16(x * rsqrt(mean(x^2) + eps) * w)
+ *   sx_add_rmsnorm x += y (y fp32, or bf16 when y_bf16), then out = bf16(x * rsqrt(mean(x^2) + eps) * w);
+ *                 w NULL: the residual add only
  *   sx_rope_kv    rotate-half RoPE of q/k at pos_base + pos[t]; q -> [n,H,128];
  *                 k,v -> cache slot slot_base + slot[t] (pos/slot NULL: t)
  *   sx_tree_attention  query t attends KV slots [0, dense_len[t]) (NULL: dense_const)
@@ -149,6 +151,8 @@ SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u,
  */
 SX_API int sx_embed(const void* E, const int* tokens, int n, int d, float* x, cudaStream_t stream);
 SX_API int sx_rmsnorm(const float* x, const void* w, int n, int d, float eps, void* y, cudaStream_t stream);
+SX_API int sx_add_rmsnorm(float* x, const void* y, int y_bf16, const void* w, int n, int d, float eps, void* out,
+                          cudaStream_t stream);
 SX_API int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const int* slot, int slot_base, int n, int H,
                       int KVH, const float* cos_t, const float* sin_t, void* q, void* kcache, void* vcache,
                       long long slots, cudaStream_t stream);

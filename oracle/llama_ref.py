@@ -56,3 +56,40 @@ def forward_logits(cfg, W: dict, tokens: list[int], bias=None, layers: int | Non
         u, w = bias
         logits = logits + u[tok] @ w.t()
     return logits
+
+
+@torch.no_grad()
+def forward_logits_tp(cfg, W_local: dict, tokens: list[int], shard, all_reduce, all_gather) -> torch.Tensor:
+    """The same forward on one rank of a tensor-parallel group: W_local holds this
+    rank's slices (paper_2406_02532_b200/tp.py TPShard.shard), `all_reduce(t)`
+    sums in place over the group, `all_gather(t) -> [world, *t.shape]`. Returns
+    the full [len(tokens), V] logits on every rank. Checks the partition: it must
+    reproduce forward_logits of the unsharded weights."""
+    n = len(tokens)
+    H, KVH, hd = cfg.heads // shard.world, cfg.kv_heads // shard.world, cfg.head_dim
+    tok = torch.tensor(tokens, dtype=torch.long)
+    x = W_local["emb"][tok].clone()
+    pos = torch.arange(n)
+    mask = torch.full((n, n), float("-inf")).triu(1)
+    for L in W_local["layers"]:
+        h = rmsnorm(x, L["n1"], cfg.eps)
+        qkv = h @ L["wqkv"].t()
+        q = qkv[:, : H * hd].view(n, H, hd)
+        k = qkv[:, H * hd : (H + KVH) * hd].view(n, KVH, hd)
+        v = qkv[:, (H + KVH) * hd :].view(n, KVH, hd)
+        q, k = rope(q, pos, cfg.rope_theta), rope(k, pos, cfg.rope_theta)
+        g = H // KVH
+        k = k.repeat_interleave(g, dim=1)
+        v = v.repeat_interleave(g, dim=1)
+        s = torch.einsum("qhd,khd->hqk", q, k) / hd**0.5 + mask
+        att = torch.einsum("hqk,khd->qhd", s.softmax(-1), v).reshape(n, H * hd)
+        y = att @ L["wo"].t()
+        all_reduce(y)
+        x = x + y
+        h = rmsnorm(x, L["n2"], cfg.eps)
+        y = (torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
+        all_reduce(y)
+        x = x + y
+    local = rmsnorm(x, W_local["nf"], cfg.eps) @ W_local["lm"].t()
+    parts = all_gather(local)
+    return torch.cat(list(parts), dim=1)

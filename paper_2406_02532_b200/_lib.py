@@ -59,6 +59,7 @@ SIGNATURES: dict[str, tuple] = {
     "sx_sample_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _vp]),
     "sx_embed": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
     "sx_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
+    "sx_add_rmsnorm": (_c_int, [_vp, _vp, _c_int, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
     "sx_rope_kv": (
         _c_int,
         [_vp, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_ll, _vp],

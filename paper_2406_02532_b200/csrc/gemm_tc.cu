@@ -38,26 +38,23 @@ namespace sx {
 struct GemmArgs {
   int M, Nf, K;
   int BN;
-  int tiles_f, tiles_t, kb_total, tiles;
+  int tiles_f, tiles_t, kb_total, tiles;  // kb_total in units of BK = 64 * kpb
   int streamk;      // 0: whole tiles round-robin, 1: stream-K ranges, 2: whole-tile waves + split tail
   long long work;   // tiles * kb_total
-  int ctas;         // grid size (stream-K partition count)
+  int ctas;         // scheduling units (CTAs, or CTA pairs when cta_group::2)
   int dp_rounds;    // mode 2: whole-tile rounds before the tail
   int tail_tiles;   // mode 2: tiles left for the split tail
   int tail_splits;  // mode 2: K-splits per tail tile
-  int epi, dual, stages;
-  uint32_t stage_bytes, a_bytes, b_bytes;
+  int epi, stages;
+  uint32_t stage_bytes, a_bytes, b_bytes;  // a/b: one 64-wide swizzle atom of the A / B tile (this CTA's rows)
   uint32_t acc_cols;  // TMEM columns per accumulator buffer
   int acc_stages;
   uint32_t tmem_cols;
   void* out;
   long long ldo;
-  int* flags;      // stream-K partial-ready flags [ctas]
-  float* part;     // stream-K partials [ctas][dual?2:1][BN][128]
+  int* flags;      // stream-K partial-ready flags [ctas * CG]
+  float* part;     // stream-K partials [ctas * CG][dual?2:1][BN][128]
   int debug_no_tma;  // SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
-  int a_tmem;        // 1: stage the weight operand in TMEM (tcgen05.cp) and issue TS MMAs
-  uint32_t a_col0;   // first TMEM column of the A buffers
-  uint32_t a_cols;   // columns per A buffer (32 per weight tile per k-block)
 };
 
 constexpr int kGemmThreads = 192;
@@ -65,15 +62,15 @@ constexpr int kFlagFloats = 1024;  // workspace prefix reserved for the stream-K
 
 SX_DEV float silu(float x) { return x / (1.0f + __expf(-x)); }
 
-// ---- work segments: (tile, kb0, kb1) in processing order for CTA c ----------
+// ---- work segments: (tile, kb0, kb1) in processing order for unit c ---------
 struct SegIter {
   long long pos, end;
   int t, step, c, r;
   int mode;
   bool tail_done;
-  SX_DEV SegIter(const GemmArgs& g, int cta) {
+  SX_DEV SegIter(const GemmArgs& g, int unit) {
     mode = g.streamk;
-    c = cta;
+    c = unit;
     r = 0;
     tail_done = false;
     if (mode == 1) {
@@ -94,7 +91,7 @@ struct SegIter {
       return true;
     }
     if (mode == 2) {
-      if (r < g.dp_rounds) {  // whole tiles: in round r the CTAs cover tiles r*P .. r*P+P-1
+      if (r < g.dp_rounds) {  // whole tiles: in round r the units cover tiles r*P .. r*P+P-1
         tile = r * g.ctas + c;
         kb0 = 0;
         kb1 = g.kb_total;
@@ -102,7 +99,7 @@ struct SegIter {
         return true;
       }
       if (tail_done || c >= g.tail_tiles * g.tail_splits) return false;
-      tail_done = true;  // one tail item per CTA; all items run concurrently
+      tail_done = true;  // one tail item per unit; all items run concurrently
       const int j = c % g.tail_tiles, s = c / g.tail_tiles;
       tile = g.dp_rounds * g.ctas + j;
       kb0 = (int)((long long)g.kb_total * s / g.tail_splits);
@@ -119,8 +116,8 @@ struct SegIter {
 };
 
 SX_DEV long long sk_start(const GemmArgs& g, int c) { return (g.work * c) / g.ctas; }
-// CTA whose range contains linear k-block k
-SX_DEV int sk_cta_of(const GemmArgs& g, long long k) {
+// unit whose range contains linear k-block k
+SX_DEV int sk_unit_of(const GemmArgs& g, long long k) {
   int c = (int)((k * g.ctas) / g.work);
   while (c + 1 < g.ctas && sk_start(g, c + 1) <= k) ++c;
   while (c > 0 && sk_start(g, c) > k) --c;
@@ -163,10 +160,11 @@ SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float 
 // TMEM accumulator (this thread's lane = feature f, BN token columns) -> global.
 //   mode 0: whole tile          -> final epilogue
 //   mode 1: helper segment      -> fp32 partial in slot `slot`, then publish flag
-//   mode 2: owner of split tile -> add partials of CTAs h0, h0+hs, ... (hn of them) in order
+//   mode 2: owner of split tile -> add the partials of slots h0, h0+hs, ... (hn of them) in order
+template <bool DUAL>
 SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool fok, int tt, int mode, int slot,
                          int h0, int hs, int hn) {
-  const long long pstride = (long long)(g.dual ? 2 : 1) * g.BN * 128;
+  const long long pstride = (long long)(DUAL ? 2 : 1) * g.BN * 128;
   if (mode == 2) {
     if (threadIdx.x == 64)
       for (int i = 0; i < hn; ++i) {
@@ -179,13 +177,13 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
     uint32_t r[16];
     uint32_t r2[16];
     tmem_ld16(tbase + c, r);
-    if (g.dual) tmem_ld16(tbase + g.BN + c, r2);
+    if (DUAL) tmem_ld16(tbase + g.BN + c, r2);
     tmem_ld_wait();
     float v[16], v2[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       v[j] = __uint_as_float(r[j]);
-      v2[j] = g.dual ? __uint_as_float(r2[j]) : 0.f;
+      v2[j] = DUAL ? __uint_as_float(r2[j]) : 0.f;
     }
     // partial layout per slot: [token/4][feature][4] floats -> one float4 per 4 tokens
     if (mode == 1) {
@@ -193,7 +191,7 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         p[q * 128] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        if (g.dual)
+        if (DUAL)
           p[(long long)g.BN * 32 + q * 128] = make_float4(v2[4 * q], v2[4 * q + 1], v2[4 * q + 2], v2[4 * q + 3]);
       }
       continue;
@@ -206,7 +204,7 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           a[q] = __ldcg(p + q * 128);
-          if (g.dual) b[q] = __ldcg(p + (long long)g.BN * 32 + q * 128);
+          if (DUAL) b[q] = __ldcg(p + (long long)g.BN * 32 + q * 128);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -214,7 +212,7 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
           v[4 * q + 1] += a[q].y;
           v[4 * q + 2] += a[q].z;
           v[4 * q + 3] += a[q].w;
-          if (g.dual) {
+          if (DUAL) {
             v2[4 * q] += b[q].x;
             v2[4 * q + 1] += b[q].y;
             v2[4 * q + 2] += b[q].z;
@@ -236,11 +234,42 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
   }
 }
 
+// ---- cta_group-dependent primitives -----------------------------------------
+template <int CG>
+SX_DEV void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t pol) {
+  if constexpr (CG == 1)
+    tma_load_2d_hint(dst, map, bar, c0, c1, pol);
+  else
+    tma_load_2d_2sm(dst, map, bar, c0, c1, pol);
+}
+template <int CG>
+SX_DEV void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (CG == 1)
+    tc_mma_bf16(d, a, b, idesc, acc);
+  else
+    tc_mma_bf16_2sm(d, a, b, idesc, acc);
+}
+template <int CG>
+SX_DEV void commit(uint64_t* bar) {
+  if constexpr (CG == 1)
+    tc_commit(bar);
+  else
+    tc_commit_2sm_mc(bar, 0x3);
+}
+
+// One kernel for both MMA shapes:
+//   CG = 1: one CTA per tile, M = 128 weight rows, BN tokens;
+//   CG = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2) per tile, M = 256
+//           weight rows (128 per CTA), each CTA stages half of the BN token rows,
+//           the leader issues the pair MMA -- half the B-operand smem traffic per SM.
+// KPB = 64-wide k-blocks (swizzle atoms) per pipeline stage: 2 halves the
+// mbarrier round trips (wait + commit) per MMA.
+template <int CG, bool DUAL, int KPB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
                    const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the 128B-swizzle atoms.
+  // 1024-B alignment for the 128B-swizzle atoms (same offset in both CTAs of a pair).
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + g.stages * g.stage_bytes);
   uint64_t* empty_bar = full_bar + g.stages;
@@ -250,11 +279,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int cta = blockIdx.x;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int unit = blockIdx.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapA);
-    if (g.dual) tma_prefetch_desc(&mapA2);
+    if (DUAL) tma_prefetch_desc(&mapA2);
     tma_prefetch_desc(&mapB);
     for (int s = 0; s < g.stages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -262,269 +292,111 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], 4 * CG);  // 4 epilogue warps per CTA (pair: both CTAs arrive at the leader)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_base_smem, g.tmem_cols);
+  if (warp == 1) {
+    if constexpr (CG == 1)
+      tmem_alloc(tmem_base_smem, g.tmem_cols);
+    else
+      tmem_alloc_2sm(tmem_base_smem, g.tmem_cols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1)
+    __syncthreads();
+  else
+    cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
+  const uint32_t a_off = (DUAL ? 2 : 1) * KPB * g.a_bytes;  // B atoms follow the A (and A2) atoms
   if (warp == 0) {
     // ---------------- TMA producer (warp-uniform loop, one elected lane issues) ----------------
-    const uint64_t pol_w = policy_evict_first();  // weights stream through once per token tile group
+    const uint64_t pol_w = policy_evict_first();  // weights stream through once per token-tile group
+    const uint64_t pol_x = policy_evict_last();   // token tiles are re-read by every weight tile
+    const int bhalf = g.BN / CG;
     int stage = 0;
     uint32_t phase = 0;
     int issued = 0;
-    SegIter it(g, cta);
+    SegIter it(g, unit);
     int tile, kb0, kb1;
     while (it.next(g, tile, kb0, kb1)) {
       const int tt = tile % g.tiles_t;
       const int tf = tile / g.tiles_t;
+      const int frow = tf * 128 * CG + (int)rank * 128;
+      const int trow = tt * g.BN + (int)rank * bhalf;
       for (int kb = kb0; kb < kb1; ++kb, ++issued) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * g.stage_bytes;
         if (elect_one()) {
           if (g.debug_no_tma && issued >= g.stages) {  // measurement mode: MMA on stale tiles
-            mbar_arrive(&full_bar[stage]);
-          } else {
-            mbar_arrive_expect_tx(&full_bar[stage], g.stage_bytes);
-            tma_load_2d_hint(sa, &mapA, &full_bar[stage], kb * 64, tf * 128, pol_w);
-            if (g.dual) tma_load_2d_hint(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, tf * 128, pol_w);
-            tma_load_2d(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64, tt * g.BN);
-          }
-        }
-        __syncwarp();
-        if (++stage == g.stages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    // The whole warp walks the (warp-uniform) loop so descriptors and counters
-    // live in uniform registers; one elected lane issues tcgen05.mma/commit.
-    // (A lane-0-only loop measured ~850 cycles of issue overhead per k-block.)
-    const uint32_t idesc = idesc_bf16_f32(128, g.BN);
-    const uint32_t smem_base = smem_u32(smem);
-    // descriptor of stage 0; stage s adds s * stage_bytes >> 4 to the start-address field
-    const uint64_t desc0 = smem_desc_k_sw128(smem);
-    const uint32_t a2_off = g.a_bytes >> 4;
-    const uint32_t b_off = ((g.dual ? 2 : 1) * g.a_bytes) >> 4;
-    const uint32_t stage_off = g.stage_bytes >> 4;
-    (void)smem_base;
-    int ts_buf = 0;  // A-operand TMEM buffer (ping-pong) in TS mode
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    SegIter it(g, cta);
-    int tile, kb0, kb1;
-    while (it.next(g, tile, kb0, kb1)) {
-      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d0 = tmem_base + acc * g.acc_cols;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
-        tc_fence_after();
-        const uint64_t da = desc0 + (uint64_t)(stage * stage_off);
-        const uint64_t db = da + b_off;
-        if (elect_one()) {
-          if (g.a_tmem) {
-            // weights -> TMEM (tcgen05.cp), then TS MMAs read only the token tile from smem
-            const uint32_t ab = tmem_base + g.a_col0 + (uint32_t)(ts_buf * g.a_cols);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              tc_cp_128x256b(ab + 8 * k, da + 2 * k);
-              if (g.dual) tc_cp_128x256b(ab + 32 + 8 * k, da + a2_off + 2 * k);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t acc_flag = (kb > kb0 || k > 0) ? 1u : 0u;
-              tc_mma_bf16_ts(d0, ab + 8 * k, db + 2 * k, idesc, acc_flag);
-              if (g.dual) tc_mma_bf16_ts(d0 + g.BN, ab + 32 + 8 * k, db + 2 * k, idesc, acc_flag);
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              // advance 16 bf16 = 32 B along K inside the swizzle atom (>>4 => +2)
-              const uint32_t acc_flag = (kb > kb0 || k > 0) ? 1u : 0u;
-              tc_mma_bf16(d0, da + 2 * k, db + 2 * k, idesc, acc_flag);
-              if (g.dual) tc_mma_bf16(d0 + g.BN, da + a2_off + 2 * k, db + 2 * k, idesc, acc_flag);
-            }
-          }
-          tc_commit(&empty_bar[stage]);
-        }
-        ts_buf ^= 1;
-        __syncwarp();
-        if (++stage == g.stages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (elect_one()) tc_commit(&tfull_bar[acc]);
-      __syncwarp();
-      if (++acc == g.acc_stages) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
-    }
-  } else {
-    // ---------------- epilogue (warps 2..5) ----------------
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int fl = quarter * 32 + lane;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    SegIter it(g, cta);
-    int tile, kb0, kb1;
-    while (it.next(g, tile, kb0, kb1)) {
-      const int tt = tile % g.tiles_t;
-      const int tf = tile / g.tiles_t;
-      const int f = tf * 128 + fl;
-      const bool fok = f < g.Nf;
-      int mode = 0, h0 = 0, hs = 1, hn = 0;
-      if (kb0 > 0) {
-        mode = 1;  // helper: publishes a partial for the tile's owner
-      } else if (kb1 < g.kb_total) {
-        mode = 2;  // owner: the rest of the tile is summed by other CTAs
-        if (g.streamk == 1) {
-          h0 = cta + 1;
-          hn = sk_cta_of(g, (long long)tile * g.kb_total + g.kb_total - 1) - cta;
-        } else {
-          h0 = cta + g.tail_tiles;
-          hs = g.tail_tiles;
-          hn = g.tail_splits - 1;
-        }
-      }
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_seg(g, tbase, f, fl, fok, tt, mode, cta, h0, hs, hn);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-      if (++acc == g.acc_stages) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, g.tmem_cols);
-  }
-}
-
-// ----------------------------------------------------------------------------
-// CTA-pair variant (tcgen05 cta_group::2, M = 256 features per pair): each CTA
-// stages its 128 weight rows and half of the BN token rows; the leader issues
-// the pair MMA. Kept behind sx_gemm_set_pair_mode(2): on B200 it measured ~7%
-// slower than the single-CTA kernel on every target-pass shape
-// (tools/gemm_micro3.py).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
-                    const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + g.stages * g.stage_bytes);
-  uint64_t* empty_bar = full_bar + g.stages;
-  uint64_t* tfull_bar = empty_bar + g.stages;
-  uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
-  const int half = g.BN / 2;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&mapA);
-    if (g.dual) tma_prefetch_desc(&mapA2);
-    tma_prefetch_desc(&mapB);
-    for (int s = 0; s < g.stages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc_2sm(tmem_base_smem, g.tmem_cols);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_base_smem;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = pair; u < g.tiles; u += npairs) {
-        const int tt = u % g.tiles_t;
-        const int tf = u / g.tiles_t;
-        for (int kb = 0; kb < g.kb_total; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * g.stage_bytes;
-          if (g.debug_no_tma && kb >= g.stages) {
             if (rank == 0) mbar_arrive(&full_bar[stage]);
           } else {
-            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * g.stage_bytes);
-            const int frow = tf * 256 + (int)rank * 128;
-            tma_load_2d_2sm(sa, &mapA, &full_bar[stage], kb * 64, frow, pol_w);
-            if (g.dual) tma_load_2d_2sm(sa + g.a_bytes, &mapA2, &full_bar[stage], kb * 64, frow, pol_w);
-            tma_load_2d_2sm(sa + (g.dual ? 2 : 1) * g.a_bytes, &mapB, &full_bar[stage], kb * 64,
-                            tt * g.BN + (int)rank * half, pol_x);
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * g.stage_bytes);
+#pragma unroll
+            for (int j = 0; j < KPB; ++j) {
+              const int kc = (kb * KPB + j) * 64;
+              tma_load<CG>(sa + j * g.a_bytes, &mapA, &full_bar[stage], kc, frow, pol_w);
+              if (DUAL) tma_load<CG>(sa + (KPB + j) * g.a_bytes, &mapA2, &full_bar[stage], kc, frow, pol_w);
+              tma_load<CG>(sa + a_off + j * g.b_bytes, &mapB, &full_bar[stage], kc, trow, pol_x);
+            }
           }
-          if (++stage == g.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == g.stages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      const uint32_t idesc = idesc_bf16_f32(256, g.BN);
+    // ---------------- MMA issuer (pair: leader CTA only) ----------------
+    // The whole warp walks the (warp-uniform) loop so descriptors and counters
+    // live in uniform registers; one elected lane issues tcgen05.mma/commit.
+    if (rank == 0) {
+      const uint32_t idesc = idesc_bf16_f32(128 * CG, g.BN);
+      const uint64_t desc0 = smem_desc_k_sw128(smem);  // stage s adds s * stage_bytes >> 4
+      const uint32_t a_atom = g.a_bytes >> 4, b_atom = g.b_bytes >> 4;
+      const uint32_t b_off = a_off >> 4;
+      const uint32_t stage_off = g.stage_bytes >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = pair; u < g.tiles; u += npairs) {
+      SegIter it(g, unit);
+      int tile, kb0, kb1;
+      while (it.next(g, tile, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * g.acc_cols;
-        for (int kb = 0; kb < g.kb_total; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* sa = smem + stage * g.stage_bytes;
-          const uint64_t da = smem_desc_k_sw128(sa);
-          const uint64_t da2 = smem_desc_k_sw128(sa + g.a_bytes);
-          const uint64_t db = smem_desc_k_sw128(sa + (g.dual ? 2 : 1) * g.a_bytes);
+          const uint64_t ds = desc0 + (uint64_t)(stage * stage_off);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t acc_flag = (kb > 0 || k > 0) ? 1u : 0u;
-            tc_mma_bf16_2sm(d0, da + 2 * k, db + 2 * k, idesc, acc_flag);
-            if (g.dual) tc_mma_bf16_2sm(d0 + g.BN, da2 + 2 * k, db + 2 * k, idesc, acc_flag);
+            for (int j = 0; j < KPB; ++j) {
+              const uint64_t da = ds + j * a_atom;
+              const uint64_t db = ds + b_off + j * b_atom;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                // advance 16 bf16 = 32 B along K inside the swizzle atom (>>4 => +2)
+                const uint32_t acc_flag = (kb > kb0 || j > 0 || k > 0) ? 1u : 0u;
+                mma<CG>(d0, da + 2 * k, db + 2 * k, idesc, acc_flag);
+                if (DUAL) mma<CG>(d0 + g.BN, da + KPB * a_atom + 2 * k, db + 2 * k, idesc, acc_flag);
+              }
+            }
+            commit<CG>(&empty_bar[stage]);
           }
-          tc_commit_2sm_mc(&empty_bar[stage], 0x3);
+          __syncwarp();
           if (++stage == g.stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_2sm_mc(&tfull_bar[acc], 0x3);
+        if (elect_one()) commit<CG>(&tfull_bar[acc]);
+        __syncwarp();
         if (++acc == g.acc_stages) {
           acc = 0;
           acc_phase ^= 1;
@@ -532,22 +404,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int fl = quarter * 32 + lane;
+    const int slot = unit * CG + (int)rank;  // this CTA's partial slot / flag
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < g.tiles; u += npairs) {
-      const int tt = u % g.tiles_t;
-      const int tf = u / g.tiles_t;
-      const int f = tf * 256 + (int)rank * 128 + fl;
+    SegIter it(g, unit);
+    int tile, kb0, kb1;
+    while (it.next(g, tile, kb0, kb1)) {
+      const int tt = tile % g.tiles_t;
+      const int tf = tile / g.tiles_t;
+      const int f = tf * 128 * CG + (int)rank * 128 + fl;
       const bool fok = f < g.Nf;
+      int mode = 0, h0 = 0, hs = 1, hn = 0;
+      if (kb0 > 0) {
+        mode = 1;  // helper: publishes a partial for the tile's owner
+      } else if (kb1 < g.kb_total) {
+        mode = 2;  // owner: the rest of the tile is summed by other units (same rank)
+        if (g.streamk == 1) {
+          h0 = (unit + 1) * CG + (int)rank;
+          hs = CG;
+          hn = sk_unit_of(g, (long long)tile * g.kb_total + g.kb_total - 1) - unit;
+        } else {
+          h0 = (unit + g.tail_tiles) * CG + (int)rank;
+          hs = g.tail_tiles * CG;
+          hn = g.tail_splits - 1;
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_seg(g, tbase, f, fl, fok, tt, 0, 0, 0, 1, 0);
+      epilogue_seg<DUAL>(g, tbase, f, fl, fok, tt, mode, slot, h0, hs, hn);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+      if (lane == 0) {
+        if constexpr (CG == 1)
+          mbar_arrive(&tempty_bar[acc]);
+        else
+          mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
       if (++acc == g.acc_stages) {
         acc = 0;
         acc_phase ^= 1;
@@ -557,19 +453,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  cluster_sync();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_2sm(tmem_base, g.tmem_cols);
+    if constexpr (CG == 1)
+      tmem_dealloc(tmem_base, g.tmem_cols);
+    else
+      tmem_dealloc_2sm(tmem_base, g.tmem_cols);
   }
 }
 
-// 0 = auto (pair for M >= 256), 1 = single-CTA only, 2 = pair whenever legal.
-// Default single: measured on B200 the pair kernel is ~7% slower on every
-// target-pass shape (tools/gemm_micro3.py).
-static int g_pair_mode = 1;
+// 0 = auto (pair when the tree pass has >= 256 tokens), 1 = single-CTA only, 2 = pair whenever legal.
+static int g_pair_mode = 0;
 
-// tuning overrides (read once): SX_GEMM_BN_CAP (token-tile cap), SX_GEMM_STAGES (max pipeline depth)
+// tuning overrides (read once): SX_GEMM_BN_CAP (token-tile cap), SX_GEMM_STAGES (max pipeline depth),
+// SX_GEMM_KPB (64-wide k-blocks per stage; 0 = auto)
 static int env_int(const char* name, int dflt) {
   const char* s = getenv(name);
   return s ? atoi(s) : dflt;
@@ -582,9 +480,8 @@ static int max_stages() {
   static int v = env_int("SX_GEMM_STAGES", 8);
   return v;
 }
-// SX_GEMM_TS=1: weight operand staged in TMEM (tcgen05.cp + TS-form MMA)
-static int ts_mode() {
-  static int v = env_int("SX_GEMM_TS", 0);
+static int kpb_req() {
+  static int v = env_int("SX_GEMM_KPB", 0);
   return v;
 }
 
@@ -597,36 +494,70 @@ static int pick_bn(int M, int cap) {
 }
 
 struct Plan {
-  int bn, tiles_f, tiles_t, tiles, kb_total, ctas, streamk;
+  int cg, kpb, bn, tiles_f, tiles_t, tiles, kb_total, ctas, streamk;
   int dp_rounds, tail_tiles, tail_splits;
+  int stages;
+  uint32_t a_bytes, b_bytes, stage_bytes;
   long long ws_floats;
 };
 
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 256;
+
+static bool use_pair(int M, int Nf, int dual) {
+  if (Nf < 256) return false;
+  if (g_pair_mode == 1) return false;
+  if (g_pair_mode == 2) return true;
+  // auto: the target pass over the tree (hundreds of tokens) is MMA-bound and
+  // the pair halves the B-operand smem traffic per SM -- when its 256-row tiles
+  // still give >= 1.5 waves over the 74 pairs. Thin draft batches stream
+  // weights and keep the single-CTA schedule (narrow token tiles, stream-K).
+  if (M < 256) return false;
+  const int bn = pick_bn(M, dual ? 128 : bn_cap_single());
+  const long long tiles = (long long)((Nf + 255) / 256) * ((M + bn - 1) / bn);
+  return tiles * 2 >= 3 * (kNumSMs / 2);
+}
+
 // sched_req: 1 = whole tiles only, 2 = force stream-K ranges, 3 = force
 // whole-tile waves + split tail; otherwise auto:
-//  - whole tiles when the waves fill >= 95% of the CTA slots;
+//  - whole tiles when the waves fill >= 95% of the units;
 //  - else, with several token tiles per weight tile, whole-tile waves plus a
 //    K-split tail (all tail items run together, so the token tiles of a weight
 //    tile still read the same k-range at the same time and share it in L2);
 //  - else (one token tile: every weight tile is read once anyway) stream-K.
 static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
   Plan p{};
+  p.cg = use_pair(M, Nf, dual) ? 2 : 1;
+  const int P = kNumSMs / p.cg;  // scheduling units
+  const int fr = 128 * p.cg;     // weight rows per tile
   p.bn = pick_bn(M, dual ? 128 : bn_cap_single());
-  p.tiles_f = (Nf + 127) / 128;
+  p.tiles_f = (Nf + fr - 1) / fr;
   // Weight-streaming shapes with few weight tiles (e.g. a 4096-wide projection of
   // the draft = 32 tiles): a single SM's TMA pulls only ~40-50 GB/s, so use
   // narrower token tiles until ~120+ CTAs stream. The weight tile is shared by
   // the token tiles through L2, HBM traffic is unchanged.
-  while (p.tiles_f * ((M + p.bn - 1) / p.bn) < 120 && p.bn > 32) {
-    const int half = ((p.bn / 2) + 15) / 16 * 16;
-    const int nb = pick_bn(M, half);
-    if (p.tiles_f * ((M + nb - 1) / nb) > kNumSMs) break;  // would spill into a second wave
-    p.bn = nb;
+  if (p.cg == 1) {
+    while (p.tiles_f * ((M + p.bn - 1) / p.bn) < 120 && p.bn > 32) {
+      const int half = ((p.bn / 2) + 15) / 16 * 16;
+      const int nb = pick_bn(M, half);
+      if (p.tiles_f * ((M + nb - 1) / nb) > kNumSMs) break;  // would spill into a second wave
+      p.bn = nb;
+    }
   }
   p.tiles_t = (M + p.bn - 1) / p.bn;
   p.tiles = p.tiles_f * p.tiles_t;
-  p.kb_total = K / 64;
-  const int P = kNumSMs;
+  p.a_bytes = 128 * 64 * 2;
+  p.b_bytes = (uint32_t)(p.bn / p.cg) * 64 * 2;
+  // k-blocks per stage: 2 when K allows and >= 3 such stages fit (deep enough to hide TMA latency)
+  auto stage_bytes = [&](int kpb) { return (uint32_t)kpb * ((dual ? 2 : 1) * p.a_bytes + p.b_bytes); };
+  int kpb = kpb_req();
+  if (kpb != 1 && kpb != 2) kpb = (K % 128 == 0 && kSmemBudget / (int)stage_bytes(2) >= 3) ? 2 : 1;
+  if (K % (64 * kpb) != 0) kpb = 1;
+  p.kpb = kpb;
+  p.stage_bytes = stage_bytes(kpb);
+  p.stages = kSmemBudget / (int)p.stage_bytes;
+  const int cap = (max_stages() + kpb - 1) / kpb;
+  if (p.stages > cap) p.stages = cap;
+  p.kb_total = K / (64 * kpb);
   const int waves = (p.tiles + P - 1) / P;
   const double eff = (double)p.tiles / ((double)waves * P);
   int mode = 0;
@@ -651,8 +582,8 @@ static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
     p.tail_splits = s;
     if (p.tail_tiles == 0 || s == 1) mode = 0;  // nothing to balance
     // the owner's fixup (reading s-1 partial tiles) must stay small next to a
-    // tail item: measured a loss at 21 k-blocks per item (o-proj), a gain at 64+
-    if (sched_req != 3 && p.kb_total / s < 48) mode = 0;
+    // tail item: measured a loss at 21 64-wide k-blocks per item (o-proj), a gain at 64+
+    if (sched_req != 3 && p.kb_total * kpb / s < 48) mode = 0;
   }
   p.streamk = mode;
   if (mode == 1) {
@@ -663,8 +594,34 @@ static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
   } else {
     p.ctas = p.tiles < P ? p.tiles : P;
   }
-  p.ws_floats = mode ? kFlagFloats + (long long)p.ctas * (dual ? 2 : 1) * p.bn * 128 : 0;
+  p.ws_floats = mode ? kFlagFloats + (long long)p.ctas * p.cg * (dual ? 2 : 1) * p.bn * 128 : 0;
   return p;
+}
+
+template <int CG, bool DUAL, int KPB>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& ma2, const CUtensorMap& mb, const GemmArgs& g,
+                       size_t smem, cudaStream_t stream) {
+  auto kern = gemm_tc_kernel<CG, DUAL, KPB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.ctas * CG);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, ma, ma2, mb, g);
+  SX_CHECK_LAUNCH("gemm_tc_kernel");
+  return SX_OK;
 }
 
 }  // namespace sx
@@ -683,7 +640,7 @@ extern "C" int sx_gemm_plan(int M, int Nf, int K, int dual, int splits_req, int*
     return arg_error("sx_gemm: need M,N > 0 and K a positive multiple of 64 (M=%d N=%d K=%d)", M, Nf, K);
   Plan p = make_plan(M, Nf, K, dual, splits_req);
   *bn_out = p.bn;
-  *splits_out = p.streamk ? p.ctas : 1;  // >1: number of stream-K ranges
+  *splits_out = p.streamk ? p.ctas : 1;  // >1: number of stream-K units
   *ws_floats_out = p.ws_floats;
   return SX_OK;
 }
@@ -698,58 +655,13 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   if (M <= 0 || Nf <= 0 || K <= 0 || (K % 64) != 0)
     return arg_error("sx_gemm: need M,N > 0 and K a positive multiple of 64 (M=%d N=%d K=%d)", M, Nf, K);
   int st;
-
-  // CTA-pair (cta_group::2) path, opt-in
-  const bool pair = Nf >= 256 && (g_pair_mode == 2 || (g_pair_mode == 0 && M >= 256));
-  if (pair) {
-    const int bn = (pick_bn(M, dual ? 128 : bn_cap_single()) + 31) / 32 * 32;
-    CUtensorMap ma, ma2, mb;
-    if ((st = make_tmap_bf16_kmajor(&ma, W, Nf, K, K, 128))) return st;
-    if ((st = make_tmap_bf16_kmajor(&ma2, dual ? W2 : W, Nf, K, K, 128))) return st;
-    if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, bn / 2))) return st;
-    GemmArgs g{};
-    g.M = M;
-    g.Nf = Nf;
-    g.K = K;
-    g.BN = bn;
-    g.tiles_f = (Nf + 255) / 256;
-    g.tiles_t = (M + bn - 1) / bn;
-    g.kb_total = K / 64;
-    g.tiles = g.tiles_f * g.tiles_t;
-    g.epi = epi;
-    g.dual = dual;
-    g.a_bytes = 128 * 64 * 2;
-    g.b_bytes = (bn / 2) * 64 * 2;
-    g.stage_bytes = (dual ? 2 : 1) * g.a_bytes + g.b_bytes;
-    g.stages = (227 * 1024 - 1024 - 256) / (int)g.stage_bytes;
-    if (g.stages > max_stages()) g.stages = max_stages();
-    g.acc_cols = bn * (dual ? 2 : 1);
-    g.acc_stages = (2 * g.acc_cols <= 512) ? 2 : 1;
-    uint32_t cols = 32;
-    while (cols < g.acc_cols * (uint32_t)g.acc_stages) cols <<= 1;
-    g.tmem_cols = cols;
-    g.out = out;
-    g.ldo = ldo;
-    g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
-    const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + (2 * g.stages + 4) * 8 + 16;
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr2 = true;
-    }
-    const int pairs = g.tiles < kNumSMs / 2 ? g.tiles : kNumSMs / 2;
-    gemm_tc2_kernel<<<2 * pairs, kGemmThreads, smem, stream>>>(ma, ma2, mb, g);
-    SX_CHECK_LAUNCH("gemm_tc2_kernel");
-    return SX_OK;
-  }
-
   Plan p = make_plan(M, Nf, K, dual, splits_req);
   if (p.ws_floats > 0 && (ws == nullptr || ws_floats < p.ws_floats))
     return arg_error("sx_gemm: stream-K workspace needs %lld floats, got %lld", p.ws_floats, ws_floats);
   CUtensorMap ma, ma2, mb;
   if ((st = make_tmap_bf16_kmajor(&ma, W, Nf, K, K, 128))) return st;
   if ((st = make_tmap_bf16_kmajor(&ma2, dual ? W2 : W, Nf, K, K, 128))) return st;
-  if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, p.bn))) return st;
+  if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, p.bn / p.cg))) return st;
 
   GemmArgs g{};
   g.M = M;
@@ -767,24 +679,14 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   g.tail_tiles = p.tail_tiles;
   g.tail_splits = p.tail_splits;
   g.epi = epi;
-  g.dual = dual;
-  g.a_bytes = 128 * 64 * 2;
-  g.b_bytes = p.bn * 64 * 2;
-  g.stage_bytes = (dual ? 2 : 1) * g.a_bytes + g.b_bytes;
-  g.stages = (227 * 1024 - 1024 - 256) / (int)g.stage_bytes;
-  if (g.stages > max_stages()) g.stages = max_stages();
+  g.a_bytes = p.a_bytes;
+  g.b_bytes = p.b_bytes;
+  g.stage_bytes = p.stage_bytes;
+  g.stages = p.stages;
   g.acc_cols = p.bn * (dual ? 2 : 1);
-  g.a_tmem = ts_mode();
-  g.a_cols = g.a_tmem ? 32u * (dual ? 2 : 1) : 0u;  // 4 K=16 slices x 8 columns per weight tile
-  const uint32_t a_need = 2 * g.a_cols;               // ping-pong
-  g.acc_stages = (2 * g.acc_cols + a_need <= 512) ? 2 : 1;
-  if (g.acc_cols + a_need > 512) {  // no room for the A buffers: SS mode
-    g.a_tmem = 0;
-    g.a_cols = 0;
-  }
-  g.a_col0 = g.acc_cols * g.acc_stages;
+  g.acc_stages = (2 * g.acc_cols <= 512) ? 2 : 1;
   uint32_t cols = 32;
-  while (cols < g.a_col0 + 2 * g.a_cols) cols <<= 1;
+  while (cols < g.acc_cols * (uint32_t)g.acc_stages) cols <<= 1;
   g.tmem_cols = cols;
   g.out = out;
   g.ldo = ldo;
@@ -793,12 +695,16 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
 
   const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + (2 * g.stages + 4) * 8 + 16;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
-  gemm_tc_kernel<<<g.ctas, kGemmThreads, smem, stream>>>(ma, ma2, mb, g);
-  SX_CHECK_LAUNCH("gemm_tc_kernel");
-  return SX_OK;
+#define SX_GEMM_LAUNCH(CG, DU, KP) \
+  if (p.cg == CG && dual == DU && p.kpb == KP) return launch_gemm<CG, DU, KP>(ma, ma2, mb, g, smem, stream);
+  SX_GEMM_LAUNCH(1, 0, 1)
+  SX_GEMM_LAUNCH(1, 0, 2)
+  SX_GEMM_LAUNCH(1, 1, 1)
+  SX_GEMM_LAUNCH(1, 1, 2)
+  SX_GEMM_LAUNCH(2, 0, 1)
+  SX_GEMM_LAUNCH(2, 0, 2)
+  SX_GEMM_LAUNCH(2, 1, 1)
+  SX_GEMM_LAUNCH(2, 1, 2)
+#undef SX_GEMM_LAUNCH
+  return arg_error("sx_gemm: no kernel for cg=%d dual=%d kpb=%d", p.cg, dual, p.kpb);
 }

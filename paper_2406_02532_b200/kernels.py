@@ -54,6 +54,22 @@ class GemmProfiler:
             n += 1
         return {"launches": n, "flops": flops, "ms": ms}
 
+    def by_shape(self, top: int = 12, steps: int = 1) -> list[dict]:
+        """Per (M, N, K, dual) shape: launches, ms and TFLOP/s (per step)."""
+        torch.cuda.synchronize()
+        agg: dict[tuple, list] = {}
+        for M, N, K, dual, e0, e1 in self.rec:
+            a = agg.setdefault((M, N, K, dual), [0, 0.0])
+            a[0] += 1
+            a[1] += e0.elapsed_time(e1)
+        rows = []
+        for (M, N, K, dual), (n, ms) in agg.items():
+            fl = 2.0 * M * N * K * (2 if dual else 1) * n
+            rows.append({"M": M, "N": N, "K": K, "dual": bool(dual), "launches_per_step": n / steps,
+                         "ms_per_step": ms / steps, "tflops": fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0})
+        rows.sort(key=lambda r: -r["ms_per_step"])
+        return rows[:top]
+
 
 PROFILER: GemmProfiler | None = None
 

@@ -33,6 +33,7 @@ import torch
 from . import _lib
 from . import kernels as K
 from .models import LanguageModel, _WS, _check_prefix
+from .tp import TPShard
 from .tree import BuilderParams
 
 
@@ -92,18 +93,11 @@ def _rope_tables(cfg: LlamaConfig, max_pos: int, device) -> tuple[torch.Tensor, 
     return freqs.cos().contiguous().to(device), freqs.sin().contiguous().to(device)
 
 
-def layer_layout(cfg: LlamaConfig) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
+def layer_layout(cfg: LlamaConfig, shard: TPShard | None = None) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
     """Byte offsets of one decoder layer's tensors in a contiguous buffer
-    (256-B aligned, the unit streamed in offload mode)."""
-    shapes = {
-        "wqkv": (cfg.qkv_out, cfg.d),
-        "wo": (cfg.d, cfg.heads * cfg.head_dim),
-        "wg": (cfg.ff, cfg.d),
-        "wu": (cfg.ff, cfg.d),
-        "wd": (cfg.d, cfg.ff),
-        "n1": (cfg.d,),
-        "n2": (cfg.d,),
-    }
+    (256-B aligned, the unit streamed in offload mode); `shard`: this rank's
+    tensor-parallel slice of the layer (tp.py)."""
+    shapes = (TPShard(0, 1) if shard is None else shard).local_shapes(cfg)
     out, off = {}, 0
     for k, shp in shapes.items():
         out[k] = (off, shp)
@@ -120,9 +114,10 @@ class LlamaWeights:
     contiguous buffer -- in HBM, or (offload) in pinned host memory."""
 
     def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0,
-                 offload: bool = False):
+                 offload: bool = False, shard: TPShard | None = None):
         self.cfg = cfg
         self.offload = offload
+        self.shard = shard
         g = torch.Generator(device=device)
         g.manual_seed(seed)
 
@@ -130,15 +125,23 @@ class LlamaWeights:
             return t.normal_(0.0, s, generator=g)
 
         self.emb = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device))
-        self.layout, self.layer_bytes = layer_layout(cfg)
+        self.layout, self.layer_bytes = layer_layout(cfg, shard)
         self.layer_bufs: list[torch.Tensor] = []
         self.layers = []
         tmp = torch.empty(self.layer_bytes, dtype=torch.uint8, device=device) if offload else None
+        # tensor parallel: draw the full layer (same draw order as the unsharded
+        # model, so every TP degree holds slices of the same weights), keep the shard
+        full_layout, full_bytes = layer_layout(cfg)
+        full_tmp = torch.empty(full_bytes, dtype=torch.uint8, device=device) if shard is not None else None
         for _ in range(cfg.layers):
             buf = tmp if offload else torch.empty(self.layer_bytes, dtype=torch.uint8, device=device)
             v = layer_views(buf, self.layout)
+            src = v if shard is None else layer_views(full_tmp, full_layout)
             for k in ("wqkv", "wo", "wg", "wu", "wd"):  # same draw order as the resident model
-                rnd_(v[k])
+                rnd_(src[k])
+            if shard is not None:
+                for k in ("wqkv", "wo", "wg", "wu", "wd"):
+                    v[k].copy_(shard.shard(cfg, k, src[k]))
             v["n1"].fill_(1.0)
             v["n2"].fill_(1.0)
             if offload:
@@ -149,9 +152,11 @@ class LlamaWeights:
             else:
                 self.layer_bufs.append(buf)
                 self.layers.append(v)
-        del tmp
+        del tmp, full_tmp
         self.nf = torch.ones(cfg.d, dtype=torch.bfloat16, device=device)
         self.lm = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device), std * lm_scale)
+        if shard is not None:
+            self.lm = shard.shard(cfg, "lm", self.lm)
 
     def to_cpu_fp32(self) -> dict:
         """fp32 CPU copy for the CPU reference forward (oracle/llama_ref.py)."""
@@ -215,15 +220,23 @@ class LayerStreamer:
 
 
 class _Buffers:
-    def __init__(self, cfg: LlamaConfig, n: int, device):
+    def __init__(self, cfg: LlamaConfig, n: int, device, shard: TPShard | None = None, reduce_bf16: bool = False):
         self.n = n
+        sh = TPShard(0, 1) if shard is None else shard
+        H = cfg.heads // sh.world
+        KVH = cfg.kv_heads // sh.world
         self.x = torch.empty((n, cfg.d), dtype=torch.float32, device=device)
+        # o / down projection output (TP: the partial sums that are all-reduced)
+        self.y = torch.empty((n, cfg.d), dtype=torch.bfloat16 if reduce_bf16 else torch.float32, device=device)
         self.h = torch.empty((n, cfg.d), dtype=torch.bfloat16, device=device)
-        self.qkv = torch.empty((n, cfg.qkv_out), dtype=torch.bfloat16, device=device)
-        self.q = torch.empty((n, cfg.heads * cfg.head_dim), dtype=torch.bfloat16, device=device)
-        self.att = torch.empty((n, cfg.heads * cfg.head_dim), dtype=torch.bfloat16, device=device)
-        self.act = torch.empty((n, cfg.ff), dtype=torch.bfloat16, device=device)
+        self.qkv = torch.empty((n, (H + 2 * KVH) * cfg.head_dim), dtype=torch.bfloat16, device=device)
+        self.q = torch.empty((n, H * cfg.head_dim), dtype=torch.bfloat16, device=device)
+        self.att = torch.empty((n, H * cfg.head_dim), dtype=torch.bfloat16, device=device)
+        self.act = torch.empty((n, cfg.ff // sh.world), dtype=torch.bfloat16, device=device)
         self.logits = torch.empty((n, cfg.vocab), dtype=torch.float32, device=device)
+        if sh.world > 1:  # vocab-parallel LM head: local slice + all-gather staging
+            self.logits_l = torch.empty((n, cfg.vocab // sh.world), dtype=torch.float32, device=device)
+            self.logits_g = torch.empty((sh.world, n, cfg.vocab // sh.world), dtype=torch.float32, device=device)
         self.tok = torch.empty(n, dtype=torch.int32, device=device)
         self.pos = torch.empty(n, dtype=torch.int32, device=device)
 
@@ -245,7 +258,12 @@ class LlamaModel(LanguageModel):
         synthetic: SyntheticBias | None = None,
         device=None,
         offload: bool = False,
+        tp=None,
+        reduce_bf16: bool = True,
     ):
+        """tp: a communicator (tp.NcclComm / tp.ThreadComm) -> this model is rank
+        tp.rank's tensor-parallel shard of the target (tp.py); the partial sums
+        of the o / down projections are all-reduced in bf16 (reduce_bf16) or fp32."""
         if isinstance(cfg, str):
             cfg = PRESETS[cfg]
         if cfg.head_dim != 128:
@@ -257,15 +275,22 @@ class LlamaModel(LanguageModel):
         self.vocab_size = cfg.vocab
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.seed = seed
-        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload)
+        self.tp = tp if (tp is not None and tp.world > 1) else None
+        self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else None
+        if self.shard is not None:
+            self.shard.check(cfg)
+        self.reduce_bf16 = bool(reduce_bf16 and self.tp is not None)
+        self.H = cfg.heads // (self.tp.world if self.tp else 1)  # local query / KV heads
+        self.KVH = cfg.kv_heads // (self.tp.world if self.tp else 1)
+        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload, shard=self.shard)
         self.streamer = LayerStreamer(self.w, self.device) if offload else None
         self.slots = max_ctx
-        self.kc = torch.zeros((cfg.layers, cfg.kv_heads, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
+        self.kc = torch.zeros((cfg.layers, self.KVH, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
         self.vc = torch.zeros_like(self.kc)
-        self.layer_stride = cfg.kv_heads * max_ctx * cfg.head_dim
+        self.layer_stride = self.KVH * max_ctx * cfg.head_dim
         self.cos, self.sin = _rope_tables(cfg, max_ctx + 64, self.device)
         self.max_tokens = max_tokens
-        self.buf = _Buffers(cfg, max_tokens, self.device)
+        self.buf = _Buffers(cfg, max_tokens, self.device, self.shard, self.reduce_bf16)
         self.synthetic = synthetic
         if synthetic is not None:
             g = torch.Generator(device=self.device)
@@ -298,19 +323,30 @@ class LlamaModel(LanguageModel):
         x, h = b.x[:n], b.h[:n]
         _lib.call("sx_embed", _lib.ptr(w.emb), _lib.ptr(tokens), n, cfg.d, _lib.ptr(x), st)
         p = _lib.ptr
+        y = b.y[:n]
+        tp, ybf = self.tp, int(self.reduce_bf16)
+        epi_y = K.EPI_BF16 if ybf else K.EPI_F32
+        H, KVH = self.H, self.KVH
         for li in range(cfg.layers):
             L = self.streamer.acquire(li) if self.streamer is not None else w.layers[li]
             kc, vc = self.kc[li], self.vc[li]
-            _lib.call("sx_rmsnorm", p(x), p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
+            if li == 0:
+                _lib.call("sx_rmsnorm", p(x), p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
+            else:  # residual add of the previous layer's down projection, fused into this norm
+                _lib.call("sx_add_rmsnorm", p(x), p(y), ybf, p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
             K.gemm(h, L["wqkv"], out=b.qkv[:n])
-            _lib.call("sx_rope_kv", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, cfg.heads, cfg.kv_heads,
+            _lib.call("sx_rope_kv", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, H, KVH,
                       p(self.cos), p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
             _lib.call("sx_tree_attention", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
-                      anc_base, p(anc_len), A, p(b.att), n, cfg.heads, cfg.kv_heads, st)
-            K.gemm(b.att[:n], L["wo"], out=x, epi=K.EPI_ADD_F32)
-            _lib.call("sx_rmsnorm", p(x), p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
+                      anc_base, p(anc_len), A, p(b.att), n, H, KVH, st)
+            K.gemm(b.att[:n], L["wo"], out=y, epi=epi_y)
+            if tp is not None:
+                tp.all_reduce_(y)
+            _lib.call("sx_add_rmsnorm", p(x), p(y), ybf, p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
             K.gemm(h, L["wg"], out=b.act[:n], epi=K.EPI_SWIGLU_BF16, w2=L["wu"])
-            K.gemm(b.act[:n], L["wd"], out=x, epi=K.EPI_ADD_F32)
+            K.gemm(b.act[:n], L["wd"], out=y, epi=epi_y)
+            if tp is not None:
+                tp.all_reduce_(y)
             if self.streamer is not None:
                 self.streamer.release(li)
         self.stats["forward_tokens"] += n
@@ -319,9 +355,17 @@ class LlamaModel(LanguageModel):
             return None
         m = n - logits_from
         hh = b.h[logits_from:n]
-        _lib.call("sx_rmsnorm", p(x[logits_from:]), p(w.nf), m, cfg.d, cfg.eps, p(hh), st)
+        _lib.call("sx_add_rmsnorm", p(x[logits_from:]), p(y[logits_from:]), ybf, p(w.nf), m, cfg.d, cfg.eps, p(hh), st)
         logits = b.logits[:m]
-        K.gemm(hh, w.lm, out=logits, epi=K.EPI_F32)
+        if tp is None:
+            K.gemm(hh, w.lm, out=logits, epi=K.EPI_F32)
+        else:  # vocab-parallel LM head: local slice, all-gather, interleave the slices into [m, V]
+            ll = b.logits_l[:m]
+            K.gemm(hh, w.lm, out=ll, epi=K.EPI_F32)
+            Vl = ll.shape[1]
+            gbuf = b.logits_g.view(-1)[: tp.world * m * Vl].view(tp.world, m, Vl)
+            tp.all_gather_(ll, gbuf)
+            logits.view(m, tp.world, Vl).copy_(gbuf.transpose(0, 1))
         if self.synthetic is not None:
             bi = self.bias_in[:m]
             torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)
@@ -415,7 +459,7 @@ class LlamaModel(LanguageModel):
                 dst = torch.tensor([c + 1 + i for i in range(len(rows))], dtype=torch.int32).to(self.device,
                                                                                                  non_blocking=True)
                 _lib.call("sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc), self.cfg.layers, self.layer_stride,
-                          self.slots, self.cfg.kv_heads, _lib.ptr(src), _lib.ptr(dst), len(rows), _lib.stream_ptr())
+                          self.slots, self.KVH, _lib.ptr(src), _lib.ptr(dst), len(rows), _lib.stream_ptr())
                 K.IO["h2d"] += 8 * len(rows)
             self.committed.extend(tree.nodes[r - 1].token for r in rows)
         elif getattr(tree, "draft_model", None) is self:
@@ -433,7 +477,7 @@ class LlamaModel(LanguageModel):
                 d_t = torch.tensor([c + 1 + i for i in range(len(src))], dtype=torch.int32).to(self.device,
                                                                                                 non_blocking=True)
                 _lib.call("sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc), self.cfg.layers, self.layer_stride,
-                          self.slots, self.cfg.kv_heads, _lib.ptr(s_t), _lib.ptr(d_t), len(src), _lib.stream_ptr())
+                          self.slots, self.KVH, _lib.ptr(s_t), _lib.ptr(d_t), len(src), _lib.stream_ptr())
                 K.IO["h2d"] += 8 * len(src)
             self.committed.extend(toks)
 

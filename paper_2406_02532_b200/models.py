@@ -22,6 +22,7 @@ in `llama.py`.
 from __future__ import annotations
 
 import json
+import threading
 from typing import Iterable, Sequence
 
 import numpy as np
@@ -90,17 +91,23 @@ def _normalize_rows(table: np.ndarray) -> np.ndarray:
 
 
 class _WorkspaceCache:
+    """Tree workspaces by (K, B, V, D), per host thread (independent generation
+    runs, e.g. tensor-parallel ranks as threads, never share device state)."""
+
     def __init__(self):
-        self._ws = {}
+        self._tls = threading.local()
 
     def get(self, budget: int, B: int, V: int, D: int) -> K.TreeWorkspace:
+        cache = getattr(self._tls, "ws", None)
+        if cache is None:
+            cache = self._tls.ws = {}
         key = (budget, B, V, D)
-        ws = self._ws.get(key)
+        ws = cache.get(key)
         if ws is None:
-            if len(self._ws) > 4:
-                self._ws.clear()
+            if len(cache) > 4:
+                cache.clear()
             ws = K.TreeWorkspace(budget, B, V, D)
-            self._ws[key] = ws
+            cache[key] = ws
         return ws
 
 

@@ -80,7 +80,7 @@ def test_gemm_pair_vs_single(cuda, mode, M, N, Kd):
         ref_sw = torch.nn.functional.silu(ref) * _ref(x, w2)
         assert (sw.float() - ref_sw).abs().max().item() < 2e-2 * max(1.0, ref_sw.abs().max().item())
     finally:
-        _lib.call("sx_gemm_set_pair_mode", 0)
+        _lib.call("sx_gemm_set_pair_mode", 1)  # library default: single-CTA
 
 
 @pytest.mark.parametrize("sched", [1, 2, 3, 0])

@@ -21,14 +21,14 @@ DRAFT_M = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--draft-m
 SHAPES = [
     # name, M (tokens), N (features), K, dual, epilogue
     ("70b.qkv", 1025, 10240, 8192, False, K.EPI_BF16),
-    ("70b.o", 1025, 8192, 8192, False, K.EPI_ADD_F32),
+    ("70b.o", 1025, 8192, 8192, False, K.EPI_F32),
     ("70b.gate_up", 1025, 28672, 8192, True, K.EPI_SWIGLU_BF16),
-    ("70b.down", 1025, 8192, 28672, False, K.EPI_ADD_F32),
+    ("70b.down", 1025, 8192, 28672, False, K.EPI_F32),
     ("70b.lm_head", 1025, 32000, 8192, False, K.EPI_F32),
     ("7b.qkv", DRAFT_M, 12288, 4096, False, K.EPI_BF16),
-    ("7b.o", DRAFT_M, 4096, 4096, False, K.EPI_ADD_F32),
+    ("7b.o", DRAFT_M, 4096, 4096, False, K.EPI_F32),
     ("7b.gate_up", DRAFT_M, 11008, 4096, True, K.EPI_SWIGLU_BF16),
-    ("7b.down", DRAFT_M, 4096, 11008, False, K.EPI_ADD_F32),
+    ("7b.down", DRAFT_M, 4096, 11008, False, K.EPI_F32),
     ("7b.lm_head", DRAFT_M, 32000, 4096, False, K.EPI_F32),
 ]
 
@@ -38,11 +38,14 @@ def main():
     ap.add_argument("--mode", type=int, default=0)
     ap.add_argument("--json", default=None)
     ap.add_argument("--sched", type=int, default=0, help="1 = whole tiles, 0 = auto (stream-K when waves are uneven)")
-    ap.add_argument("--draft-m", type=int, default=128)
+    ap.add_argument("--draft-m", type=int, default=128, help="(use --draft-m=N: read at import)")
+    ap.add_argument("--only", default="", help="shape-name prefix filter")
     a = ap.parse_args()
     _lib.call("sx_gemm_set_pair_mode", a.mode)
     res = []
     for name, M, N, Kd, dual, epi in SHAPES:
+        if not name.startswith(a.only):
+            continue
         x = torch.randn(M, Kd, device="cuda").bfloat16()
         # several weight copies so consecutive launches stream from HBM, not L2
         ncopy = max(1, int(2e9 // (N * Kd * 2 * (2 if dual else 1))))

@@ -1,0 +1,12 @@
+#!/bin/bash
+# One GPU session: smoke, GPU tests, C2 bench, per-kernel step profile, ncu launch list of the bench.
+set -x
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/nvsmi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 600 python tools/profile_step.py --json gpurun_out/kernels_c2.json > gpurun_out/profile_step.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_c2.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+  > gpurun_out/bench_ncu.log 2>&1
