@@ -132,6 +132,24 @@ SX_API int sx_argmax_rows(const void* rows, int row_kind, long long ld, int V, i
 SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u, int n, int* out,
                           cudaStream_t stream);
 
+/* ------------------------------------ KI1/KI2: SpecInfer baseline (8(f) row 1)
+ * build_stochastic's draws (pkg/src/speckit/tree.py:383-425): token[i] =
+ * sample(w[row_ids[i]], u[i]) and out_logq[i] = log w[row][token] (may be NULL).
+ * verify_specinfer (pkg/src/speckit/specinfer.py:53-96) as one CTA: tree rows
+ * trows (row 0 = anchor, row n+1 = node n); per row r the children are node ids
+ * [child_start[r], +child_count[r]) drawn from q[q_row[r]] (fp64 [*, ldq]);
+ * token / mult per node; uniforms = the "specinfer-accept" stream (n_u of them,
+ * an upper bound). out (device int[4 + max_path]): [path_len, bonus_token,
+ * uniforms_used, error (0 ok, 1 residual invalid, 2 missing q, 3 uniforms
+ * exhausted), path node ids...]. scratch: sx_row_scratch_bytes(V).
+ */
+SX_API int sx_sample_rows_idx(const double* w, long long ld, int V, const int* row_ids, const double* u, int n,
+                              int* out_tok, double* out_logq, cudaStream_t stream);
+SX_API int sx_specinfer_verify(const void* trows, int row_kind, long long ld, int V, const double* q, long long ldq,
+                               const int* q_row, const int* child_start, const int* child_count, const int* token,
+                               const int* mult, int max_path, const double* uniforms, int n_u, double temperature,
+                               double top_p, int* out, void* scratch, cudaStream_t stream);
+
 /* ------------------------------------------- KE / KA / KV3: model forward
  * Llama-shaped forward used for the draft rounds (stage 1) and the single
  * target pass over the flattened tree (stage 2); together they implement

@@ -210,6 +210,48 @@ def gen_logit_engine():
     return out
 
 
+def gen_specinfer_grid(n=60):
+    """SpecInfer baseline (specinfer.py:53-127, tree.py:383-425): stochastic
+    trees and full generate_specinfer runs on Markov pairs, plus logits-LM pairs
+    at V=32000 (canonical softmax rows, like the GPU)."""
+    from speckit import specinfer as ref_si
+
+    out = []
+    for i in range(n):
+        gen = np.random.default_rng(5000 + i)
+        V = int(gen.integers(3, 12))
+        sharp = float(gen.uniform(0.05, 2.0))
+        depth = int(gen.integers(1, 5))
+        branching = [int(gen.integers(1, 5))] + [int(gen.integers(1, 3)) for _ in range(depth - 1)]
+        t, p = [(0.6, 0.9), (1.0, 1.0), (0.0, 1.0), (1.3, 0.8)][i % 4]
+        target = speckit.make_synthetic(7000 + i, V, sharp)
+        draft = target.power_smoothed(0.6)
+        prompt = tuple(int(x) for x in gen.integers(0, V, size=3))
+        cfg = speckit.SamplingConfig(t, p, seed=i, max_new_tokens=20)
+        rng = speckit.CounterRng(i, ref_si.DRAFT_STREAM)
+        tree = ref_tree.build_stochastic(prompt, draft, branching, rng, cfg)
+        toks, st = ref_si.generate_specinfer(prompt, draft, target, branching, cfg)
+        out.append({"kind": "markov", "target_seed": 7000 + i, "V": V, "sharpness": sharp, "draft_power": 0.6,
+                    "branching": branching, "t": t, "top_p": p, "seed": i, "prompt": list(prompt),
+                    "tree": tree_record(tree), "mult": [nd.multiplicity for nd in tree.nodes],
+                    "tokens": toks, "target_calls": st.target_calls, "draft_calls": st.draft_calls,
+                    "accepted": st.accepted_per_iteration})
+    for ci in range(4):
+        V = 32000
+        dspec = {"vocab": V, "seed": 300 + ci, "scale": 1.6}
+        tspec = {"vocab": V, "seed": 300 + ci, "scale": 1.9}
+        draft, target = ReplayLM(V, logits_model(dspec)), ReplayLM(V, logits_model(tspec))
+        prompt = tuple(int(x) for x in np.random.default_rng(950 + ci).integers(0, V, size=6))
+        branching = ref_si.branching_for_budget([12, 24, 8, 40][ci], [4, 3, 2, 5][ci])
+        t, p = [(0.6, 0.9), (1.0, 1.0), (0.8, 0.95), (0.0, 1.0)][ci]
+        cfg = speckit.SamplingConfig(t, p, seed=ci, max_new_tokens=16)
+        toks, st = ref_si.generate_specinfer(prompt, draft, target, branching, cfg)
+        out.append({"kind": "logits", "draft": dspec, "target": tspec, "branching": branching, "t": t, "top_p": p,
+                    "seed": ci, "prompt": list(prompt), "tokens": toks, "target_calls": st.target_calls,
+                    "draft_calls": st.draft_calls, "accepted": st.accepted_per_iteration})
+    return out
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     jobs = {
@@ -218,6 +260,7 @@ def main():
         "engine_grid.json": gen_engine_grid,
         "logit_trees.json": gen_logit_trees,
         "logit_engine.json": gen_logit_engine,
+        "specinfer_grid.json": gen_specinfer_grid,
     }
     only = set(sys.argv[1:])
     for name, fn in jobs.items():

@@ -699,3 +699,158 @@ def stats_record(method, cfg, stats, budget, depth, batch_size) -> dict:
 def tree_topology(tree) -> list[tuple[int, int]]:
     """(parent, token) per node id: the integer part parity is asserted on."""
     return [(n.parent, n.token) for n in tree.nodes]
+
+
+# ---------------------------------------------------------------------------
+# specinfer.py + tree.py build_stochastic (the SpecInfer baseline, SURVEY 8(f) row 1)
+# ---------------------------------------------------------------------------
+
+SI_DRAFT_STREAM = "specinfer-draft"  # specinfer.py:26
+SI_ACCEPT_STREAM = "specinfer-accept"  # specinfer.py:27
+
+
+def _log_edges(q: np.ndarray) -> np.ndarray:
+    """tree.py:230-232 -- log of the scored distribution, zero -> -inf."""
+    out = np.full(q.shape, -np.inf)
+    nz = q > 0
+    out[nz] = ox_log(q[nz])
+    return out
+
+
+def build_stochastic(prefix, draft, branching, rng, warp=None, warp_scores: bool = True) -> DraftTree:
+    """tree.py:383-425 -- branching[d] i.i.d. samples per node at depth d from the
+    (warped) draft distribution; repeats merge into one node with multiplicity;
+    the sampled-from distribution of every expanded node is kept."""
+    if not branching:
+        raise ValueError("branching schedule must be non-empty")
+    if any(w < 1 for w in branching):
+        raise ValueError(f"branching widths must be >= 1, got {branching}")
+    tree = DraftTree(prefix)
+    tree.draft_dists = {}
+    level = [ROOT]
+    for width in branching:
+        if not level:
+            break
+        dists = draft.next_distributions([tree.full_prefix(n) for n in level])
+        tree.rounds += 1
+        next_level = []
+        for node_id, dist in zip(level, dists):
+            q = _scored_dist(dist, warp, warp_scores)
+            tree.draft_dists[node_id] = q
+            log_q = _log_edges(q)
+            for _ in range(width):
+                token = sample(q, rng)
+                existing = tree.child_with_token(node_id, token)
+                if existing is not None:
+                    tree.nodes[existing].multiplicity += 1
+                else:
+                    next_level.append(tree.add_child(node_id, token, float(log_q[token])))
+        level = next_level
+    return tree
+
+
+def validate_distribution(p: np.ndarray) -> np.ndarray:
+    """sampling.py:44-56 (sum in the canonical order)."""
+    p = np.asarray(p, dtype=np.float64)
+    if p.ndim != 1 or p.size == 0:
+        raise ValueError("distribution must be a non-empty 1-D array")
+    if np.any(p < 0):
+        raise ValueError("distribution has negative entries")
+    total = canon_sum(p)
+    if abs(total - 1.0) > DIST_ATOL:
+        raise ValueError(f"distribution sums to {total!r}, expected 1 within {DIST_ATOL}")
+    return p
+
+
+def residual(p: np.ndarray, q: np.ndarray) -> np.ndarray:
+    """specinfer.py:42-50 -- normalize(max(p - q, 0)); p itself when nothing is left."""
+    diff = np.maximum(p - q, 0.0)
+    total = canon_sum(diff)
+    if total <= 0.0:
+        return np.array(p, dtype=np.float64, copy=True)
+    return validate_distribution(diff / total)
+
+
+@dataclass
+class VerifyOutcome:
+    """specinfer.py:30-39"""
+
+    accepted_path: list[int]
+    bonus_token: int
+
+    @property
+    def tokens_emitted(self) -> int:
+        return len(self.accepted_path) + 1
+
+
+def verify_specinfer(tree: DraftTree, target, warp: SamplingConfig, rng: CounterRng) -> VerifyOutcome:
+    """specinfer.py:53-96 -- multi-round rejection walk: child after child (each
+    `multiplicity` times) is accepted with probability min(1, p[x]/q[x]); a
+    rejection moves p to the residual; no acceptance -> bonus token from p."""
+    if getattr(tree, "draft_dists", None) is None:
+        raise ValueError("tree carries no draft distributions; build it with build_stochastic")
+    flat = flatten(tree)
+    prefixes = [tree.prefix] + [tree.full_prefix(i) for i in flat.order]
+    target_dists = target.next_distributions(prefixes)
+    node = ROOT
+    path: list[int] = []
+    p = apply_warp(target_dists[0], warp)
+    while True:
+        accepted = None
+        for child_id in tree.children_of(node):
+            child = tree.nodes[child_id]
+            q = tree.draft_dists[node]
+            for _ in range(child.multiplicity):
+                ratio = min(1.0, p[child.token] / q[child.token])
+                if rng.uniform() < ratio:
+                    accepted = child_id
+                    break
+                p = residual(p, q)
+            if accepted is not None:
+                break
+        if accepted is None:
+            return VerifyOutcome(accepted_path=path, bonus_token=sample(p, rng))
+        path.append(accepted)
+        node = accepted
+        p = apply_warp(target_dists[accepted + 1], warp)
+
+
+def generate_specinfer(prompt, draft, target, branching, cfg: SamplingConfig):
+    """specinfer.py:99-127"""
+    prompt = tuple(prompt)
+    rng_draft = CounterRng(cfg.seed, SI_DRAFT_STREAM)
+    rng_accept = CounterRng(cfg.seed, SI_ACCEPT_STREAM)
+    stats = GenStats()
+    tokens: list[int] = []
+    while len(tokens) < cfg.max_new_tokens:
+        tree = build_stochastic(prompt + tuple(tokens), draft, branching, rng_draft, cfg)
+        stats.draft_calls += tree.rounds
+        outcome = verify_specinfer(tree, target, cfg, rng_accept)
+        stats.target_calls += 1
+        emitted = [tree.nodes[i].token for i in outcome.accepted_path]
+        emitted.append(outcome.bonus_token)
+        emitted = emitted[: cfg.max_new_tokens - len(tokens)]
+        tokens.extend(emitted)
+        stats.accepted_per_iteration.append(len(emitted))
+    stats.tokens_generated = len(tokens)
+    return tokens, stats
+
+
+def branching_for_budget(budget: int, depth: int) -> list[int]:
+    """specinfer.py:130-143 -- `width` stems of length `depth`."""
+    if budget < 1:
+        raise ValueError(f"budget must be >= 1, got {budget}")
+    if depth < 1:
+        raise ValueError(f"depth must be >= 1, got {depth}")
+    depth = min(depth, budget)
+    width = max(1, round(budget / depth))
+    return [width] + [1] * (depth - 1)
+
+
+def schedule_size(branching: list[int]) -> int:
+    """specinfer.py:146-153"""
+    total, level = 0, 1
+    for width in branching:
+        level *= width
+        total += level
+    return total

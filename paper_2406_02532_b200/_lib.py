@@ -57,6 +57,12 @@ SIGNATURES: dict[str, tuple] = {
     "sx_softmax_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _c_ll, _vp]),
     "sx_argmax_rows": (_c_int, [_vp, _c_int, _c_ll, _c_int, _c_int, _vp, _vp]),
     "sx_sample_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _vp]),
+    "sx_sample_rows_idx": (_c_int, [_vp, _c_ll, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp]),
+    "sx_specinfer_verify": (
+        _c_int,
+        [_vp, _c_int, _c_ll, _c_int, _vp, _c_ll, _vp, _vp, _vp, _vp, _vp, _c_int, _vp, _c_int, ctypes.c_double,
+         ctypes.c_double, _vp, _vp, _vp],
+    ),
     "sx_embed": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
     "sx_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
     "sx_add_rmsnorm": (_c_int, [_vp, _vp, _c_int, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),

@@ -565,12 +565,13 @@ static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
     mode = sched_req - 1;
   } else if (sched_req != 1 && eff < 0.95) {
     // several token tiles: waves + K-split tail (keeps the weight tile shared in
-    // L2). One token tile: stream-K pays off only for thin token tiles (M <= 128:
+    // L2). One token tile: stream-K pays off only for thin token tiles (M <= 64:
     // 34 -> 19 us on a 4096 x 4096 projection at M = 2, 216 -> 104 us at M = 64,
-    // K = 32768; neutral-to-worse at M = 256, tools/gemm_sched_micro.py).
+    // K = 32768, tools/gemm_sched_micro.py; at M = 128 / 256 whole tiles win on
+    // every 7B draft projection, e.g. qkv 37 -> 32 us, tools/gemm_bench.py).
     if (p.tiles_t > 1)
       mode = 2;
-    else if (M <= 128)
+    else if (M <= 64)
       mode = 1;
   }
   if (mode == 2) {

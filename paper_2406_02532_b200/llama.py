@@ -302,7 +302,11 @@ class LlamaModel(LanguageModel):
             self.bias_in = torch.empty((max_tokens, synthetic.rank), dtype=torch.bfloat16, device=self.device)
         self.committed: list[int] = []  # tokens whose KV is in slots [0, len)
         self.record: list[dict] | None = None  # test hook: per build, prefix -> fp32 logits row
-        self.use_graphs = True  # draft rounds as CUDA graphs (fixed B rows)
+        self.use_graphs = True  # draft rounds and one-token chains as CUDA graphs
+        self._one_args = torch.zeros(4, dtype=torch.int32, device=self.device)
+        self._g1 = None
+        self._g1_out = None
+        self._g1_warm = False
         LlamaModel._serial += 1
         self._uid = LlamaModel._serial
         self.stats = {"forward_tokens": 0, "forwards": 0}
@@ -383,8 +387,39 @@ class LlamaModel(LanguageModel):
         del self.committed[c:]
         return c, list(prefix[c:])
 
+    def _chain_one(self, c: int, token: int) -> torch.Tensor:
+        """One token at slot/position c with logits -- the draft's first round of
+        every tree (the root) and each step of sequential decoding -- replayed as
+        a CUDA graph (per-token scalars live in a device array, so one capture
+        serves every c). The first call runs eagerly to settle kernel attributes
+        and tensor maps, the second captures."""
+        if c + 1 > self.slots:
+            raise RuntimeError(f"KV cache full ({self.slots} slots)")
+        a = self._one_args
+        a.copy_(torch.tensor([token, c, c, c + 1], dtype=torch.int32), non_blocking=True)
+        K.IO["h2d"] += 16
+        tok, pos, slot, dl = a[0:1], a[1:2], a[2:3], a[3:4]
+        if self._g1 is None and self._g1_warm:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._g1_out = self.forward(1, tok, pos, 0, slot, 0, dl, 0, None, 0, None, 0, 0)
+            self._g1 = g
+        if self._g1 is not None:
+            self._g1.replay()
+            out = self._g1_out
+            self.stats["forward_tokens"] += 1
+            self.stats["forwards"] += 1
+        else:
+            out = self.forward(1, tok, pos, 0, slot, 0, dl, 0, None, 0, None, 0, 0)
+            self._g1_warm = True
+        self.committed.append(int(token))
+        return out
+
     def _chain(self, c: int, toks: Sequence[int], want_logits: bool) -> torch.Tensor | None:
         """Causal chain of tokens at slots/positions c.. (prefill, catch-up)."""
+        if len(toks) == 1 and want_logits and self.use_graphs and self.streamer is None and self.tp is None:
+            return self._chain_one(c, toks[0])
         out = None
         i = 0
         step = self.buf.n

@@ -167,3 +167,35 @@ def test_logit_engine_matches_reference():
             assert got == run["tokens"] == run["sequential"]
             assert stats.target_calls == run["target_calls"] and stats.draft_calls == run["draft_calls"]
             assert stats.accepted_per_iteration == run["accepted"]
+
+
+def test_specinfer_grid_matches_reference():
+    """SpecInfer baseline (specinfer.py:53-127): the oracle's stochastic trees
+    (topology, edge log-probs, multiplicities) and full generate_specinfer runs
+    equal the reference's on Markov and V=32000 logits pairs."""
+    for i, rec in enumerate(load("specinfer_grid.json")):
+        if rec["kind"] == "markov":
+            target = ox.make_synthetic(rec["target_seed"], rec["V"], rec["sharpness"])
+            draft = target.power_smoothed(rec["draft_power"])
+        else:
+            draft, target = logits_lm(rec["draft"]), logits_lm(rec["target"])
+        cfg = ox.SamplingConfig(rec["t"], rec["top_p"], seed=rec["seed"], max_new_tokens=len(rec["tokens"]))
+        prompt = tuple(rec["prompt"])
+        if "tree" in rec:
+            tree = ox.build_stochastic(prompt, draft, rec["branching"], ox.CounterRng(rec["seed"], ox.SI_DRAFT_STREAM), cfg)
+            assert [n.parent for n in tree.nodes] == rec["tree"]["parent"], i
+            assert [n.token for n in tree.nodes] == rec["tree"]["token"], i
+            assert [n.multiplicity for n in tree.nodes] == rec["mult"], i
+            for a, b in zip([n.edge_logprob for n in tree.nodes], rec["tree"]["edge"]):
+                assert a == b or abs(a - b) <= 1e-12 * max(1.0, abs(b)), i
+        toks, st = ox.generate_specinfer(prompt, draft, target, rec["branching"], cfg)
+        assert toks == rec["tokens"], i
+        assert st.accepted_per_iteration == rec["accepted"] and st.draft_calls == rec["draft_calls"], i
+
+
+def test_specinfer_schedules():
+    assert ox.branching_for_budget(12, 4) == [3, 1, 1, 1]
+    assert ox.schedule_size([3, 1, 1, 1]) == 12
+    assert ox.branching_for_budget(5, 8) == [1, 1, 1, 1, 1]
+    with pytest.raises(ValueError):
+        ox.branching_for_budget(0, 3)
