@@ -14,6 +14,8 @@ from .models import LanguageModel, MarkovModel, TabularModel, make_synthetic, mo
 from .rng import CounterRng
 from .sampling import SamplingConfig, apply_warp, sample, validate_distribution
 from .tree import ROOT, BuilderParams, DraftNode, DraftTree, FlattenedTree, build_sssp, flatten
+from .specinfer import (VerifyOutcome, branching_for_budget, build_stochastic, generate_specinfer, schedule_size,
+                        verify_specinfer)
 
 __version__ = "0.1.0"
 
@@ -32,6 +34,12 @@ __all__ = [
     "TabularModel",
     "apply_warp",
     "build_sssp",
+    "build_stochastic",
+    "branching_for_budget",
+    "generate_specinfer",
+    "schedule_size",
+    "verify_specinfer",
+    "VerifyOutcome",
     "flatten",
     "generate_sequential",
     "generate_specexec",

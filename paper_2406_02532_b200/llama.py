@@ -34,7 +34,7 @@ from . import _lib
 from . import kernels as K
 from .models import LanguageModel, _WS, _check_prefix
 from .tp import TPShard
-from .tree import BuilderParams
+from .tree import BuilderParams, tree_tables
 
 
 @dataclass(frozen=True)
@@ -460,6 +460,10 @@ class LlamaModel(LanguageModel):
         _check_prefix(prefix, self.vocab_size)
         return _LlamaDraftSession(self, tuple(prefix), params)
 
+    def stochastic_session(self, prefix, max_nodes: int, max_depth: int) -> "_LlamaStochastic":
+        _check_prefix(prefix, self.vocab_size)
+        return _LlamaStochastic(self, tuple(prefix), max_nodes, max_depth)
+
     def tree_rows(self, tree) -> torch.Tensor:
         """ONE target pass over the anchor + every tree node: fp32 logits [n+1, V]."""
         prefix = tree.prefix
@@ -471,8 +475,15 @@ class LlamaModel(LanguageModel):
         if c + n > self.slots:
             raise RuntimeError(f"KV cache full: need {c + n} slots, have {self.slots}")
         ws = tree.workspace
-        anc, anc_len, depth, tok = ws.final_tables(n)
-        logits = self.forward(n, tok, depth, c, None, c, None, c, anc, c, anc_len, ws.D + 1, 0)
+        if ws is not None:
+            anc, anc_len, depth, tok = ws.final_tables(n)
+            A = ws.D + 1
+        else:  # host-built tree (SpecInfer): same tables, uploaded
+            tabs = tree_tables(tree)
+            anc, anc_len, depth, tok = (torch.from_numpy(a).to(self.device, non_blocking=True) for a in tabs)
+            A = tabs[0].shape[1]
+            K.IO["h2d"] += sum(a.nbytes for a in tabs)
+        logits = self.forward(n, tok, depth, c, None, c, None, c, anc, c, anc_len, A, 0)
         self.committed.append(prefix[-1])  # the root's KV is at slot c = its position
         tree.target_base = c
         if self.record is not None:
@@ -623,3 +634,72 @@ class _LlamaDraftSession:
         tree.draft_root_slot = self.root_slot
         tree.host_slot = tree.device_slot.cpu().tolist()
         K.IO["d2h"] += 4 * len(tree.host_slot)
+
+
+class _LlamaStochastic:
+    """Level-by-level draft rows for SpecInfer's stochastic builder
+    (tree.py:383-425): the root row by the usual catch-up chain, then each level
+    in one forward where node i sits at KV slot root+1+i and attends the
+    committed prefix, the root and its ancestors (host-built ancestor lists)."""
+
+    def __init__(self, model: LlamaModel, prefix: tuple[int, ...], max_nodes: int, max_depth: int):
+        self.m = model
+        self.prefix = prefix
+        c, pending = model._sync(prefix)
+        self.c, self.pending = c, pending
+        self.root_slot = c + len(pending) - 1
+        if self.root_slot + 1 + max_nodes > model.slots:
+            raise RuntimeError(f"draft KV slots exhausted ({self.root_slot + 1 + max_nodes} > {model.slots})")
+        self.A = max_depth + 1
+        self.expanded: set[int] = set()
+        self.rec = None
+        if model.record is not None:  # replay-oracle hook: prefix -> fp32 logits of this build
+            self.rec = {}
+            model.record.append(self.rec)
+
+    def level_rows(self, tree, level: list[int]) -> torch.Tensor:
+        out = self._level_rows(tree, level)
+        if self.rec is not None:
+            rows = out.cpu().numpy()
+            for j, nid in enumerate(level):
+                self.rec[tree.full_prefix(nid)] = rows[j].copy()
+        return out
+
+    def _level_rows(self, tree, level: list[int]) -> torch.Tensor:
+        m = self.m
+        if level == [-1]:
+            return m._chain(self.c, self.pending, True)
+        n = len(level)
+        if n > m.buf.n:
+            raise RuntimeError(f"SpecInfer level of {n} nodes exceeds max_tokens={m.buf.n}")
+        anc = np.zeros((n, self.A), dtype=np.int32)
+        alen = np.zeros(n, dtype=np.int32)
+        depth = np.zeros(n, dtype=np.int32)
+        slot = np.zeros(n, dtype=np.int32)
+        tok = np.zeros(n, dtype=np.int32)
+        rs = self.root_slot
+        for j, nid in enumerate(level):
+            chain = []
+            x = nid
+            while x != -1:
+                chain.append(rs + 1 + x)
+                x = tree.nodes[x].parent
+            chain.append(rs)
+            chain.reverse()
+            anc[j, : len(chain)] = chain
+            alen[j] = len(chain)
+            depth[j] = tree.nodes[nid].depth
+            slot[j] = 1 + nid
+            tok[j] = tree.nodes[nid].token
+        dev = m.device
+        t_anc, t_alen, t_depth, t_slot, t_tok = (torch.from_numpy(a).to(dev, non_blocking=True)
+                                                  for a in (anc, alen, depth, slot, tok))
+        K.IO["h2d"] += int(anc.nbytes + 4 * 4 * n)
+        self.expanded.update(level)
+        return m.forward(n, t_tok, t_depth, rs, t_slot, rs, None, rs, t_anc, 0, t_alen, self.A, 0)
+
+    def finish(self, tree) -> None:
+        """KV bookkeeping for commit_walk: nodes whose KV the draft computed."""
+        tree.draft_model = self.m
+        tree.draft_root_slot = self.root_slot
+        tree.host_slot = [self.root_slot + 1 + i if i in self.expanded else -1 for i in range(len(tree.nodes))]

@@ -133,6 +133,19 @@ class _TableSession:
         tree.ctx0 = self.ctx0
 
 
+class _TableStochastic:
+    """Level rows for SpecInfer's stochastic builder (exact tables)."""
+
+    def __init__(self, model: "MarkovModel"):
+        self.model = model
+
+    def level_rows(self, tree, level: list[int]) -> torch.Tensor:
+        return self.model.rows_for_prefixes([tree.full_prefix(n) for n in level])
+
+    def finish(self, tree) -> None:
+        pass
+
+
 class MarkovModel(LanguageModel):
     """Order-k Markov chain over a dense table (models.py:100-151), table in HBM."""
 
@@ -188,8 +201,21 @@ class MarkovModel(LanguageModel):
         _check_prefix(prefix, self.vocab_size)
         return _TableSession(self, prefix, params)
 
+    def rows_for_prefixes(self, prefixes) -> torch.Tensor:
+        """fp64 rows [n, V] on the device for arbitrary prefixes (a gather of table rows)."""
+        idx = [self._row_index(tuple(p)) for p in prefixes]
+        sel = torch.tensor(idx, dtype=torch.long).to(self.table_dev.device, non_blocking=True)
+        return self.table_dev.index_select(0, sel)
+
+    def stochastic_session(self, prefix: Prefix, max_nodes: int, max_depth: int) -> "_TableStochastic":
+        _check_prefix(prefix, self.vocab_size)
+        return _TableStochastic(self)
+
     def tree_rows(self, tree) -> torch.Tensor:
-        """Rows for the anchor and every node of a tree built on the GPU."""
+        """Rows for the anchor and every node of a tree (GPU-built, or host-built
+        like SpecInfer's stochastic trees)."""
+        if tree.workspace is None:
+            return self.rows_for_prefixes([tree.prefix] + [tree.full_prefix(nd.node_id) for nd in tree.nodes])
         n = len(tree.nodes)
         ws = tree.workspace
         ids = torch.arange(-1, n, dtype=torch.int32, device=ws.device)

@@ -183,6 +183,29 @@ def score_mode(warp: SamplingConfig | None, warp_scores: bool) -> tuple[int, flo
     return SCORE_WARP, float(warp.temperature), float(warp.top_p)
 
 
+def tree_tables(tree: DraftTree) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """Host-built trees (e.g. SpecInfer's stochastic trees): the ancestor tables
+    of the flattened tree (tree.py:208-219) in the layout the GPU builder's
+    finalize produces -- per row (0 = root, i+1 = node i): ancestor rows
+    root-first ending with itself [n+1, D+1], their count, depth and token."""
+    n = len(tree.nodes)
+    A = tree.max_depth() + 1
+    anc = np.zeros((n + 1, A), dtype=np.int32)
+    alen = np.ones(n + 1, dtype=np.int32)
+    depth = np.zeros(n + 1, dtype=np.int32)
+    tok = np.zeros(n + 1, dtype=np.int32)
+    tok[0] = tree.prefix[-1] if tree.prefix else 0
+    for nd in tree.nodes:  # parents have smaller ids
+        r, pr = nd.node_id + 1, nd.parent + 1
+        k = alen[pr]
+        anc[r, :k] = anc[pr, :k]
+        anc[r, k] = r
+        alen[r] = k + 1
+        depth[r] = nd.depth
+        tok[r] = nd.token
+    return anc, alen, depth, tok
+
+
 def _tree_from_device(prefix: Prefix, parent, token, edge, rounds: int) -> DraftTree:
     tree = DraftTree(prefix)
     for p, t, e in zip(parent.tolist(), token.tolist(), edge.tolist()):
