@@ -60,7 +60,10 @@ enum {
   SX_EPI_BF16 = 0,        /* out bf16  = acc                       */
   SX_EPI_F32 = 1,         /* out fp32  = acc                       */
   SX_EPI_ADD_F32 = 2,     /* out fp32 += acc (residual stream)     */
-  SX_EPI_SWIGLU_BF16 = 3  /* out bf16  = silu(acc(W)) * acc(W2)    */
+  SX_EPI_SWIGLU_BF16 = 3, /* out bf16  = silu(acc(W)) * acc(W2)    */
+  SX_EPI_SWIGLU_IL = 4    /* W = [gate; up] interleaved in 64-row blocks (rows 128j..128j+63 =
+                             gate features 64j.., rows 128j+64.. = up of the same features);
+                             out bf16 [M, N/2] = silu(gate) * up   (N % 128 == 0)      */
 };
 /* 0 = auto (default: CTA-pair cta_group::2 tiles for M >= 256 tokens), 1 = single-CTA only, 2 = pair when legal */
 SX_API int sx_gemm_set_pair_mode(int mode);

@@ -81,7 +81,7 @@ SIGNATURES: dict[str, tuple] = {
 ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1
 SCORE_RAW, SCORE_ARGMAX, SCORE_WARP = 0, 1, 2
 
-EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16 = 0, 1, 2, 3
+EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL = 0, 1, 2, 3, 4
 
 _lib = None
 

@@ -9,11 +9,12 @@
 //                for causal prefill chunks dense_len = own slot + 1), and
 //   anc[0..n)  : an explicit list of extra KV slots (root + tree ancestors +
 //                itself; <= max_depth + 1 entries).
-// The dense part is a flash-attention main loop on tensor cores (bf16
-// mma.sync m16n8k16, fp32 online softmax, cp.async double-buffered K/V tiles,
-// XOR-swizzled shared memory); the sparse ancestor part (<= D+1 keys per row)
-// is merged into the same online-softmax state on CUDA cores. GQA: one CTA
-// serves one KV head and 64 query rows = (64 / G) tokens x G heads.
+// One flash-attention main loop on tensor cores (bf16 mma.sync m16n8k16, fp32
+// online softmax, cp.async double-buffered K/V tiles, XOR-swizzled shared
+// memory) covers both parts: the dense tiles of the committed prefix, then
+// "ancestor tiles" gathered by slot -- the concatenated ancestor lists of the
+// CTA's tokens (<= D+1 keys each), each row masked to its own segment. GQA:
+// one CTA serves one KV head and 64 query rows = (64 / G) tokens x G heads.
 #include "capi_util.h"
 #include "common.cuh"
 #include "specexec_b200.h"
@@ -77,22 +78,21 @@ SX_DEV uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+constexpr int kMaxAncKeys = 64 * 32;  // QB tokens x A ancestors (A <= 32)
+
 struct AttnSmem {
   uint8_t qs[kAttRows * 256];
   uint8_t ks[2][kKeyTile * 256];
   uint8_t vs[2][kKeyTile * 256];
   int dlen[kAttRows];
-  float m[kAttRows];
-  float l[kAttRows];
+  int seg[kAttRows + 1];  // per token of the CTA: start of its ancestor segment
+  int aslot[kMaxAncKeys];
   int maxlen;
 };
-
-constexpr size_t kOStageOff = (sizeof(AttnSmem) + 127) & ~size_t(127);
 
 __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   AttnSmem& sm = *reinterpret_cast<AttnSmem*>(smem_raw);
-  float* ostage = reinterpret_cast<float*>(smem_raw + kOStageOff);  // [64][128] fp32, 128-B aligned
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kvh = blockIdx.y;
@@ -108,6 +108,22 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
     sm.dlen[tid] = dl;
     atomicMax(&sm.maxlen, dl);
   }
+  if (tid == 0) {  // ancestor segments of the CTA's tokens (prefix sum, <= 64 tokens)
+    int acc = 0;
+    for (int i = 0; i < a.QB; ++i) {
+      sm.seg[i] = acc;
+      const int t = t0 + i;
+      acc += (t < a.N && a.anc_len) ? a.anc_len[t] : 0;
+    }
+    sm.seg[a.QB] = acc;
+  }
+  __syncthreads();
+  const int n_anc = sm.seg[a.QB];
+  for (int i = tid; i < a.QB * a.A; i += blockDim.x) {
+    const int tl = i / a.A, j = i % a.A, t = t0 + tl;
+    if (t < a.N && j < sm.seg[tl + 1] - sm.seg[tl])
+      sm.aslot[sm.seg[tl] + j] = a.anc_base + a.anc[(long long)t * a.A + j];
+  }
   // Q tile: rows r = token-major, head-minor
   const uint32_t qs = smem_u32(sm.qs);
   for (int i = tid; i < kAttRows * 16; i += blockDim.x) {
@@ -119,15 +135,26 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
   cp_async_commit();
   __syncthreads();
   const int maxlen = sm.maxlen;
-  const int ntiles = (maxlen + kKeyTile - 1) / kKeyTile;
+  const int ndense = (maxlen + kKeyTile - 1) / kKeyTile;
+  const int ntiles = ndense + (n_anc + kKeyTile - 1) / kKeyTile;
 
+  // tiles [0, ndense): committed slots; tiles [ndense, ntiles): ancestor slots
   auto load_kv = [&](int tile, int buf) {
     const uint32_t ks = smem_u32(sm.ks[buf]), vs = smem_u32(sm.vs[buf]);
     for (int i = tid; i < kKeyTile * 16; i += blockDim.x) {
       const int r = i >> 4, c = i & 15;
-      const int key = tile * kKeyTile + r;
-      const bool ok = key < maxlen;
-      const long long off = (long long)(ok ? key : 0) * kHd + c * 8;
+      long long slot;
+      bool ok;
+      if (tile < ndense) {
+        const int key = tile * kKeyTile + r;
+        ok = key < maxlen;
+        slot = ok ? key : 0;
+      } else {
+        const int k = (tile - ndense) * kKeyTile + r;
+        ok = k < n_anc;
+        slot = ok ? sm.aslot[k] : 0;
+      }
+      const long long off = slot * kHd + c * 8;
       cp_async16(ks + swz(r, c * 8), kbase + off, ok ? 16 : 0);
       cp_async16(vs + swz(r, c * 8), vbase + off, ok ? 16 : 0);
     }
@@ -153,6 +180,8 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
     ldsm_x4(qs + swz(r, c), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
   }
   const int dl_a = sm.dlen[ra], dl_b = sm.dlen[rb];
+  const int sa_lo = sm.seg[ra / a.G], sa_hi = sm.seg[ra / a.G + 1];
+  const int sb_lo = sm.seg[rb / a.G], sb_hi = sm.seg[rb / a.G + 1];
 
   for (int kt = 0; kt < ntiles; ++kt) {
     const int buf = kt & 1;
@@ -178,15 +207,19 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
         mma_bf16(s[nt], qf[ks + 1], b2, b3);
       }
     }
-    // mask + scale + online softmax
+    // mask (dense: key < dense_len; ancestors: the row's own segment) + scale + online softmax
+    const bool dense = kt < ndense;
+    const int kb = dense ? kt * kKeyTile : (kt - ndense) * kKeyTile;
+    const int lo_a = dense ? 0 : sa_lo, hi_a = dense ? dl_a : sa_hi;
+    const int lo_b = dense ? 0 : sb_lo, hi_b = dense ? dl_b : sb_hi;
     float mx_a = -INFINITY, mx_b = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
-      const int key = kt * kKeyTile + nt * 8 + (lane & 3) * 2;
-      s[nt][0] = key < dl_a ? s[nt][0] * a.scale_log2 : -INFINITY;
-      s[nt][1] = key + 1 < dl_a ? s[nt][1] * a.scale_log2 : -INFINITY;
-      s[nt][2] = key < dl_b ? s[nt][2] * a.scale_log2 : -INFINITY;
-      s[nt][3] = key + 1 < dl_b ? s[nt][3] * a.scale_log2 : -INFINITY;
+      const int key = kb + nt * 8 + (lane & 3) * 2;
+      s[nt][0] = (key >= lo_a && key < hi_a) ? s[nt][0] * a.scale_log2 : -INFINITY;
+      s[nt][1] = (key + 1 >= lo_a && key + 1 < hi_a) ? s[nt][1] * a.scale_log2 : -INFINITY;
+      s[nt][2] = (key >= lo_b && key < hi_b) ? s[nt][2] * a.scale_log2 : -INFINITY;
+      s[nt][3] = (key + 1 >= lo_b && key + 1 < hi_b) ? s[nt][3] * a.scale_log2 : -INFINITY;
       mx_a = fmaxf(mx_a, fmaxf(s[nt][0], s[nt][1]));
       mx_b = fmaxf(mx_b, fmaxf(s[nt][2], s[nt][3]));
     }
@@ -242,61 +275,16 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
     __syncthreads();
   }
 
-  // stage dense state for the sparse (ancestor) phase
+  // normalise and store: rows ra / rb, dims nd*8 + (lane&3)*2 (+1)
+  const float inv_a = l_a > 0.f ? 1.f / l_a : 0.f, inv_b = l_b > 0.f ? 1.f / l_b : 0.f;
+  const int ta = t0 + ra / a.G, tb = t0 + rb / a.G;
+  __nv_bfloat16* da = a.out + ((long long)ta * a.H + kvh * a.G + ra % a.G) * kHd;
+  __nv_bfloat16* db = a.out + ((long long)tb * a.H + kvh * a.G + rb % a.G) * kHd;
 #pragma unroll
   for (int nd = 0; nd < 16; ++nd) {
     const int c = nd * 8 + (lane & 3) * 2;
-    ostage[ra * kHd + c] = o[nd][0];
-    ostage[ra * kHd + c + 1] = o[nd][1];
-    ostage[rb * kHd + c] = o[nd][2];
-    ostage[rb * kHd + c + 1] = o[nd][3];
-  }
-  if ((lane & 3) == 0) {
-    sm.m[ra] = m_a;
-    sm.m[rb] = m_b;
-    sm.l[ra] = l_a;
-    sm.l[rb] = l_b;
-  }
-  __syncthreads();
-
-  // sparse ancestors (CUDA cores), one warp per row; lane owns dims 4*lane..4*lane+3
-  for (int r = warp; r < kAttRows; r += kAttWarps) {
-    const int t = t0 + r / a.G;
-    if (t >= a.N) continue;
-    const int h = kvh * a.G + r % a.G;
-    float m = sm.m[r], l = sm.l[r];
-    float4 acc = reinterpret_cast<const float4*>(ostage + r * kHd)[lane];
-    const uint2 qraw = reinterpret_cast<const uint2*>(a.q + ((long long)t * a.H + h) * kHd)[lane];
-    const float2 q01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qraw.x));
-    const float2 q23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qraw.y));
-    const int na = a.anc_len ? a.anc_len[t] : 0;
-    for (int j = 0; j < na; ++j) {
-      const long long slot = a.anc_base + a.anc[(long long)t * a.A + j];
-      const uint2 kraw = reinterpret_cast<const uint2*>(kbase + slot * kHd)[lane];
-      const float2 k01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kraw.x));
-      const float2 k23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kraw.y));
-      float d = q01.x * k01.x + q01.y * k01.y + q23.x * k23.x + q23.y * k23.y;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffff, d, off);
-      const float sc = d * a.scale_log2;
-      const float mn = fmaxf(m, sc);
-      const float corr = exp2f(m - mn), p = exp2f(sc - mn);
-      const uint2 vraw = reinterpret_cast<const uint2*>(vbase + slot * kHd)[lane];
-      const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vraw.x));
-      const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vraw.y));
-      acc.x = acc.x * corr + p * v01.x;
-      acc.y = acc.y * corr + p * v01.y;
-      acc.z = acc.z * corr + p * v23.x;
-      acc.w = acc.w * corr + p * v23.y;
-      l = l * corr + p;
-      m = mn;
-    }
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* dst = a.out + ((long long)t * a.H + h) * kHd;
-    uint2 packed;
-    packed.x = pack_bf16(acc.x * inv, acc.y * inv);
-    packed.y = pack_bf16(acc.z * inv, acc.w * inv);
-    reinterpret_cast<uint2*>(dst)[lane] = packed;
+    if (ta < a.N) *reinterpret_cast<uint32_t*>(da + c) = pack_bf16(o[nd][0] * inv_a, o[nd][1] * inv_a);
+    if (tb < a.N) *reinterpret_cast<uint32_t*>(db + c) = pack_bf16(o[nd][2] * inv_b, o[nd][3] * inv_b);
   }
 }
 
@@ -329,7 +317,9 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   a.G = G;
   a.QB = kAttRows / G;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)kHd);
-  const size_t smem = kOStageOff + kAttRows * kHd * sizeof(float);
+  if (A < 0 || (long long)(kAttRows / G) * A > kMaxAncKeys)
+    return arg_error("attention: %d tokens x %d ancestors exceed %d ancestor keys per CTA", kAttRows / G, A, kMaxAncKeys);
+  const size_t smem = sizeof(AttnSmem);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tree_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

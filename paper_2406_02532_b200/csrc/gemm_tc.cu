@@ -133,7 +133,10 @@ SX_DEV int ld_acquire(const int* p) {
 SX_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 
 // Final epilogue of one 16-column chunk (values already summed over K).
-SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float (&v2)[16], int f, bool fok, int t0) {
+// xs: 16 x 64 fp32 smem exchange buffer (SWIGLU_IL: the up rows 64..127 of the
+// tile hand their values to the gate rows 0..63 of the same features).
+SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float (&v2)[16], int f, int fl, bool fok,
+                           int t0, float* xs) {
   if (g.epi == SX_EPI_BF16) {
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
 #pragma unroll
@@ -149,6 +152,21 @@ SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float 
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + f] += v[j];
+  } else if (g.epi == SX_EPI_SWIGLU_IL) {
+    const int r = fl & 63;
+    if (fl >= 64) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) xs[j * 64 + r] = v[j];
+    }
+    epi_bar();
+    if (fl < 64) {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
+      const int fo = ((f - fl) >> 1) + r;  // tile rows 128j.. -> output features 64j..
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + fo] = __float2bfloat16(silu(v[j]) * xs[j * 64 + r]);
+    }
+    epi_bar();
   } else {  // SX_EPI_SWIGLU_BF16
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
 #pragma unroll
@@ -163,7 +181,7 @@ SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float 
 //   mode 2: owner of split tile -> add the partials of slots h0, h0+hs, ... (hn of them) in order
 template <bool DUAL>
 SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool fok, int tt, int mode, int slot,
-                         int h0, int hs, int hn) {
+                         int h0, int hs, int hn, float* xs) {
   const long long pstride = (long long)(DUAL ? 2 : 1) * g.BN * 128;
   if (mode == 2) {
     if (threadIdx.x == 64)
@@ -221,7 +239,7 @@ SX_DEV void epilogue_seg(const GemmArgs& g, uint32_t tbase, int f, int fl, bool 
         }
       }
     }
-    epilogue_store(g, v, v2, f, fok, tt * g.BN + c);
+    epilogue_store(g, v, v2, f, fl, fok, tt * g.BN + c, xs);
   }
   if (mode == 1) {
     __threadfence();
@@ -276,6 +294,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull_bar = empty_bar + g.stages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* xs = reinterpret_cast<float*>(smem + g.stages * g.stage_bytes + 1024);  // epilogue exchange, 4 KB
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -435,7 +454,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * g.acc_cols;
-      epilogue_seg<DUAL>(g, tbase, f, fl, fok, tt, mode, slot, h0, hs, hn);
+      epilogue_seg<DUAL>(g, tbase, f, fl, fok, tt, mode, slot, h0, hs, hn, xs);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -501,12 +520,13 @@ struct Plan {
   long long ws_floats;
 };
 
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 256;
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024 - 4096;  // align pad, barriers, epilogue exchange
 
-static bool use_pair(int M, int Nf, int dual) {
+static bool use_pair(int M, int Nf, int dual, int cg_req) {
   if (Nf < 256) return false;
-  if (g_pair_mode == 1) return false;
-  if (g_pair_mode == 2) return true;
+  const int mode = cg_req ? cg_req : g_pair_mode;
+  if (mode == 1) return false;
+  if (mode == 2) return true;
   // auto: the target pass over the tree (hundreds of tokens) is MMA-bound and
   // the pair halves the B-operand smem traffic per SM -- when its 256-row tiles
   // still give >= 1.5 waves over the 74 pairs. Thin draft batches stream
@@ -517,25 +537,33 @@ static bool use_pair(int M, int Nf, int dual) {
   return tiles * 2 >= 3 * (kNumSMs / 2);
 }
 
-// sched_req: 1 = whole tiles only, 2 = force stream-K ranges, 3 = force
+// req = sched | cg << 4 | (bn_cap / 16) << 8 (a plan request; 0 = all auto):
+// cg 1 = single-CTA tiles, 2 = CTA pair (else the sx_gemm_set_pair_mode policy);
+// bn_cap = token-tile width cap (explicit: no narrowing);
+// sched: 1 = whole tiles only, 2 = force stream-K ranges, 3 = force
 // whole-tile waves + split tail; otherwise auto:
 //  - whole tiles when the waves fill >= 95% of the units;
 //  - else, with several token tiles per weight tile, whole-tile waves plus a
 //    K-split tail (all tail items run together, so the token tiles of a weight
 //    tile still read the same k-range at the same time and share it in L2);
 //  - else (one token tile: every weight tile is read once anyway) stream-K.
-static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
+static Plan make_plan(int M, int Nf, int K, int dual, int req) {
   Plan p{};
-  p.cg = use_pair(M, Nf, dual) ? 2 : 1;
+  const int sched_req = req & 15;
+  const int cg_req = (req >> 4) & 3;
+  const int bn_req = ((req >> 8) & 255) * 16;
+  p.cg = use_pair(M, Nf, dual, cg_req) ? 2 : 1;
   const int P = kNumSMs / p.cg;  // scheduling units
   const int fr = 128 * p.cg;     // weight rows per tile
-  p.bn = pick_bn(M, dual ? 128 : bn_cap_single());
+  int cap = dual ? 128 : bn_cap_single();
+  if (bn_req > 0) cap = bn_req < cap ? bn_req : cap;
+  p.bn = pick_bn(M, cap);
   p.tiles_f = (Nf + fr - 1) / fr;
   // Weight-streaming shapes with few weight tiles (e.g. a 4096-wide projection of
   // the draft = 32 tiles): a single SM's TMA pulls only ~40-50 GB/s, so use
   // narrower token tiles until ~120+ CTAs stream. The weight tile is shared by
   // the token tiles through L2, HBM traffic is unchanged.
-  if (p.cg == 1) {
+  if (p.cg == 1 && bn_req == 0) {
     while (p.tiles_f * ((M + p.bn - 1) / p.bn) < 120 && p.bn > 32) {
       const int half = ((p.bn / 2) + 15) / 16 * 16;
       const int nb = pick_bn(M, half);
@@ -555,8 +583,8 @@ static Plan make_plan(int M, int Nf, int K, int dual, int sched_req) {
   p.kpb = kpb;
   p.stage_bytes = stage_bytes(kpb);
   p.stages = kSmemBudget / (int)p.stage_bytes;
-  const int cap = (max_stages() + kpb - 1) / kpb;
-  if (p.stages > cap) p.stages = cap;
+  const int stage_cap = (max_stages() + kpb - 1) / kpb;
+  if (p.stages > stage_cap) p.stages = stage_cap;
   p.kb_total = K / (64 * kpb);
   const int waves = (p.tiles + P - 1) / P;
   const double eff = (double)p.tiles / ((double)waves * P);
@@ -651,8 +679,11 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
                             cudaStream_t stream) {
   const int dual = W2 != nullptr;
   if (dual != (epi == SX_EPI_SWIGLU_BF16)) return arg_error("sx_gemm: SWIGLU epilogue needs W2 and vice versa");
-  if (epi < 0 || epi > SX_EPI_SWIGLU_BF16) return arg_error("sx_gemm: bad epilogue %d", epi);
-  if (ldo < Nf) return arg_error("sx_gemm: ldo (%lld) < N (%d)", ldo, Nf);
+  if (epi < 0 || epi > SX_EPI_SWIGLU_IL) return arg_error("sx_gemm: bad epilogue %d", epi);
+  if (epi == SX_EPI_SWIGLU_IL && (Nf % 128) != 0)
+    return arg_error("sx_gemm: interleaved SwiGLU needs N %% 128 == 0 (N=%d)", Nf);
+  const int ncols = epi == SX_EPI_SWIGLU_IL ? Nf / 2 : Nf;
+  if (ldo < ncols) return arg_error("sx_gemm: ldo (%lld) < output width (%d)", ldo, ncols);
   if (M <= 0 || Nf <= 0 || K <= 0 || (K % 64) != 0)
     return arg_error("sx_gemm: need M,N > 0 and K a positive multiple of 64 (M=%d N=%d K=%d)", M, Nf, K);
   int st;
@@ -695,7 +726,7 @@ extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* 
   g.part = p.streamk ? ws + kFlagFloats : nullptr;
   g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
 
-  const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + (2 * g.stages + 4) * 8 + 16;
+  const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + 1024 + 4096;
 #define SX_GEMM_LAUNCH(CG, DU, KP) \
   if (p.cg == CG && dual == DU && p.kpb == KP) return launch_gemm<CG, DU, KP>(ma, ma2, mb, g, smem, stream);
   SX_GEMM_LAUNCH(1, 0, 1)

@@ -98,6 +98,19 @@ __global__ void __launch_bounds__(kRowThreads) tree_warp_rows_kernel(uint8_t* ws
 
 // --------------------------------------------------------------------------
 // Row statistics for logits rows: max and canonical sum of exp(z - max).
+//
+// Threshold prefilter (exact): once the tree holds K candidates, a child can
+// only enter if its key beats the threshold, and the threshold only decreases
+// (SURVEY Appendix A.7). An fp32 estimate of the child's nll,
+//   nll~ = parent_nll - ((z - m) - log S~),  S~ = fp32 sum of __expf(z - m),
+// is within 1e-4 of the exact float64 value (|z - m| rounding + S~ relative
+// error, both < 2e-5 here), so a candidate with nll~ - kPrefilterSlack >
+// thr_nll can never survive: it is dropped without the canonical fp64
+// exp/log. A row whose best child (z = m, nll~ = parent_nll + log S~) fails
+// that test skips the fp64 sum entirely. Survivors and borderline candidates
+// still take the exact path, so the tree is unchanged bit for bit.
+constexpr double kPrefilterSlack = 1e-3;
+
 __global__ void __launch_bounds__(kRowThreads) tree_row_stats_kernel(uint8_t* ws, TreeLayout L, const float* rows,
                                                                        long long ld) {
   __shared__ RowSmemLite sm;
@@ -105,12 +118,32 @@ __global__ void __launch_bounds__(kRowThreads) tree_row_stats_kernel(uint8_t* ws
   const int b = blockIdx.x;
   if (b >= c->batch_n) return;
   const float* z = rows + b * ld;
-  float m;
-  double S;
-  row_stats_lite(sm, z, L.V, m, S);
+  const int V = L.V;
+  float mx = -CUDART_INF_F;
+  for (int v = threadIdx.x; v < V; v += kRowThreads) mx = fmaxf(mx, z[v]);
+  const float m = block_max_f(sm, mx);
+  float sa = 0.f;
+  for (int v = threadIdx.x; v < V; v += kRowThreads) sa += __expf(z[v] - m);
+  for (int o = 16; o > 0; o >>= 1) sa += __shfl_xor_sync(0xffffffff, sa, o);
+  if ((threadIdx.x & 31) == 0) sm.redf[threadIdx.x >> 5] = sa;
+  __syncthreads();
+  float S_est = 0.f;
+  for (int w = 0; w < kRowThreads / 32; ++w) S_est += sm.redf[w];
+  __syncthreads();
+  const float lsa = logf(S_est);
+  const double parent_nll = at<double>(ws, L.b_nll)[b];
+  const bool skip = c->has_thr && dsub(dadd(parent_nll, (double)lsa), kPrefilterSlack) > c->thr_nll;
+  if (skip) {
+    if (threadIdx.x == 0) at<float>(ws, L.r_lsa)[b] = -CUDART_INF_F;
+    return;
+  }
+  double acc = 0.0;  // canonical sum (warp_rows.cuh)
+  for (int v = threadIdx.x; v < V; v += kRowThreads) acc = dadd(acc, sx_exp(dsub((double)z[v], (double)m)));
+  const double S = block_canon_sum(sm, acc);
   if (threadIdx.x == 0) {
     at<float>(ws, L.r_max)[b] = m;
     at<double>(ws, L.r_sum)[b] = S;
+    at<float>(ws, L.r_lsa)[b] = lsa;
   }
 }
 
@@ -164,9 +197,12 @@ __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout
   const unsigned long long tl = c->thr_lo;
   float m = 0.f;
   double S = 1.0;
+  float lsa = 0.f;
   const float* z = nullptr;
   const double* p = nullptr;
   if (row_kind == SX_ROWS_LOGITS_F32) {
+    lsa = at<float>(ws, L.r_lsa)[b];
+    if (lsa == -CUDART_INF_F) return;  // no child of this row can beat the threshold
     z = reinterpret_cast<const float*>(rows) + b * ld;
     m = at<float>(ws, L.r_max)[b];
     S = at<double>(ws, L.r_sum)[b];
@@ -181,7 +217,10 @@ __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout
     bool keep = false;
     double nll = 0.0, edge = 0.0;
     unsigned long long lo = 0;
-    if (v < V) {
+    // prefilter (logits rows): drop candidates whose fp32 nll estimate is clearly past the threshold
+    const bool pre = v < V && (!z || !has_thr ||
+                               !(dsub(dsub(parent_nll, (double)((z[v] - m) - lsa)), kPrefilterSlack) > c->thr_nll));
+    if (pre) {
       const double pv = z ? ddiv(sx_exp(dsub((double)z[v], (double)m)), S) : p[v];
       if (pv > 0.0) {
         edge = sx_log(pv);

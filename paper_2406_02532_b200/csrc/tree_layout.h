@@ -35,6 +35,7 @@ struct TreeLayout {
   long long w_rows;     // fp64 [B, V] warped rows (t > 0 scoring)
   long long w_keys, w_idx, w_keys2, w_idx2;  // [B, V] sort scratch
   long long f_anc, f_anc_len, f_depth, f_token;  // final target-row tables [(K+1)]
+  long long r_lsa;      // float [B]: fp32 log-sum-exp estimate (threshold prefilter), -inf: row skipped
   long long total;
 };
 
@@ -91,6 +92,7 @@ __host__ __device__ inline TreeLayout tree_layout(int K, int B, int V, int D) {
   L.f_anc_len = take(4LL * (K + 1));
   L.f_depth = take(4LL * (K + 1));
   L.f_token = take(4LL * (K + 1));
+  L.r_lsa = take(4LL * B);
   L.total = o;
   return L;
 }

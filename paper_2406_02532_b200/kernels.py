@@ -13,13 +13,14 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import EPI_ADD_F32, EPI_BF16, EPI_F32, EPI_SWIGLU_BF16, call, ptr, stream_ptr
+from ._lib import EPI_ADD_F32, EPI_BF16, EPI_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL, call, ptr, stream_ptr
 
 __all__ = [
     "EPI_ADD_F32",
     "EPI_BF16",
     "EPI_F32",
     "EPI_SWIGLU_BF16",
+    "EPI_SWIGLU_IL",
     "gemm",
     "gemm_plan",
 ]
@@ -126,7 +127,8 @@ def gemm(
         raise ValueError(f"gemm: inner dims differ ({K} vs {w.shape[1]})")
     if out is None:
         dt = torch.float32 if epi in (EPI_F32, EPI_ADD_F32) else torch.bfloat16
-        out = (torch.zeros if epi == EPI_ADD_F32 else torch.empty)((M, N), dtype=dt, device=x.device)
+        ncol = N // 2 if epi == EPI_SWIGLU_IL else N
+        out = (torch.zeros if epi == EPI_ADD_F32 else torch.empty)((M, ncol), dtype=dt, device=x.device)
     _, _, ws_need = gemm_plan(M, N, K, w2 is not None, splits)
     ws = _workspace(ws_need, x.device)
     prof = PROFILER
@@ -288,6 +290,12 @@ class TreeWorkspace:
         self.off = dict(zip(_OFF_NAMES, list(offs)))
         self.ctl_host = torch.zeros(16, dtype=torch.int32).pin_memory()
         self.rounds = 0
+        # pinned staging of the finished tree (parent, token, slot | edge): copied
+        # asynchronously so the host builds DraftTree while the target pass runs
+        self.host_i = torch.zeros((3, K + 1), dtype=torch.int32).pin_memory()
+        self.host_e = torch.zeros(K + 1, dtype=torch.float64).pin_memory()
+        self.host_ready = torch.cuda.Event()
+        self.pending_tree = None
 
     def view(self, name: str, dtype: torch.dtype, n: int) -> torch.Tensor:
         o = self.off[name]
@@ -354,6 +362,16 @@ class TreeWorkspace:
         call("sx_tree_finalize", ptr(self.buf), self.K, self.B, self.V, self.D, int(root_token), ptr(parent), ptr(token),
              ptr(edge), ptr(depth), ptr(slot), stream_ptr())
         return parent[:n], token[:n], edge[:n], depth[:n], slot[:n]
+
+    def stage_to_host(self, parent, token, slot, edge) -> None:
+        """Async D2H of the finished tree into the pinned staging buffers."""
+        n = parent.numel()
+        self.host_i[0, :n].copy_(parent, non_blocking=True)
+        self.host_i[1, :n].copy_(token, non_blocking=True)
+        self.host_i[2, :n].copy_(slot, non_blocking=True)
+        self.host_e[:n].copy_(edge, non_blocking=True)
+        self.host_ready.record()
+        IO["d2h"] += 20 * n
 
 
 def markov_rows(table: torch.Tensor, order: int, ctx0: torch.Tensor, ws: TreeWorkspace, node_ids: torch.Tensor | None,

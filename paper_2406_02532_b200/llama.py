@@ -93,11 +93,36 @@ def _rope_tables(cfg: LlamaConfig, max_pos: int, device) -> tuple[torch.Tensor, 
     return freqs.cos().contiguous().to(device), freqs.sin().contiguous().to(device)
 
 
-def layer_layout(cfg: LlamaConfig, shard: TPShard | None = None) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
+def interleave_gate_up(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    """[gate; up] interleaved in 64-row blocks -- the stored layout of the
+    SwiGLU projection: one GEMM tile of 128 weight rows covers gate and up of
+    the same 64 features, so the epilogue (SX_EPI_SWIGLU_IL) writes
+    silu(gate) * up without a second accumulator."""
+    f, d = gate.shape
+    if f % 64:
+        raise ValueError(f"FFN width {f} must be a multiple of 64")
+    return torch.stack([gate.reshape(f // 64, 64, d), up.reshape(f // 64, 64, d)], dim=1).reshape(2 * f, d)
+
+
+def split_gate_up(wgu: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    f2, d = wgu.shape
+    v = wgu.reshape(f2 // 128, 2, 64, d)
+    return v[:, 0].reshape(f2 // 2, d), v[:, 1].reshape(f2 // 2, d)
+
+
+def layer_layout(cfg: LlamaConfig, shard: TPShard | None = None,
+                 stored: bool = True) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
     """Byte offsets of one decoder layer's tensors in a contiguous buffer
     (256-B aligned, the unit streamed in offload mode); `shard`: this rank's
-    tensor-parallel slice of the layer (tp.py)."""
-    shapes = (TPShard(0, 1) if shard is None else shard).local_shapes(cfg)
+    tensor-parallel slice of the layer (tp.py). stored=True: the HBM layout
+    (gate/up interleaved as "wgu"); False: the draw layout (wg, wu apart)."""
+    shapes = dict((TPShard(0, 1) if shard is None else shard).local_shapes(cfg))
+    if stored:
+        f, d = shapes.pop("wg")
+        shapes.pop("wu")
+        wd = shapes.pop("wd")
+        n1, n2 = shapes.pop("n1"), shapes.pop("n2")
+        shapes.update({"wgu": (2 * f, d), "wd": wd, "n1": n1, "n2": n2})
     out, off = {}, 0
     for k, shp in shapes.items():
         out[k] = (off, shp)
@@ -111,7 +136,8 @@ def layer_views(buf: torch.Tensor, layout) -> dict[str, torch.Tensor]:
 
 class LlamaWeights:
     """bf16 weights in nn.Linear layout ([out, in]); each decoder layer is one
-    contiguous buffer -- in HBM, or (offload) in pinned host memory."""
+    contiguous buffer -- in HBM, or (offload) in pinned host memory. Gate and
+    up projections are stored interleaved ("wgu", interleave_gate_up)."""
 
     def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0,
                  offload: bool = False, shard: TPShard | None = None):
@@ -129,19 +155,20 @@ class LlamaWeights:
         self.layer_bufs: list[torch.Tensor] = []
         self.layers = []
         tmp = torch.empty(self.layer_bytes, dtype=torch.uint8, device=device) if offload else None
-        # tensor parallel: draw the full layer (same draw order as the unsharded
-        # model, so every TP degree holds slices of the same weights), keep the shard
-        full_layout, full_bytes = layer_layout(cfg)
-        full_tmp = torch.empty(full_bytes, dtype=torch.uint8, device=device) if shard is not None else None
+        # every layer is drawn in the full, unsharded draw layout (same draw order
+        # for every TP degree / storage layout), then sliced (TP) and stored
+        gen_layout, gen_bytes = layer_layout(cfg, stored=False)
+        gen_tmp = torch.empty(gen_bytes, dtype=torch.uint8, device=device)
+        sh = shard if shard is not None else TPShard(0, 1)
         for _ in range(cfg.layers):
             buf = tmp if offload else torch.empty(self.layer_bytes, dtype=torch.uint8, device=device)
             v = layer_views(buf, self.layout)
-            src = v if shard is None else layer_views(full_tmp, full_layout)
-            for k in ("wqkv", "wo", "wg", "wu", "wd"):  # same draw order as the resident model
+            src = layer_views(gen_tmp, gen_layout)
+            for k in ("wqkv", "wo", "wg", "wu", "wd"):  # draw order
                 rnd_(src[k])
-            if shard is not None:
-                for k in ("wqkv", "wo", "wg", "wu", "wd"):
-                    v[k].copy_(shard.shard(cfg, k, src[k]))
+            for k in ("wqkv", "wo", "wd"):
+                v[k].copy_(sh.shard(cfg, k, src[k]))
+            v["wgu"].copy_(interleave_gate_up(sh.shard(cfg, "wg", src["wg"]), sh.shard(cfg, "wu", src["wu"])))
             v["n1"].fill_(1.0)
             v["n2"].fill_(1.0)
             if offload:
@@ -152,7 +179,7 @@ class LlamaWeights:
             else:
                 self.layer_bufs.append(buf)
                 self.layers.append(v)
-        del tmp, full_tmp
+        del tmp, gen_tmp
         self.nf = torch.ones(cfg.d, dtype=torch.bfloat16, device=device)
         self.lm = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device), std * lm_scale)
         if shard is not None:
@@ -161,9 +188,15 @@ class LlamaWeights:
     def to_cpu_fp32(self) -> dict:
         """fp32 CPU copy for the CPU reference forward (oracle/llama_ref.py)."""
         f = lambda t: t.float().cpu()  # noqa: E731
+
+        def layer(L):
+            out = {k: f(v) for k, v in L.items() if k != "wgu"}
+            out["wg"], out["wu"] = (f(t) for t in split_gate_up(L["wgu"]))
+            return out
+
         return {
             "emb": f(self.emb),
-            "layers": [{k: f(v) for k, v in L.items()} for L in self.layers],
+            "layers": [layer(L) for L in self.layers],
             "nf": f(self.nf),
             "lm": f(self.lm),
         }
@@ -347,7 +380,7 @@ class LlamaModel(LanguageModel):
             if tp is not None:
                 tp.all_reduce_(y)
             _lib.call("sx_add_rmsnorm", p(x), p(y), ybf, p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
-            K.gemm(h, L["wg"], out=b.act[:n], epi=K.EPI_SWIGLU_BF16, w2=L["wu"])
+            K.gemm(h, L["wgu"], out=b.act[:n], epi=K.EPI_SWIGLU_IL)
             K.gemm(b.act[:n], L["wd"], out=y, epi=epi_y)
             if tp is not None:
                 tp.all_reduce_(y)
@@ -471,7 +504,7 @@ class LlamaModel(LanguageModel):
         if len(pending) > 1:
             self._chain(c, pending[:-1], False)
             c += len(pending) - 1
-        n = len(tree.nodes) + 1
+        n = len(tree) + 1
         if c + n > self.slots:
             raise RuntimeError(f"KV cache full: need {c + n} slots, have {self.slots}")
         ws = tree.workspace
@@ -510,7 +543,11 @@ class LlamaModel(LanguageModel):
             self.committed.extend(tree.nodes[r - 1].token for r in rows)
         elif getattr(tree, "draft_model", None) is self:
             c = tree.draft_root_slot
-            slots = tree.host_slot
+            if hasattr(tree, "host_slot"):  # host-built (SpecInfer) tree
+                slots = tree.host_slot
+            else:  # GPU-built tree: slots staged with the nodes
+                tree.nodes  # noqa: B018
+                slots = tree.host_slot_staged
             src, toks = [], []
             for r in res.path_rows:
                 s = slots[r - 1]
@@ -631,9 +668,7 @@ class _LlamaDraftSession:
 
     def finish(self, tree) -> None:
         tree.draft_model = self.m
-        tree.draft_root_slot = self.root_slot
-        tree.host_slot = tree.device_slot.cpu().tolist()
-        K.IO["d2h"] += 4 * len(tree.host_slot)
+        tree.draft_root_slot = self.root_slot  # node KV slots arrive with the staged tree (host_slot_staged)
 
 
 class _LlamaStochastic:

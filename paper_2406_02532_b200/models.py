@@ -216,7 +216,7 @@ class MarkovModel(LanguageModel):
         like SpecInfer's stochastic trees)."""
         if tree.workspace is None:
             return self.rows_for_prefixes([tree.prefix] + [tree.full_prefix(nd.node_id) for nd in tree.nodes])
-        n = len(tree.nodes)
+        n = len(tree)
         ws = tree.workspace
         ids = torch.arange(-1, n, dtype=torch.int32, device=ws.device)
         out = torch.empty((n + 1, self.vocab_size), dtype=torch.float64, device=ws.device)

@@ -61,7 +61,9 @@ class DraftTree:
 
     def __init__(self, prefix: Prefix) -> None:
         self.prefix: Prefix = tuple(prefix)
-        self.nodes: list[DraftNode] = []
+        self._nodes: list[DraftNode] = []
+        self._fill = None  # GPU-built trees: nodes materialise on first access
+        self._n = 0
         self.rounds: int = 0
         self.draft_dists = None
         self._children: dict[int, list[int]] = {ROOT: []}
@@ -70,8 +72,15 @@ class DraftTree:
         self.device_token = None
         self.workspace = None
 
+    @property
+    def nodes(self) -> list[DraftNode]:
+        if self._fill is not None:
+            fill, self._fill = self._fill, None
+            fill(self)
+        return self._nodes
+
     def __len__(self) -> int:
-        return len(self.nodes)
+        return self._n if self._fill is not None else len(self._nodes)
 
     def add_child(self, parent: int, token: int, edge_logprob: float) -> int:
         if parent != ROOT:
@@ -91,11 +100,13 @@ class DraftTree:
             raise KeyError(f"no node with id {node_id}")
 
     def children_of(self, node_id: int) -> list[int]:
+        self.nodes  # noqa: B018  (materialise a GPU-built tree)
         if node_id != ROOT:
             self._check_id(node_id)
         return list(self._children[node_id])
 
     def child_with_token(self, node_id: int, token: int) -> int | None:
+        self.nodes  # noqa: B018
         for child in self._children[node_id]:
             if self.nodes[child].token == token:
                 return child
@@ -206,11 +217,24 @@ def tree_tables(tree: DraftTree) -> tuple[np.ndarray, np.ndarray, np.ndarray, np
     return anc, alen, depth, tok
 
 
-def _tree_from_device(prefix: Prefix, parent, token, edge, rounds: int) -> DraftTree:
+def _tree_from_device(prefix: Prefix, ws, n: int, rounds: int) -> DraftTree:
+    """DraftTree whose host nodes are built from the pinned staging buffers on
+    first access (after the copies land): the target pass is already enqueued
+    by then, so the host-side construction overlaps GPU work."""
     tree = DraftTree(prefix)
-    for p, t, e in zip(parent.tolist(), token.tolist(), edge.tolist()):
-        tree.add_child(p, t, e)
     tree.rounds = rounds
+    tree._n = n
+
+    def fill(t: DraftTree) -> None:
+        ws.host_ready.synchronize()
+        if ws.pending_tree is t:
+            ws.pending_tree = None
+        par, tok = ws.host_i[0, :n].tolist(), ws.host_i[1, :n].tolist()
+        for p, k, e in zip(par, tok, ws.host_e[:n].tolist()):
+            t.add_child(p, k, e)
+        t.host_slot_staged = ws.host_i[2, :n].tolist()
+
+    tree._fill = fill
     return tree
 
 
@@ -245,11 +269,12 @@ def build_sssp(
             break
         session.advance(ctl)
     n = ctl["count"]
+    if ws.pending_tree is not None:  # the staging buffers are about to be reused
+        ws.pending_tree.nodes  # noqa: B018  (materialise the previous tree first)
     parent, token, edge, depth, slot = ws.finalize(n, prefix[-1] if prefix else 0)
-    tree = _tree_from_device(prefix, parent.cpu(), token.cpu(), edge.cpu(), ws.rounds)
-    from .kernels import IO
-
-    IO["d2h"] += 16 * n
+    ws.stage_to_host(parent, token, slot, edge)
+    tree = _tree_from_device(prefix, ws, n, ws.rounds)
+    ws.pending_tree = tree
     tree.device_parent, tree.device_token, tree.workspace = parent, token, ws
     tree.device_depth = depth
     tree.device_slot = slot

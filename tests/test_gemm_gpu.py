@@ -80,7 +80,7 @@ def test_gemm_pair_vs_single(cuda, mode, M, N, Kd):
         ref_sw = torch.nn.functional.silu(ref) * _ref(x, w2)
         assert (sw.float() - ref_sw).abs().max().item() < 2e-2 * max(1.0, ref_sw.abs().max().item())
     finally:
-        _lib.call("sx_gemm_set_pair_mode", 1)  # library default: single-CTA
+        _lib.call("sx_gemm_set_pair_mode", 0)  # library default: auto
 
 
 @pytest.mark.parametrize("sched", [1, 2, 3, 0])
@@ -125,3 +125,32 @@ def test_gemm_large_perf_smoke(cuda):
     ms = s.elapsed_time(e) / 10
     tflops = 2 * M * N * Kd / ms / 1e9
     print(f"\n[gemm] 1025x8192x8192: {ms:.3f} ms  {tflops:.0f} TFLOP/s")
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("sched", [0, 1, 2, 3])
+@pytest.mark.parametrize("M,F,Kd", [(1025, 2048, 512), (256, 1408, 1024), (40, 512, 256), (300, 704, 256)])
+def test_gemm_swiglu_interleaved(cuda, mode, sched, M, F, Kd):
+    """SX_EPI_SWIGLU_IL: one GEMM over [gate; up] interleaved in 64-row blocks
+    (llama.interleave_gate_up) == silu(x gate^T) * (x up^T), every tile shape /
+    schedule (stream-K partials are summed before the exchange)."""
+    from paper_2406_02532_b200 import _lib
+    from paper_2406_02532_b200.llama import interleave_gate_up
+
+    _lib.call("sx_gemm_set_pair_mode", mode)
+    try:
+        g = torch.Generator(device=cuda).manual_seed(M * 7 + F)
+        x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+        wg = (torch.randn(F, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+        wu = (torch.randn(F, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+        y = K.gemm(x, interleave_gate_up(wg, wu), epi=K.EPI_SWIGLU_IL, splits=sched)
+        ref = torch.nn.functional.silu(_ref(x, wg)) * _ref(x, wu)
+        torch.cuda.synchronize()
+        assert y.shape == (M, F)
+        assert (y.float() - ref).abs().max().item() < 2e-2 * max(1.0, ref.abs().max().item())
+        # same rounding as the dual-accumulator epilogue (identical fp32 sums in the plain schedule)
+        if sched == 1:
+            yd = K.gemm(x, wg, epi=K.EPI_SWIGLU_BF16, w2=wu, splits=1)
+            assert (y.float() - yd.float()).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
+    finally:
+        _lib.call("sx_gemm_set_pair_mode", 0)

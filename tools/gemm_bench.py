@@ -23,11 +23,13 @@ SHAPES = [
     ("70b.qkv", 1025, 10240, 8192, False, K.EPI_BF16),
     ("70b.o", 1025, 8192, 8192, False, K.EPI_F32),
     ("70b.gate_up", 1025, 28672, 8192, True, K.EPI_SWIGLU_BF16),
+    ("70b.gate_up_il", 1025, 57344, 8192, False, K.EPI_SWIGLU_IL),
     ("70b.down", 1025, 8192, 28672, False, K.EPI_F32),
     ("70b.lm_head", 1025, 32000, 8192, False, K.EPI_F32),
     ("7b.qkv", DRAFT_M, 12288, 4096, False, K.EPI_BF16),
     ("7b.o", DRAFT_M, 4096, 4096, False, K.EPI_F32),
     ("7b.gate_up", DRAFT_M, 11008, 4096, True, K.EPI_SWIGLU_BF16),
+    ("7b.gate_up_il", DRAFT_M, 22016, 4096, False, K.EPI_SWIGLU_IL),
     ("7b.down", DRAFT_M, 4096, 11008, False, K.EPI_F32),
     ("7b.lm_head", DRAFT_M, 32000, 4096, False, K.EPI_F32),
 ]
