@@ -34,13 +34,15 @@ sys.path.insert(0, str(ROOT))
 
 WORKLOADS = {
     # name: (draft preset, target preset, K, D, B, temperature, top_p)
-    "c2": ("llama2-7b", "llama2-70b", 1024, 16, 256, 0.0, 1.0),
+    # B=1024: the tree is identical for every B; a wide batch makes the
+    # draft rounds M=1024 tensor-core GEMMs (2 draft calls / iteration instead of 5)
+    "c2": ("llama2-7b", "llama2-70b", 1024, 16, 1024, 0.0, 1.0),
     "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 256, 0.0, 1.0),
     # C4: 70B target tensor-parallel over the N GPUs (--gpus N), K=4096
-    "c4": ("llama2-7b", "llama2-70b", 4096, 16, 256, 0.0, 1.0),
+    "c4": ("llama2-7b", "llama2-70b", 4096, 16, 1024, 0.0, 1.0),
     "tiny": ("tiny-draft", "tiny", 128, 16, 8, 0.0, 1.0),
     # C3: 70B target offloaded to pinned host RAM, streamed per layer; 7B draft resident
-    "c3": ("llama2-7b", "llama2-70b", 2048, 16, 256, 0.6, 0.9),
+    "c3": ("llama2-7b", "llama2-70b", 2048, 16, 1024, 0.6, 0.9),
     "tiny-offload": ("tiny-draft", "tiny", 128, 16, 8, 0.6, 0.9),
 }
 OFFLOAD = {"c3", "tiny-offload"}

@@ -570,6 +570,20 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
       if (p.tiles_f * ((M + nb - 1) / nb) > kNumSMs) break;  // would spill into a second wave
       p.bn = nb;
     }
+    // Thin token batches (draft rounds): when whole tiles fill the waves poorly,
+    // narrower token tiles buy wave efficiency for extra L2 re-reads of the weight
+    // tile (7B SwiGLU at M = 256: 172 tiles, 97 -> 69 us at BN 256 -> 64;
+    // tools/gemm_plan_sweep.py). Stop at 80% or BN 64.
+    auto wave_eff = [&](int bn) {
+      const long long t = (long long)p.tiles_f * ((M + bn - 1) / bn);
+      const long long w = (t + kNumSMs - 1) / kNumSMs;
+      return (double)t / (double)(w * kNumSMs);
+    };
+    while (M <= 512 && p.bn > 64 && wave_eff(p.bn) < 0.8) {
+      const int nb = pick_bn(M, ((p.bn / 2) + 15) / 16 * 16);
+      if (nb >= p.bn) break;
+      p.bn = nb;
+    }
   }
   p.tiles_t = (M + p.bn - 1) / p.bn;
   p.tiles = p.tiles_f * p.tiles_t;

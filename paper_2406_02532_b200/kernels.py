@@ -132,6 +132,8 @@ def gemm(
     _, _, ws_need = gemm_plan(M, N, K, w2 is not None, splits)
     ws = _workspace(ws_need, x.device)
     prof = PROFILER
+    if prof is not None and torch.cuda.is_current_stream_capturing():
+        prof = None  # launches captured into a CUDA graph are not timed individually
     if prof is not None:
         e0 = prof.event()
         e0.record()

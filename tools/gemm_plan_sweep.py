@@ -70,28 +70,34 @@ def main():
             K.gemm(x, ws[i[0] % nw], out=out, epi=epi, splits=req)
             i[0] += 1
 
-        auto_us = timeit(lambda: run(0), reps)
-        best = (auto_us, 0)
-        cands = []
+        cands = [0]
         for cg in (1, 2):
-            for bn in (0, 32, 64, 128, 208, 256):
-                for sched in (1, 2, 3):
+            for bn in (0, 64, 128, 208, 256):
+                for sched in (1, 3, 2):
                     cands.append(sched | cg << 4 | (bn // 16) << 8)
-        for req in cands:
+        ok = []
+        for req in cands:  # drop illegal combinations
             try:
-                us = timeit(lambda: run(req), reps)
-            except Exception as e:  # noqa: BLE001 (illegal combination for this shape)
-                continue
+                run(req)
+                ok.append(req)
+            except Exception:  # noqa: BLE001
+                pass
+        torch.cuda.synchronize()
+        # round-robin over the candidates (3 passes, min per candidate) so clock
+        # drift under the power cap does not favour early candidates
+        best_us = {r: float("inf") for r in ok}
+        for _ in range(3):
+            for req in ok:
+                best_us[req] = min(best_us[req], timeit(lambda: run(req), reps))
+        for req in ok:
             plan = K.gemm_plan(M, N, Kd, False, req)
-            recs.append({"shape": name, "M": M, "N": N, "K": Kd, "req": req, "us": us, "plan": plan,
-                         "tflops": flops / us / 1e6})
-            if us < best[0]:
-                best = (us, req)
+            recs.append({"shape": name, "M": M, "N": N, "K": Kd, "req": req, "us": best_us[req], "plan": plan,
+                         "tflops": flops / best_us[req] / 1e6, "auto": req == 0})
+        auto_us = best_us[0]
+        best = min((us, r) for r, us in best_us.items())
         print(f"{name:14s} M={M:5d} auto {auto_us:8.1f} us ({flops / auto_us / 1e6:6.0f} TF) plan={K.gemm_plan(M, N, Kd, False, 0)}"
               f" | best {best[0]:8.1f} us req={best[1]} (cg={(best[1] >> 4) & 3} bn={((best[1] >> 8) & 255) * 16}"
               f" sched={best[1] & 15}) plan={K.gemm_plan(M, N, Kd, False, best[1])}", flush=True)
-        recs.append({"shape": name, "M": M, "N": N, "K": Kd, "req": 0, "us": auto_us, "auto": True,
-                     "best_req": best[1], "best_us": best[0]})
         del ws, x, out
         torch.cuda.empty_cache()
     if a.out:
