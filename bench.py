@@ -46,6 +46,13 @@ WORKLOADS = {
     "tiny-offload": ("tiny-draft", "tiny", 128, 16, 8, 0.6, 0.9),
 }
 OFFLOAD = {"c3", "tiny-offload"}
+METRIC = "generated tokens/sec (accepted tokens per target iteration reported beside)"
+
+
+def workload_desc(name: str, K: int, B: int) -> str:
+    d, t, _, D, _, temp, _ = WORKLOADS[name]
+    return (f"{name}: {d} draft + {t} target, K={K}, D={D}, B={B}, t={temp}"
+            + (", target offloaded (per-layer H2D streaming)" if name in OFFLOAD else ", target resident in HBM"))
 
 
 def parse():
@@ -68,6 +75,9 @@ def parse():
     ap.add_argument("--parallel", choices=["tp", "replicas"], default="tp",
                     help="N>1: tensor-parallel target (one stream) or N independent replicas")
     ap.add_argument("--reduce", choices=["bf16", "fp32"], default="bf16", help="TP all-reduce precision")
+    ap.add_argument("--tp-comm", choices=["fused", "nccl"], default="fused",
+                    help="TP reduction: GEMM epilogue reduce-scatter over peer memory (falls back to NCCL if "
+                         "symmetric memory is unavailable) or NCCL all-reduce")
     return ap.parse_args()
 
 
@@ -189,6 +199,20 @@ def measure_h2d(torch, nbytes: int = 1 << 30, reps: int = 5) -> float:
     return gbs
 
 
+def ncu_traffic(prefix: str = "gemm_tc_kernel<2") -> tuple[float | None, str]:
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set
+    full` captures (profiles/*/ncu_summary.json; one capture per target-pass
+    GEMM shape, each launched once per layer, so the plain mean is the per-launch
+    average of the pass)."""
+    best = None
+    for f in sorted(ROOT.glob("profiles/*/ncu_summary.json")):
+        rows = [r for r in json.loads(f.read_text()) if prefix in r.get("kernel", "") and r.get("dram_bytes")
+                and "70b" in r.get("report", "")]
+        if rows:
+            best = (sum(r["dram_bytes"] for r in rows) / len(rows), f"{f.relative_to(ROOT)} ({len(rows)} shapes)")
+    return best if best else (None, "no ncu capture committed")
+
+
 # ----------------------------------------------------------------------------- CPU baseline
 def cpu_baseline(args, w, accepted_per_iter: float, rounds_per_iter: float, tree_nodes: int, ctx: int) -> dict:
     """The oracle port timed on this host: one fp32 decoder layer of the target
@@ -263,10 +287,10 @@ def run_reference(args):
     sec = statistics.mean(steps)
     value = 1.0 / sec
     cb["value"] = value
-    line = {"impl": "reference", "metric": "generated tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {w[0]} draft + {w[1]} target, K={K}, D={w[3]}, B={B}, t={w[5]}",
+            "config": {"workload": workload_desc(args.workload, K, B),
                        "note": "CPU oracle port (extrapolated per-layer timing; 1 accepted token/iteration assumed)"},
             "cpu_baseline": cb, "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -308,7 +332,8 @@ def main():
     ctx_cap = args.prompt_len + (args.warmup + args.steps) * (D + 1) * 3 + 64
     offload = args.workload in OFFLOAD
     target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn,
-                        offload=offload, tp=comm, reduce_bf16=args.reduce == "bf16")
+                        offload=offload, tp=comm, reduce_bf16=args.reduce == "bf16",
+                        tp_fused=None if args.tp_comm == "fused" else False)
     draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
                        synthetic=syn)
     torch.cuda.synchronize()
@@ -367,9 +392,12 @@ def main():
     small = prof.summary(min_m=0)
     ach = big["flops"] / (big["ms"] / 1e3) / 1e12 if big["ms"] > 0 else 0.0
     gemm_share = small["ms"] / ms if ms > 0 else 0.0
+    traffic, traffic_src = ncu_traffic()
     roof = {"bound": "tensor", "kernel": "gemm_tc_kernel (target pass, M=K+1 tree tokens)", "achieved": ach,
             "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"] if pk["bf16_sus"] else None,
-            "peak_source": f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)", "traffic": None,
+            "peak_source": f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
+            "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_source": traffic_src,
             "launches": big["launches"], "gemm_share_of_step": gemm_share,
             "flops_per_launch_avg": big["flops"] / max(1, big["launches"])}
 
@@ -411,16 +439,15 @@ def main():
     if rank == 0:
         tb = PRESETS[tname].weight_bytes() + PRESETS[dname].weight_bytes()
         line = {
-            "metric": "generated tokens/sec (accepted tokens per target iteration reported beside)",
+            "metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong" if tp else "weak",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic: random-init weights (N(0,0.02)), random 128-token prompt" +
                     (f", shared synthetic prev-token bias scale {args.synthetic}" if syn else ""),
-            "config": {"workload": f"{args.workload}: {dname} draft + {tname} target, resident in HBM, K={K}, D={D}, "
-                                   f"B={B}, t={temp}, scoring={scoring}" + (", target offloaded (per-layer H2D streaming)" if offload else "") + "",
-                       "parallelism": (f"tp{world} target (NCCL, {args.reduce} all-reduce), draft replicated"
+            "config": {"workload": workload_desc(args.workload, K, B), "scoring": scoring,
+                       "parallelism": (f"tp{world} target ({'fused GEMM reduce-scatter over peer memory' if target.tp_fused else 'NCCL all-reduce'}, {args.reduce}), draft replicated"
                                        if tp else f"replicas x{world}") if world > 1 else "1 GPU",
                        "l2": f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)",
                        "prompt_len": args.prompt_len},

@@ -61,9 +61,10 @@ enum {
   SX_EPI_F32 = 1,         /* out fp32  = acc                       */
   SX_EPI_ADD_F32 = 2,     /* out fp32 += acc (residual stream)     */
   SX_EPI_SWIGLU_BF16 = 3, /* out bf16  = silu(acc(W)) * acc(W2)    */
-  SX_EPI_SWIGLU_IL = 4    /* W = [gate; up] interleaved in 64-row blocks (rows 128j..128j+63 =
+  SX_EPI_SWIGLU_IL = 4,   /* W = [gate; up] interleaved in 64-row blocks (rows 128j..128j+63 =
                              gate features 64j.., rows 128j+64.. = up of the same features);
                              out bf16 [M, N/2] = silu(gate) * up   (N % 128 == 0)      */
+  SX_EPI_RS_BF16 = 5      /* internal: the reduce-scatter epilogue of sx_gemm_bf16_rs        */
 };
 /* 0 = auto (default: CTA-pair cta_group::2 tiles for M >= 256 tokens), 1 = single-CTA only, 2 = pair when legal */
 SX_API int sx_gemm_set_pair_mode(int mode);
@@ -71,6 +72,18 @@ SX_API int sx_gemm_plan(int M, int N, int K, int dual, int splits_req, int* bn_o
                  long long* ws_floats_out);
 SX_API int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* out, float* ws, long long ws_floats,
                  int M, int N, int K, long long ldo, int epi, int splits_req, cudaStream_t stream);
+/* Tensor-parallel row-parallel projection fused with the reduce-scatter half of
+ * its all-reduce: this rank's partial Y = X W^T (bf16) is written by the GEMM
+ * epilogue straight into the owners' inboxes over NVLink peer memory:
+ * feature f -> rank f / (N/world), at peer_inbox[owner] + ((rank * M + t) * (N/world)
+ * + f % (N/world)). peer_inbox: DEVICE array of `world` pointers (symmetric
+ * memory, [world][M][N/world] bf16 each). Then, after a cross-rank barrier,
+ * sx_tp_reduce_bcast on every rank sums its slice in rank order and writes it into
+ * every rank's y [M, N] (the all-gather half). Deterministic; identical on all ranks. */
+SX_API int sx_gemm_bf16_rs(const void* W, const void* X, void* const* peer_inbox, int rank, int world, float* ws,
+                           long long ws_floats, int M, int N, int K, int splits_req, cudaStream_t stream);
+SX_API int sx_tp_reduce_bcast(const void* inbox, int rank, int world, int M, int N, void* const* peer_y, int y_bf16,
+                              cudaStream_t stream);
 
 /* ------------------------------------- KT1-KT3: draft-tree build (stage 1)
  * build_sssp, pkg/src/speckit/tree.py:240-327, as a device-resident state

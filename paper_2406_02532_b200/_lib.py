@@ -66,6 +66,8 @@ SIGNATURES: dict[str, tuple] = {
     "sx_embed": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
     "sx_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
     "sx_add_rmsnorm": (_c_int, [_vp, _vp, _c_int, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
+    "sx_gemm_bf16_rs": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _vp, _c_ll, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "sx_tp_reduce_bcast": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp]),
     "sx_rope_kv": (
         _c_int,
         [_vp, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_ll, _vp],
@@ -81,7 +83,7 @@ SIGNATURES: dict[str, tuple] = {
 ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1
 SCORE_RAW, SCORE_ARGMAX, SCORE_WARP = 0, 1, 2
 
-EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL = 0, 1, 2, 3, 4
+EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL, EPI_RS_BF16 = 0, 1, 2, 3, 4, 5
 
 _lib = None
 

@@ -187,6 +187,47 @@ extern "C" int sx_rmsnorm(const float* x, const void* w, int n, int d, float eps
   return SX_OK;
 }
 
+// Owner-side half of the fused all-reduce (sx_gemm_bf16_rs): y_slice[t][c] =
+// sum over source ranks r (in order) of inbox[r][t][c], written to every rank's
+// y at columns rank * S + c (peer stores over NVLink; y fp32 or bf16).
+__global__ void tp_reduce_bcast_kernel(const __nv_bfloat16* __restrict__ inbox, int rank, int world, int M, int S, int N,
+                                       void* const* __restrict__ peer_y, int y_bf16) {
+  const long long n = (long long)M * S / 2;  // bf16 pairs
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int r = 0; r < world; ++r) {
+      const float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(inbox + (long long)r * M * S)[i]);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    const long long e = 2 * i;
+    const long long t = e / S, c = e % S;
+    const long long off = t * N + (long long)rank * S + c;
+    for (int q = 0; q < world; ++q) {
+      if (y_bf16)
+        *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(peer_y[q]) + off) =
+            __floats2bfloat162_rn(acc.x, acc.y);
+      else
+        *reinterpret_cast<float2*>(reinterpret_cast<float*>(peer_y[q]) + off) = acc;
+    }
+  }
+}
+
+extern "C" int sx_tp_reduce_bcast(const void* inbox, int rank, int world, int M, int N, void* const* peer_y, int y_bf16,
+                                  cudaStream_t stream) {
+  if (M <= 0) return SX_OK;
+  if (world < 1 || rank < 0 || rank >= world || N % world || (N / world) % 2)
+    return arg_error("tp_reduce_bcast: bad rank %d / world %d / N %d", rank, world, N);
+  const int S = N / world;
+  const long long pairs = (long long)M * S / 2;
+  int grid = (int)((pairs + 255) / 256);
+  if (grid > 4 * kNumSMs) grid = 4 * kNumSMs;
+  tp_reduce_bcast_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(inbox), rank, world, M, S, N,
+                                                   peer_y, y_bf16);
+  SX_CHECK_LAUNCH("tp_reduce_bcast_kernel");
+  return SX_OK;
+}
+
 extern "C" int sx_add_rmsnorm(float* x, const void* y, int y_bf16, const void* w, int n, int d, float eps, void* out,
                               cudaStream_t stream) {
   if (n <= 0) return SX_OK;

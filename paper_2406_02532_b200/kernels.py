@@ -169,6 +169,20 @@ from ._lib import ROWS_LOGITS_F32, ROWS_PROBS_F64, SCORE_ARGMAX, SCORE_RAW, SCOR
 _scratch_cache: dict[tuple[int, str], torch.Tensor] = {}
 
 
+def gemm_rs(x: torch.Tensor, w: torch.Tensor, peer_inbox: torch.Tensor, rank: int, world: int, splits: int = 0) -> None:
+    """Row-parallel projection fused with the reduce-scatter half of its
+    all-reduce (sx_gemm_bf16_rs): the epilogue writes each feature slice of
+    this rank's bf16 partial into its owner's inbox (peer_inbox: device int64
+    pointer table)."""
+    _require_cuda(x, w, peer_inbox)
+    M, Kd = x.shape
+    N = w.shape[0]
+    _, _, ws_need = gemm_plan(M, N, Kd, False, splits)
+    ws = _workspace(ws_need, x.device)
+    call("sx_gemm_bf16_rs", ptr(w), ptr(x), ptr(peer_inbox), rank, world, ptr(ws), ws.numel() if ws is not None else 0,
+         M, N, Kd, splits, stream_ptr())
+
+
 def scratch(nbytes: int, device: torch.device, tag: str) -> torch.Tensor:
     key = (device.index or 0, tag)
     buf = _scratch_cache.get(key)

@@ -293,10 +293,16 @@ class LlamaModel(LanguageModel):
         offload: bool = False,
         tp=None,
         reduce_bf16: bool = True,
+        tp_fused: bool | None = None,
     ):
         """tp: a communicator (tp.NcclComm / tp.ThreadComm) -> this model is rank
         tp.rank's tensor-parallel shard of the target (tp.py); the partial sums
-        of the o / down projections are all-reduced in bf16 (reduce_bf16) or fp32."""
+        of the o / down projections are all-reduced in bf16 (reduce_bf16) or fp32.
+        tp_fused: instead of a separate all-reduce, the projection's GEMM epilogue
+        writes each feature slice of its bf16 partial into the owner rank's inbox
+        over peer memory (sx_gemm_bf16_rs) and the owner reduces and broadcasts
+        the slice (sx_tp_reduce_bcast). None = fused when the communicator
+        provides peer memory, else the NCCL all-reduce."""
         if isinstance(cfg, str):
             cfg = PRESETS[cfg]
         if cfg.head_dim != 128:
@@ -324,6 +330,23 @@ class LlamaModel(LanguageModel):
         self.cos, self.sin = _rope_tables(cfg, max_ctx + 64, self.device)
         self.max_tokens = max_tokens
         self.buf = _Buffers(cfg, max_tokens, self.device, self.shard, self.reduce_bf16)
+        self.tp_fused = False
+        if self.tp is not None and tp_fused is not False:
+            W = self.tp.world
+            try:
+                if cfg.d % (W * 128):
+                    raise ValueError(f"fused TP reduce-scatter needs d={cfg.d} divisible by 128 x {W}")
+                self.inbox, self.inbox_peers = self.tp.symm_buffer(W * max_tokens * (cfg.d // W), torch.bfloat16)
+                ydt = torch.bfloat16 if self.reduce_bf16 else torch.float32
+                ybuf, self.y_peers = self.tp.symm_buffer(max_tokens * cfg.d, ydt)
+                self.buf.y = ybuf.view(max_tokens, cfg.d)  # peers write the reduced slices into it
+                self.tp_fused = True
+            except Exception as e:  # noqa: BLE001
+                if tp_fused:
+                    raise
+                import sys
+
+                print(f"[llama] fused TP reduce-scatter unavailable ({e}); using the NCCL all-reduce", file=sys.stderr)
         self.synthetic = synthetic
         if synthetic is not None:
             g = torch.Generator(device=self.device)
@@ -376,14 +399,20 @@ class LlamaModel(LanguageModel):
                       p(self.cos), p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
             _lib.call("sx_tree_attention", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
                       anc_base, p(anc_len), A, p(b.att), n, H, KVH, st)
-            K.gemm(b.att[:n], L["wo"], out=y, epi=epi_y)
-            if tp is not None:
-                tp.all_reduce_(y)
+            if self.tp_fused:
+                self._fused_reduce(b.att[:n], L["wo"], n)
+            else:
+                K.gemm(b.att[:n], L["wo"], out=y, epi=epi_y)
+                if tp is not None:
+                    tp.all_reduce_(y)
             _lib.call("sx_add_rmsnorm", p(x), p(y), ybf, p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
             K.gemm(h, L["wgu"], out=b.act[:n], epi=K.EPI_SWIGLU_IL)
-            K.gemm(b.act[:n], L["wd"], out=y, epi=epi_y)
-            if tp is not None:
-                tp.all_reduce_(y)
+            if self.tp_fused:
+                self._fused_reduce(b.act[:n], L["wd"], n)
+            else:
+                K.gemm(b.act[:n], L["wd"], out=y, epi=epi_y)
+                if tp is not None:
+                    tp.all_reduce_(y)
             if self.streamer is not None:
                 self.streamer.release(li)
         self.stats["forward_tokens"] += n
@@ -408,6 +437,16 @@ class LlamaModel(LanguageModel):
             torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)
             K.gemm(bi, self.bias_w, out=logits, epi=K.EPI_ADD_F32)
         return logits
+
+    def _fused_reduce(self, xin: torch.Tensor, w: torch.Tensor, n: int) -> None:
+        """y[:n] = sum over ranks of xin @ w^T: GEMM + reduce-scatter over peer
+        memory, barrier, owner reduce + broadcast, barrier."""
+        tp = self.tp
+        K.gemm_rs(xin, w, self.inbox_peers, tp.rank, tp.world)
+        tp.barrier_device()
+        _lib.call("sx_tp_reduce_bcast", _lib.ptr(self.inbox), tp.rank, tp.world, n, self.cfg.d, _lib.ptr(self.y_peers),
+                  int(self.reduce_bf16), _lib.stream_ptr())
+        tp.barrier_device()
 
     # ---------------------------------------------------------- prefix cache
     def _sync(self, prefix: tuple[int, ...]) -> tuple[int, list[int]]:

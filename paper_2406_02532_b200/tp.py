@@ -127,6 +127,23 @@ class NcclComm:
         self.dist.broadcast(t, src, group=self.group)
         return [int(v) for v in t.tolist()]
 
+    # -- peer memory for the fused GEMM + reduce-scatter path (sx_gemm_bf16_rs)
+    def symm_buffer(self, numel: int, dtype: torch.dtype):
+        """A buffer in symmetric memory (every rank maps every peer's copy over
+        NVLink); returns (local tensor, device int64 tensor of the peers' base
+        pointers in rank order)."""
+        import torch.distributed._symmetric_memory as symm_mem
+
+        t = symm_mem.empty(numel, dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+        h = symm_mem.rendezvous(t, group=self.group if self.group is not None else self.dist.group.WORLD)
+        self._symm = getattr(self, "_symm", [])
+        self._symm.append(h)
+        return t, torch.tensor(list(h.buffer_ptrs), dtype=torch.int64, device=t.device)
+
+    def barrier_device(self) -> None:
+        """Stream-ordered cross-rank barrier (all prior peer stores visible)."""
+        self._symm[0].barrier(channel=0)
+
 
 class _Hub:
     def __init__(self, world: int):
@@ -185,3 +202,17 @@ class ThreadComm:
         out = list(self.hub.slots[src])
         self.hub.barrier.wait()
         return out
+
+    def symm_buffer(self, numel: int, dtype: torch.dtype):
+        """Per-rank buffers on the shared device; the 'peer pointers' are the
+        other thread-ranks' buffers -- the same kernels as over NVLink."""
+        t = torch.zeros(numel, dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+        self.hub.slots[self.rank] = t.data_ptr()
+        self.hub.barrier.wait()
+        ptrs = list(self.hub.slots)
+        self.hub.barrier.wait()
+        return t, torch.tensor(ptrs, dtype=torch.int64, device=t.device)
+
+    def barrier_device(self) -> None:
+        torch.cuda.current_stream().synchronize()
+        self.hub.barrier.wait()

@@ -42,8 +42,9 @@ def run_ranks(world, fn):
     return out
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("world", [2])
-def test_tp_logits_match_unsharded(cuda, world):
+def test_tp_logits_match_unsharded(cuda, world, fused):
     full = LlamaModel(CFG, seed=3, max_ctx=1024, max_tokens=256)
     prefix = tuple(int(t) for t in np.random.default_rng(1).integers(0, 32000, size=40))
     exp = full.prefix_rows(prefix)[0].clone()
@@ -53,14 +54,16 @@ def test_tp_logits_match_unsharded(cuda, world):
     for reduce_bf16, tol in ((False, 1e-2), (True, 2e-2)):
         comms = ThreadComm.group(world)
         outs = run_ranks(world, lambda r: LlamaModel(CFG, seed=3, max_ctx=1024, max_tokens=256, tp=comms[r],
-                                                     reduce_bf16=reduce_bf16).prefix_rows(prefix)[0].clone())
+                                                     reduce_bf16=reduce_bf16, tp_fused=fused)
+                         .prefix_rows(prefix)[0].clone())
         for o in outs[1:]:
             assert torch.equal(o, outs[0])  # every rank holds identical all-gathered rows
         assert (outs[0] - exp).abs().max().item() < tol, reduce_bf16
         assert (outs[0].cpu() - cpu).abs().max().item() < 2e-2
 
 
-def test_tp_target_generation_ranks_agree_replay_parity(cuda, monkeypatch):
+@pytest.mark.parametrize("fused", [False, True])
+def test_tp_target_generation_ranks_agree_replay_parity(cuda, monkeypatch, fused):
     world = 2
     syn = SyntheticBias(seed=7, rank=64, scale=4.0)
     comms = ThreadComm.group(world)
@@ -69,7 +72,7 @@ def test_tp_target_generation_ranks_agree_replay_parity(cuda, monkeypatch):
     cfg = sx.SamplingConfig(0.0, 1.0, seed=3, max_new_tokens=40)
 
     def rank(r):
-        target = LlamaModel(CFG, seed=3, max_ctx=2048, max_tokens=512, synthetic=syn, tp=comms[r])
+        target = LlamaModel(CFG, seed=3, max_ctx=2048, max_tokens=512, synthetic=syn, tp=comms[r], tp_fused=fused)
         draft = LlamaModel("tiny-draft", seed=2, max_ctx=4096, max_tokens=512, synthetic=syn)
         draft.use_graphs = False  # no concurrent graph capture from two threads
         if r == 0:
