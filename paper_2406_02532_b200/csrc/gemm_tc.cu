@@ -57,6 +57,7 @@ struct GemmArgs {
   // inbox[owner][rs_rank][t][f - owner * rs_slice] (bf16) -- the reduce-scatter
   // half of the all-reduce, written by the epilogue over NVLink as tiles finish
   int rs_rank, rs_world, rs_slice;
+  int vec_store;  // 1: output rows 16-B aligned -> smem-transposed epilogue with 16-B stores
   int* flags;      // stream-K partial-ready flags [ctas * CG]
   float* part;     // stream-K partials [ctas * CG][dual?2:1][BN][128]
   int debug_no_tma;  // SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
@@ -66,6 +67,10 @@ constexpr int kGemmThreads = 192;
 constexpr int kFlagFloats = 1024;  // workspace prefix reserved for the stream-K flags
 
 SX_DEV float silu(float x) { return x / (1.0f + __expf(-x)); }
+SX_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 
 // ---- work segments: (tile, kb0, kb1) in processing order for unit c ---------
 struct SegIter {
@@ -138,10 +143,75 @@ SX_DEV int ld_acquire(const int* p) {
 SX_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 
 // Final epilogue of one 16-column chunk (values already summed over K).
-// xs: 16 x 64 fp32 smem exchange buffer (SWIGLU_IL: the up rows 64..127 of the
-// tile hand their values to the gate rows 0..63 of the same features).
+// xs: 16 x 128 fp32 smem tile (8 KB). Vector path: the 4 epilogue warps write
+// their rows (thread = feature, 16 tokens each) into xs[token][feature], then
+// every thread stores 16-byte runs of consecutive features of one token row
+// (8 bf16 / 4 fp32) instead of 16 scattered 2-4 byte stores; SWIGLU_IL reads
+// gate (rows 0..63) and up (rows 64..127) of the same 64 features from xs.
 SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float (&v2)[16], int f, int fl, bool fok,
                            int t0, float* xs) {
+  const int fbase = f - fl;  // first feature (weight row) of this CTA's 128-row tile
+  if (g.vec_store && (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_F32 || g.epi == SX_EPI_SWIGLU_IL)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xs[j * 128 + fl] = v[j];
+    epi_bar();
+    const int tid = fl;  // 0..127
+    if (g.epi == SX_EPI_BF16) {
+      // 16 tokens x 16 groups of 8 features = 256 items, 2 per thread
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int item = tid + it * 128, j = item >> 4, grp = item & 15;
+        const int t = t0 + j, f0 = fbase + grp * 8;
+        if (t < g.M) {
+          const float* src = xs + j * 128 + grp * 8;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + (long long)t * g.ldo + f0;
+          if (f0 + 8 <= g.Nf) {
+            uint4 pk;
+            pk.x = pack_bf16x2(src[0], src[1]);
+            pk.y = pack_bf16x2(src[2], src[3]);
+            pk.z = pack_bf16x2(src[4], src[5]);
+            pk.w = pack_bf16x2(src[6], src[7]);
+            *reinterpret_cast<uint4*>(o) = pk;
+          } else {
+            for (int e = 0; e < 8 && f0 + e < g.Nf; ++e) o[e] = __float2bfloat16(src[e]);
+          }
+        }
+      }
+    } else if (g.epi == SX_EPI_F32) {
+      // 16 tokens x 32 groups of 4 features = 512 items, 4 per thread
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int item = tid + it * 128, j = item >> 5, grp = item & 31;
+        const int t = t0 + j, f0 = fbase + grp * 4;
+        if (t < g.M) {
+          const float4 val = *reinterpret_cast<const float4*>(xs + j * 128 + grp * 4);
+          float* o = reinterpret_cast<float*>(g.out) + (long long)t * g.ldo + f0;
+          if (f0 + 4 <= g.Nf) {
+            *reinterpret_cast<float4*>(o) = val;
+          } else {
+            const float vv[4] = {val.x, val.y, val.z, val.w};
+            for (int e = 0; e < 4 && f0 + e < g.Nf; ++e) o[e] = vv[e];
+          }
+        }
+      }
+    } else {  // SWIGLU_IL: 16 tokens x 8 groups of 8 output features = 128 items
+      const int j = tid >> 3, grp = tid & 7;
+      const int t = t0 + j;
+      if (t < g.M && fbase < g.Nf) {  // a pair's second CTA may hold rows past N
+        const float* gs = xs + j * 128 + grp * 8;
+        const float* us = gs + 64;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + (long long)t * g.ldo + (fbase >> 1) + grp * 8;
+        uint4 pk;
+        pk.x = pack_bf16x2(silu(gs[0]) * us[0], silu(gs[1]) * us[1]);
+        pk.y = pack_bf16x2(silu(gs[2]) * us[2], silu(gs[3]) * us[3]);
+        pk.z = pack_bf16x2(silu(gs[4]) * us[4], silu(gs[5]) * us[5]);
+        pk.w = pack_bf16x2(silu(gs[6]) * us[6], silu(gs[7]) * us[7]);
+        *reinterpret_cast<uint4*>(o) = pk;
+      }
+    }
+    epi_bar();  // xs is rewritten by the next chunk
+    return;
+  }
   if (g.epi == SX_EPI_BF16) {
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
 #pragma unroll
@@ -175,7 +245,7 @@ SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float 
     epi_bar();
     if (fl < 64) {
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out);
-      const int fo = ((f - fl) >> 1) + r;  // tile rows 128j.. -> output features 64j..
+      const int fo = (fbase >> 1) + r;  // tile rows 128j.. -> output features 64j..
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         if (t0 + j < g.M && fok) o[(long long)(t0 + j) * g.ldo + fo] = __float2bfloat16(silu(v[j]) * xs[j * 64 + r]);
@@ -308,7 +378,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull_bar = empty_bar + g.stages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  float* xs = reinterpret_cast<float*>(smem + g.stages * g.stage_bytes + 1024);  // epilogue exchange, 4 KB
+  float* xs = reinterpret_cast<float*>(smem + g.stages * g.stage_bytes + 1024);  // epilogue tile, 8 KB
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -537,7 +607,7 @@ struct Plan {
   long long ws_floats;
 };
 
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024 - 4096;  // align pad, barriers, epilogue exchange
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024 - 8192;  // align pad, barriers, epilogue tile
 
 static bool use_pair(int M, int Nf, int dual, int cg_req) {
   if (Nf < 256) return false;
@@ -773,6 +843,8 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.tmem_cols = cols;
   g.out = out;
   g.ldo = ldo;
+  g.vec_store = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
+  if (epi == SX_EPI_SWIGLU_IL && (Nf % 128)) g.vec_store = 0;
   g.rs_rank = rs_rank;
   g.rs_world = rs_world;
   g.rs_slice = rs_slice;
@@ -780,7 +852,7 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.part = p.streamk ? ws + kFlagFloats : nullptr;
   g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
 
-  const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + 1024 + 4096;
+  const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + 1024 + 8192;
 #define SX_GEMM_LAUNCH(CG, DU, KP) \
   if (p.cg == CG && dual == DU && p.kpb == KP) return launch_gemm<CG, DU, KP>(ma, ma2, mb, g, smem, stream);
   SX_GEMM_LAUNCH(1, 0, 1)

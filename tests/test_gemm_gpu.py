@@ -154,3 +154,22 @@ def test_gemm_swiglu_interleaved(cuda, mode, sched, M, F, Kd):
             assert (y.float() - yd.float()).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
     finally:
         _lib.call("sx_gemm_set_pair_mode", 0)
+
+
+@pytest.mark.parametrize("epi", [K.EPI_BF16, K.EPI_F32])
+@pytest.mark.parametrize("M,N,Kd,ldo", [(1025, 1003, 256, 1024), (300, 4000, 512, 4000), (17, 520, 128, 1001)])
+def test_gemm_strided_output_edges(cuda, epi, M, N, Kd, ldo):
+    """Output into a wider row-strided buffer (vectorised 16-B epilogue when the
+    rows are 16-B aligned, partial last feature group, scalar path otherwise);
+    columns past N stay untouched."""
+    g = torch.Generator(device=cuda).manual_seed(M + N + ldo)
+    x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+    w = (torch.randn(N, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+    dt = torch.float32 if epi == K.EPI_F32 else torch.bfloat16
+    buf = torch.full((M, ldo), 7.0, dtype=dt, device=cuda)
+    K.gemm(x, w, out=buf[:, :N], epi=epi)
+    torch.cuda.synchronize()
+    ref = _ref(x, w)
+    tol = 1e-3 * Kd ** 0.5 if epi == K.EPI_F32 else 2e-2 * max(1.0, ref.abs().max().item())
+    assert (buf[:, :N].float() - ref).abs().max().item() < tol
+    assert (buf[:, N:] == 7.0).all()
