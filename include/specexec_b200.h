@@ -148,6 +148,19 @@ SX_API int sx_argmax_rows(const void* rows, int row_kind, long long ld, int V, i
 SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u, int n, int* out,
                           cudaStream_t stream);
 
+/* ------------------------------------------ KB1/KB2: beam search (8(f) row 4)
+ * One step of build_beam (pkg/src/speckit/tree.py:330-380): q = the beams'
+ * scored rows (fp64 [nb, ldq]), beam_nll / beam_rank (lex rank of each beam's
+ * path) per beam; keeps the beam_size best candidates by (nll, path).
+ * scratch: sx_beam_scratch_bytes(nb, V); c_* per-row candidate buffers
+ * [nb * beam_size] (c_cnt [nb]); out_* [beam_size], out_n: kept count.
+ * nb * beam_size <= 8192. */
+SX_API long long sx_beam_scratch_bytes(int nb, int V);
+SX_API int sx_beam_step(const double* q, long long ldq, int V, int nb, const double* beam_nll, const int* beam_rank,
+                        int beam_size, void* scratch, double* c_nll, double* c_edge, int* c_tok, int* c_cnt,
+                        int* out_n, double* out_nll, double* out_edge, int* out_beam, int* out_tok,
+                        cudaStream_t stream);
+
 /* ------------------------------------ KI1/KI2: SpecInfer baseline (8(f) row 1)
  * build_stochastic's draws (pkg/src/speckit/tree.py:383-425): token[i] =
  * sample(w[row_ids[i]], u[i]) and out_logq[i] = log w[row][token] (may be NULL).

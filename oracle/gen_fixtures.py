@@ -252,6 +252,35 @@ def gen_specinfer_grid(n=60):
     return out
 
 
+def gen_beam_instances(n=80):
+    """build_beam (tree.py:330-380) on Markov models, raw and warped scoring, plus
+    logits-LM draft at V=32000."""
+    out = []
+    for i in range(n):
+        gen = np.random.default_rng(6000 + i)
+        V = int(gen.integers(2, 12))
+        sharp = float(gen.uniform(0.05, 2.5))
+        beam, max_len = int(gen.integers(1, 9)), int(gen.integers(1, 6))
+        warp = [None, (0.6, 0.9), (0.0, 1.0), (1.0, 0.8)][i % 4]
+        model = speckit.make_synthetic(8000 + i, V, sharp)
+        prompt = tuple(int(x) for x in gen.integers(0, V, size=2))
+        cfg = speckit.SamplingConfig(*warp) if warp else None
+        tree = ref_tree.build_beam(prompt, model, beam, max_len, cfg)
+        out.append({"kind": "markov", "seed": 8000 + i, "V": V, "sharpness": sharp, "beam": beam, "max_len": max_len,
+                    "warp": warp, "prompt": list(prompt), "tree": tree_record(tree)})
+    for ci in range(3):
+        V = 32000
+        spec = {"vocab": V, "seed": 400 + ci, "scale": 2.2}
+        lm = ReplayLM(V, logits_model(spec))
+        prompt = tuple(int(x) for x in np.random.default_rng(970 + ci).integers(0, V, size=5))
+        beam, max_len = [8, 16, 4][ci], [4, 3, 6][ci]
+        warp = [None, (0.6, 0.9), (1.0, 1.0)][ci]
+        tree = ref_tree.build_beam(prompt, lm, beam, max_len, speckit.SamplingConfig(*warp) if warp else None)
+        out.append({"kind": "logits", "spec": spec, "beam": beam, "max_len": max_len, "warp": warp,
+                    "prompt": list(prompt), "tree": tree_record(tree)})
+    return out
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     jobs = {
@@ -261,6 +290,7 @@ def main():
         "logit_trees.json": gen_logit_trees,
         "logit_engine.json": gen_logit_engine,
         "specinfer_grid.json": gen_specinfer_grid,
+        "beam_instances.json": gen_beam_instances,
     }
     only = set(sys.argv[1:])
     for name, fn in jobs.items():

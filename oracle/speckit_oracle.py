@@ -854,3 +854,53 @@ def schedule_size(branching: list[int]) -> int:
         level *= width
         total += level
     return total
+
+
+# ---------------------------------------------------------------------------
+# tree.py build_beam (Appendix F ablation)
+# ---------------------------------------------------------------------------
+
+
+def build_beam(prefix, draft, beam_size: int, max_len: int, warp=None, warp_scores: bool = True) -> DraftTree:
+    """tree.py:330-380 -- standard beam search under (nll, path); the tree is the
+    prefix closure of the final beam, node ids in (length, path) order.
+
+    One exact shortcut: each beam row contributes only its `beam_size` best
+    candidates by (nll, token) -- within a row the path prefix is shared, so no
+    other candidate of that row can reach the global top `beam_size`."""
+    if beam_size < 1:
+        raise ValueError(f"beam_size must be >= 1, got {beam_size}")
+    if max_len < 1:
+        raise ValueError(f"max_len must be >= 1, got {max_len}")
+    tree = DraftTree(prefix)
+    beams: list[tuple[float, Prefix]] = [(0.0, ())]
+    edges: dict[Prefix, float] = {}
+    for _ in range(max_len):
+        dists = draft.next_distributions([tuple(prefix) + path for _, path in beams])
+        tree.rounds += 1
+        candidates = []
+        for (nll, path), dist in zip(beams, dists):
+            scored = _scored_dist(dist, warp, warp_scores)
+            toks = np.nonzero(scored > 0)[0]
+            edge = ox_log(scored[toks])
+            cn = nll - edge
+            if toks.size > beam_size:
+                keep = np.lexsort((toks, cn))[:beam_size]
+                toks, edge, cn = toks[keep], edge[keep], cn[keep]
+            for t, e, c in zip(toks.tolist(), edge.tolist(), cn.tolist()):
+                candidates.append((c, path + (int(t),), e))
+        if not candidates:
+            break
+        candidates.sort(key=lambda c: (c[0], c[1]))
+        kept = candidates[:beam_size]
+        for _, path, edge in kept:
+            edges[path] = edge
+        beams = [(nll, path) for nll, path, _ in kept]
+    keep: set[Prefix] = set()
+    for _, path in beams:
+        for end in range(1, len(path) + 1):
+            keep.add(path[:end])
+    path_to_id: dict[Prefix, int] = {(): ROOT}
+    for path in sorted(keep, key=lambda p: (len(p), p)):
+        path_to_id[path] = tree.add_child(path_to_id[path[:-1]], path[-1], edges[path])
+    return tree

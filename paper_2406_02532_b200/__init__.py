@@ -14,6 +14,7 @@ from .models import LanguageModel, MarkovModel, TabularModel, make_synthetic, mo
 from .rng import CounterRng
 from .sampling import SamplingConfig, apply_warp, sample, validate_distribution
 from .tree import ROOT, BuilderParams, DraftNode, DraftTree, FlattenedTree, build_sssp, flatten
+from .beam import build_beam
 from .specinfer import (VerifyOutcome, branching_for_budget, build_stochastic, generate_specinfer, schedule_size,
                         verify_specinfer)
 
@@ -34,6 +35,7 @@ __all__ = [
     "TabularModel",
     "apply_warp",
     "build_sssp",
+    "build_beam",
     "build_stochastic",
     "branching_for_budget",
     "generate_specinfer",

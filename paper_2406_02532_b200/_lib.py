@@ -57,6 +57,11 @@ SIGNATURES: dict[str, tuple] = {
     "sx_softmax_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _c_ll, _vp]),
     "sx_argmax_rows": (_c_int, [_vp, _c_int, _c_ll, _c_int, _c_int, _vp, _vp]),
     "sx_sample_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _vp]),
+    "sx_beam_scratch_bytes": (_c_ll, [_c_int, _c_int]),
+    "sx_beam_step": (
+        _c_int,
+        [_vp, _c_ll, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    ),
     "sx_sample_rows_idx": (_c_int, [_vp, _c_ll, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp]),
     "sx_specinfer_verify": (
         _c_int,

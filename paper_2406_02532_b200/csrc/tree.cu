@@ -653,9 +653,147 @@ __global__ void markov_rows_kernel(const double* __restrict__ table, int V, int 
   for (int v = threadIdx.x; v < V; v += blockDim.x) dst[v] = src[v];
 }
 
+// --------------------------------------------------------------------------
+// KB1/KB2: beam search (build_beam, pkg/src/speckit/tree.py:330-380).
+// KB1, one CTA per beam row: every token with q > 0 gets nll = beam_nll - log q
+// (canonical log), the row's candidates are radix-sorted by (nll, token) and
+// the first k kept (no other candidate of the row can reach the global top k:
+// its path prefix is shared). KB2, one CTA: the nb x k survivors sorted by
+// (nll, lex rank of the beam path, token) -- the reference's (nll, path) order
+// for equal-length paths -- and the first beam_size returned.
+__global__ void __launch_bounds__(kRowThreads) beam_row_topk_kernel(const double* q, long long ldq, int V,
+                                                                     const double* beam_nll, int k,
+                                                                     unsigned long long* keys, int* idx,
+                                                                     unsigned long long* keys2, int* idx2,
+                                                                     double* c_nll, double* c_edge, int* c_tok,
+                                                                     int* c_cnt) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
+  const int b = blockIdx.x;
+  const double* row = q + (long long)b * ldq;
+  const long long o = (long long)b * V;
+  const double bn = beam_nll[b];
+  int valid = 0;
+  for (int v = threadIdx.x; v < V; v += kRowThreads) {
+    const double p = row[v];
+    unsigned long long key = ~0ULL;
+    if (p > 0.0) {
+      key = (unsigned long long)__double_as_longlong(dsub(bn, sx_log(p)));
+      ++valid;
+    }
+    keys[o + v] = key;
+    idx[o + v] = v;
+  }
+  __threadfence_block();
+  __syncthreads();
+  block_radix_sort(sm, keys + o, idx + o, keys2 + o, idx2 + o, V, 8);  // 8 passes: result in keys/idx
+  // count of valid entries = block sum of `valid`
+  sm.redi[threadIdx.x] = valid;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kRowThreads; ++i) tot += sm.redi[i];
+    sm.redi[0] = tot;
+  }
+  __syncthreads();
+  const int cnt = min(k, sm.redi[0]);
+  for (int i = threadIdx.x; i < cnt; i += kRowThreads) {
+    const int tok = idx[o + i];
+    const double nll = __longlong_as_double((long long)keys[o + i]);
+    c_nll[(long long)b * k + i] = nll;
+    c_edge[(long long)b * k + i] = sx_log(row[tok]);
+    c_tok[(long long)b * k + i] = tok;
+  }
+  if (threadIdx.x == 0) c_cnt[b] = cnt;
+}
+
+constexpr int kBeamSortMax = 8192;
+
+__global__ void __launch_bounds__(1024) beam_select_kernel(int nb, int k, const int* beam_rank, const double* c_nll,
+                                                          const double* c_edge, const int* c_tok, const int* c_cnt,
+                                                          int beam_size, int* out_n, double* out_nll,
+                                                          double* out_edge, int* out_beam, int* out_tok) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int total = nb * k;
+  int n = 1;
+  while (n < total) n <<= 1;
+  unsigned long long* kh = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned long long* kl = kh + n;
+  int* kv = reinterpret_cast<int*>(kl + n);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int b = i / k, j = i % k;
+    if (i < total && j < c_cnt[b]) {
+      kh[i] = (unsigned long long)__double_as_longlong(c_nll[i]);
+      kl[i] = ((unsigned long long)(unsigned)beam_rank[b] << 32) | (unsigned)c_tok[i];
+      kv[i] = i;
+    } else {
+      kh[i] = ~0ULL;
+      kl[i] = ~0ULL;
+      kv[i] = -1;
+    }
+  }
+  __syncthreads();
+  bitonic_sort_128(kh, kl, kv, n);
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    while (c < beam_size && c < n && kv[c] >= 0) ++c;
+    s_n = c;
+    *out_n = c;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s_n; i += blockDim.x) {
+    const int src = kv[i];
+    out_nll[i] = c_nll[src];
+    out_edge[i] = c_edge[src];
+    out_beam[i] = src / k;
+    out_tok[i] = c_tok[src];
+  }
+}
+
 }  // namespace sx
 
 using namespace sx;
+
+extern "C" long long sx_beam_scratch_bytes(int nb, int V) {
+  const long long e = (long long)nb * V;
+  auto al = [](long long x) { return (x + 255) & ~255LL; };
+  return 2 * al(8 * e) + 2 * al(4 * e);
+}
+
+extern "C" int sx_beam_step(const double* q, long long ldq, int V, int nb, const double* beam_nll,
+                            const int* beam_rank, int beam_size, void* scratch, double* c_nll, double* c_edge,
+                            int* c_tok, int* c_cnt, int* out_n, double* out_nll, double* out_edge, int* out_beam,
+                            int* out_tok, cudaStream_t stream) {
+  if (nb < 1 || V < 2 || beam_size < 1) return arg_error("beam_step: need nb >= 1, V >= 2, beam_size >= 1");
+  if ((long long)nb * beam_size > kBeamSortMax)
+    return arg_error("beam_step: %d beams x beam_size %d exceed the %d-entry single-CTA sort", nb, beam_size,
+                     kBeamSortMax);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(beam_row_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
+    cudaFuncSetAttribute(beam_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBeamSortMax * 20);
+    attr = true;
+  }
+  const long long e = (long long)nb * V;
+  auto al = [](long long x) { return (x + 255) & ~255LL; };
+  uint8_t* s = reinterpret_cast<uint8_t*>(scratch);
+  unsigned long long* k1 = reinterpret_cast<unsigned long long*>(s);
+  unsigned long long* k2 = reinterpret_cast<unsigned long long*>(s + al(8 * e));
+  int* i1 = reinterpret_cast<int*>(s + 2 * al(8 * e));
+  int* i2 = reinterpret_cast<int*>(s + 2 * al(8 * e) + al(4 * e));
+  const int k = beam_size;
+  beam_row_topk_kernel<<<nb, kRowThreads, sizeof(RowSmem), stream>>>(q, ldq, V, beam_nll, k, k1, i1, k2, i2, c_nll,
+                                                                       c_edge, c_tok, c_cnt);
+  SX_CHECK_LAUNCH("beam_row_topk_kernel");
+  int n = 1;
+  while (n < nb * k) n <<= 1;
+  const size_t smem = (size_t)n * 20;
+  beam_select_kernel<<<1, 1024, smem, stream>>>(nb, k, beam_rank, c_nll, c_edge, c_tok, c_cnt, beam_size, out_n,
+                                                out_nll, out_edge, out_beam, out_tok);
+  SX_CHECK_LAUNCH("beam_select_kernel");
+  return SX_OK;
+}
 
 static size_t upd_smem_bytes(const TreeLayout& L) {
   return ((sizeof(UpdSmem) + 15) & ~size_t(15)) + (size_t)L.kpad * (8 + 8 + 4) + 64;

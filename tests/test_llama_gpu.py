@@ -155,3 +155,26 @@ def test_offloaded_target_matches_resident(pair):
     b, sb = sx.generate_specexec((5, 6, 7, 8), draft, off, sx.BuilderParams(64, 8, 16), cfg)
     assert a == b and sa.accepted_per_iteration == sb.accepted_per_iteration
     assert off.streamer.bytes >= off.w.layer_bytes * off.cfg.layers * sb.target_calls
+
+
+@pytest.mark.parametrize("V,K_,D_,B_", [(128256, 2048, 8, 128), (32000, 8192, 12, 1024)])
+def test_large_tree_replay_bit_exact(cuda, V, K_, D_, B_):
+    """SURVEY 8(a) sizes: a Llama-3-vocabulary draft (V = 128256) and the largest
+    budget (K = 8192) -- the GPU tree equals the oracle's build_sssp on the
+    GPU's own rows (raw scoring), node for node."""
+    from paper_2406_02532_b200.llama import LlamaConfig
+
+    cfg = LlamaConfig(V, 256, 2, 2, 1, 512, 5e5, 1e-5, name=f"tiny-v{V}")
+    draft = LlamaModel(cfg, seed=5, max_ctx=4 * K_ + 2 * B_ * (D_ + 1) + 256, max_tokens=max(B_, 64),
+                       synthetic=SyntheticBias(seed=3, rank=64, scale=3.0))
+    draft.record = []
+    prompt = tuple(int(t) for t in np.random.default_rng(V + K_).integers(0, V, size=16))
+    g = sx.build_sssp(prompt, draft, sx.BuilderParams(K_, D_, B_), None, warp_scores=False)
+    tab = draft.record[-1]
+    draft.record = None
+    lm = ox.LogitsLM(V, lambda ps: np.stack([tab[tuple(q)] for q in ps]))
+    o = ox.build_sssp(prompt, lm, ox.BuilderParams(K_, D_, B_), None, warp_scores=False)
+    assert len(g.nodes) == K_
+    assert [(n.parent, n.token) for n in g.nodes] == [(n.parent, n.token) for n in o.nodes]
+    assert [n.edge_logprob for n in g.nodes] == [n.edge_logprob for n in o.nodes]
+    assert g.rounds == o.rounds

@@ -199,3 +199,15 @@ def test_specinfer_schedules():
     assert ox.branching_for_budget(5, 8) == [1, 1, 1, 1, 1]
     with pytest.raises(ValueError):
         ox.branching_for_budget(0, 3)
+
+
+def test_beam_instances_match_reference():
+    """build_beam (tree.py:330-380): the oracle's trees equal the reference's."""
+    for i, rec in enumerate(load("beam_instances.json")):
+        if rec["kind"] == "markov":
+            model = ox.make_synthetic(rec["seed"], rec["V"], rec["sharpness"])
+        else:
+            model = logits_lm(rec["spec"])
+        warp = ox.SamplingConfig(*rec["warp"]) if rec["warp"] else None
+        tree = ox.build_beam(tuple(rec["prompt"]), model, rec["beam"], rec["max_len"], warp)
+        assert_tree_matches(tree, rec["tree"], i)
