@@ -98,6 +98,14 @@ SX_DEV void tma_load_2d_hint(void* smem_dst, const CUtensorMap* map, uint64_t* b
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// L2 prefetch of one TMA box (no shared memory, no barrier)
+SX_DEV void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1)
+               : "memory");
+}
+// Programmatic dependent launch: wait for the preceding grid (and its memory)
+SX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 SX_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

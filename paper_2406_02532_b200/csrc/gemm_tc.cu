@@ -422,6 +422,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint64_t pol_w = g.tiles_t == 1 ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = policy_evict_last();   // token tiles are re-read by every weight tile
     const int bhalf = g.BN / CG;
+    {
+      // Programmatic dependent launch: this grid may start while the previous
+      // kernel drains. The weights do not depend on it -- warm L2 with the first
+      // ring of weight boxes, then wait before touching its outputs (tokens).
+      SegIter it0(g, unit);
+      int tile, kb0, kb1;
+      if (it0.next(g, tile, kb0, kb1) && elect_one()) {
+        const int frow = (tile / g.tiles_t) * 128 * CG + (int)rank * 128;
+        const int n = min(kb1 - kb0, g.stages);
+        for (int kb = kb0; kb < kb0 + n; ++kb)
+          for (int j = 0; j < KPB; ++j) {
+            tma_prefetch_2d(&mapA, (kb * KPB + j) * 64, frow);
+            if (DUAL) tma_prefetch_2d(&mapA2, (kb * KPB + j) * 64, frow);
+          }
+      }
+      __syncwarp();
+      griddep_wait();
+    }
     int stage = 0;
     uint32_t phase = 0;
     int issued = 0;
@@ -511,6 +529,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
+    griddep_wait();  // outputs may still be read by the previous kernel
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int fl = quarter * 32 + lane;
     const int slot = unit * CG + (int)rank;  // this CTA's partial slot / flag
@@ -571,6 +590,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // 0 = auto (pair when the tree pass has >= 256 tokens), 1 = single-CTA only, 2 = pair whenever legal.
 static int g_pair_mode = 0;
+// programmatic dependent launch of the GEMM (SX_GEMM_PDL=0 disables)
+static const int g_pdl = getenv("SX_GEMM_PDL") ? atoi(getenv("SX_GEMM_PDL")) : 1;
 
 // tuning overrides (read once): SX_GEMM_BN_CAP (token-tile cap), SX_GEMM_STAGES (max pipeline depth),
 // SX_GEMM_KPB (64-wide k-blocks per stage; 0 = auto)
@@ -646,6 +667,27 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
   if (bn_req > 0) cap = bn_req < cap ? bn_req : cap;
   p.bn = pick_bn(M, cap);
   p.tiles_f = (Nf + fr - 1) / fr;
+  // CTA-pair tree-pass shapes: the token-tile width sets both the padding of
+  // M = K+1 and how the tiles fill the 74 pairs; pick the width with the lowest
+  // (rounds x width) over {auto, 176, 128} when it is >10% better (70B o-proj at
+  // M = 1025: 160 tiles of 208 = 2.2 rounds -> 288 tiles of 128 = 3.9 rounds,
+  // 118 -> 113 us, profiles/r1/plan_sweep_c2.jsonl).
+  if (p.cg == 2 && bn_req == 0 && !dual && K <= 8192) {  // long-K shapes balance with the split tail instead
+    auto cost = [&](int bn) {
+      const long long t = (long long)p.tiles_f * ((M + bn - 1) / bn);
+      return (double)((t + P - 1) / P) * bn;
+    };
+    int best = p.bn;
+    double best_cost = cost(p.bn);
+    for (int c : {176, 128}) {
+      const int bn = pick_bn(M, c < cap ? c : cap);
+      if (cost(bn) < 0.9 * best_cost) {
+        best = bn;
+        best_cost = cost(bn);
+      }
+    }
+    p.bn = best;
+  }
   // Weight-streaming shapes with few weight tiles (e.g. a 4096-wide projection of
   // the draft = 32 tiles): a single SM's TMA pulls only ~40-50 GB/s, so use
   // narrower token tiles until ~120+ CTAs stream. The weight tile is shared by
@@ -742,13 +784,15 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& ma2, const CUte
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CG;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol.wait in the kernel)
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, kern, ma, ma2, mb, g);
   SX_CHECK_LAUNCH("gemm_tc_kernel");
   return SX_OK;
