@@ -151,21 +151,6 @@ SX_DEV void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint3
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// D[tmem] (+)= A[tmem] * B[smem]^T: the A operand is read from TMEM (the "TS"
-// form), so only B is fetched from shared memory by the MMA.
-SX_DEV void tc_mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
-      : "memory");
-}
-// shared -> tensor memory copy of a 128-row x 256-bit slice (one K=16 bf16 slice of a
-// 128-row operand described by a K-major SW128 descriptor) into 8 TMEM columns
-SX_DEV void tc_cp_128x256b(uint32_t taddr, uint64_t s_desc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(s_desc) : "memory");
-}
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 SX_DEV void tc_commit(uint64_t* bar) {
   asm volatile(

@@ -33,7 +33,7 @@ import torch
 from . import _lib
 from . import kernels as K
 from .models import LanguageModel, _WS, _check_prefix
-from .tp import TPShard
+from .tp import TPShard, gather_vocab
 from .tree import BuilderParams, tree_tables
 
 
@@ -428,10 +428,7 @@ class LlamaModel(LanguageModel):
         else:  # vocab-parallel LM head: local slice, all-gather, interleave the slices into [m, V]
             ll = b.logits_l[:m]
             K.gemm(hh, w.lm, out=ll, epi=K.EPI_F32)
-            Vl = ll.shape[1]
-            gbuf = b.logits_g.view(-1)[: tp.world * m * Vl].view(tp.world, m, Vl)
-            tp.all_gather_(ll, gbuf)
-            logits.view(m, tp.world, Vl).copy_(gbuf.transpose(0, 1))
+            gather_vocab(tp, ll, logits, b.logits_g)
         if self.synthetic is not None:
             bi = self.bias_in[:m]
             torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)

@@ -104,6 +104,18 @@ class TPShard:
         raise KeyError(name)
 
 
+def gather_vocab(comm, local: torch.Tensor, out: torch.Tensor, staging: torch.Tensor) -> None:
+    """Vocab-parallel LM head: every rank holds logits[:, r*Vl:(r+1)*Vl] in
+    `local` [m, Vl]; all-gather into `staging` (>= world*m*Vl elements) and
+    interleave the slices into `out` [m, world*Vl] -- the same full rows on
+    every rank."""
+    m, Vl = local.shape
+    W = comm.world
+    g = staging.view(-1)[: W * m * Vl].view(W, m, Vl)
+    comm.all_gather_(local, g)
+    out.view(m, W, Vl).copy_(g.transpose(0, 1))
+
+
 class NcclComm:
     """torch.distributed communicator (NCCL over NVLink on the B200 box)."""
 
@@ -120,7 +132,8 @@ class NcclComm:
 
     def all_gather_(self, local: torch.Tensor, out: torch.Tensor) -> None:
         """local [world-slices of out]: out [world, *local.shape] contiguous."""
-        self.dist.all_gather_into_tensor(out, local, group=self.group)
+        # concatenated layout [world * rows, ...] (accepted by every backend)
+        self.dist.all_gather_into_tensor(out.view(-1, *local.shape[1:]), local, group=self.group)
 
     def broadcast_ints(self, vals: list[int], src: int = 0) -> list[int]:
         t = torch.tensor(vals, dtype=torch.int64, device="cuda")

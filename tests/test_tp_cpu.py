@@ -79,3 +79,31 @@ def test_tp_shard_checks():
     assert sh.heads(CFG) == (2, 4) and sh.kv_heads(CFG) == (1, 2) and sh.vocab(CFG) == (48, 96)
     shapes = sh.local_shapes(CFG)
     assert shapes["wqkv"] == ((2 + 2) * 16, 64) and shapes["wd"] == (64, 48)
+
+
+def _comm_worker(rank, world, port, out):
+    """NcclComm (the torch.distributed communicator the GPU model uses) over
+    gloo: all-reduce and the vocab-parallel logits gather + interleave."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_02532_b200.tp import NcclComm, gather_vocab
+
+    comm = NcclComm()
+    y = torch.full((3, 4), float(rank + 1))
+    comm.all_reduce_(y)
+    m, Vl = 5, 3
+    full = torch.arange(m * Vl * world, dtype=torch.float32).view(m, Vl * world)
+    local = full[:, rank * Vl : (rank + 1) * Vl].contiguous()
+    got = torch.empty(m, Vl * world)
+    gather_vocab(comm, local, got, torch.empty(world * m * Vl + 7))
+    out[rank] = (float(y[0, 0]), bool(torch.equal(got, full)))
+    dist.destroy_process_group()
+
+
+def test_nccl_comm_semantics_over_gloo():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        assert out[r][0] == 3.0 and out[r][1]

@@ -29,6 +29,11 @@ SETS = {
         ("7b.qkv.m1", 1, 12288, 4096, BF16), ("7b.o.m1", 1, 4096, 4096, F32),
         ("7b.gate_up.m1", 1, 22016, 4096, IL), ("7b.down.m1", 1, 4096, 11008, F32),
     ],
+    "draft1024": [
+        ("7b.qkv", 1024, 12288, 4096, BF16), ("7b.o", 1024, 4096, 4096, F32),
+        ("7b.gate_up", 1024, 22016, 4096, IL), ("7b.down", 1024, 4096, 11008, F32),
+        ("7b.lm", 1024, 32000, 4096, F32),
+    ],
     "c4": [
         ("70b.qkv", 4097, 10240, 8192, BF16), ("70b.o", 4097, 8192, 8192, F32),
         ("70b.gate_up", 4097, 57344, 8192, IL), ("70b.down", 4097, 8192, 28672, F32),
