@@ -387,6 +387,28 @@ def main():
 
     # dominant kernel: the tcgen05 GEMM of the target pass over the tree
     pk = peaks()
+    # iteration roofline: target pass = its GEMM FLOPs at the sustained bf16 peak;
+    # draft = per call max(FLOPs at peak, weight bytes at HBM) over the rows it
+    # forwards (B per batched round, 1 for the root round); walk/host ~ 0
+    tcfg, dcfg = PRESETS[tname], PRESETS[dname]
+    dcalls = draft_calls / max(1, iters)
+    d_params = dcfg.n_params() - dcfg.vocab * dcfg.d  # embedding rows are gathered, not multiplied
+    d_round = lambda rows: max(2.0 * rows * d_params / (pk["bf16_sus"] * 1e12),  # noqa: E731
+                               dcfg.weight_bytes() / (pk["hbm"] * 1e9))
+    draft_bound = d_round(1) + max(0.0, dcalls - 1) * d_round(B)
+    if offload:
+        target_bound = PRESETS[tname].weight_bytes() / (h2d_peak * 1e9) if h2d_peak else 0.0
+    else:
+        t_params = tcfg.n_params() - tcfg.vocab * tcfg.d
+        target_bound = 2.0 * (K + 1) * t_params / (pk["bf16_sus"] * 1e12)
+    if tp:
+        target_bound /= world  # the target pass is sharded over the ranks
+    roof_s = draft_bound + target_bound
+    iter_roofline = {"target_bound_ms": target_bound * 1e3, "draft_bound_ms": draft_bound * 1e3,
+                     "tokens_per_s_at_roofline": accepted_per_iter / roof_s if roof_s > 0 else None,
+                     "frac": (roof_s * 1e3) / (ms_max / args.steps) if ms_max > 0 else None,
+                     "note": "target: 2*(K+1)*params at the measured sustained bf16 peak (offload: weight bytes at the "
+                             "measured pinned H2D rate); draft: per call max(2*rows*params at peak, weights at HBM)"}
     gemm_shapes = prof.by_shape(steps=args.steps)
     big = prof.summary(min_m=max(2, K // 2))
     small = prof.summary(min_m=0)
@@ -454,6 +476,7 @@ def main():
             "accepted_tokens_per_iter": accepted_per_iter,
             "draft_calls_per_iter": draft_calls / max(1, iters),
             "stage_ms_per_step": stages,
+            "iteration_roofline": iter_roofline,
             "gemm_shapes": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in gemm_shapes],
             "roofline": roof,
             "cpu_baseline": cb,

@@ -7,7 +7,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tree_score|tree_row_stats|tree_update" -s 2 -c 6 -o gpurun_out/ncu_tree $B > gpurun_out/ncu_tree.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tree_attention" -s 200 -c 2 -o gpurun_out/ncu_attn $B > gpurun_out/ncu_attn.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kv_compact|verify_walk|add_rmsnorm|rope_kv" -s 300 -c 6 -o gpurun_out/ncu_misc $B > gpurun_out/ncu_misc.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"add_rmsnorm|rope_kv" -s 300 -c 4 -o gpurun_out/ncu_misc $B > gpurun_out/ncu_misc.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kv_compact|verify_walk" -s 4 -c 4 -o gpurun_out/ncu_walk $B --synthetic 4 > gpurun_out/ncu_walk.log 2>&1
 for s in 70b.qkv 70b.o 70b.gate_up_il 70b.down 7b.gate_up_il; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 2 -c 1 -o gpurun_out/ncu_gemm_$s python tools/gemm_one.py $s 0 >> gpurun_out/ncu_gemm.log 2>&1
 done
