@@ -108,14 +108,14 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
     sm.dlen[tid] = dl;
     atomicMax(&sm.maxlen, dl);
   }
-  if (tid == 0) {  // ancestor segments of the CTA's tokens (prefix sum, <= 64 tokens)
-    int acc = 0;
-    for (int i = 0; i < a.QB; ++i) {
-      sm.seg[i] = acc;
-      const int t = t0 + i;
-      acc += (t < a.N && a.anc_len) ? a.anc_len[t] : 0;
-    }
-    sm.seg[a.QB] = acc;
+  if (tid < a.QB) {  // ancestor counts, loaded in parallel
+    const int t = t0 + tid;
+    sm.seg[tid + 1] = (t < a.N && a.anc_len) ? a.anc_len[t] : 0;
+  }
+  __syncthreads();
+  if (tid == 0) {  // ancestor segments of the CTA's tokens (prefix sum over smem, <= 64 tokens)
+    sm.seg[0] = 0;
+    for (int i = 1; i <= a.QB; ++i) sm.seg[i] += sm.seg[i - 1];
   }
   __syncthreads();
   const int n_anc = sm.seg[a.QB];

@@ -151,12 +151,13 @@ SX_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 
 SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float (&v2)[16], int f, int fl, bool fok,
                            int t0, float* xs) {
   const int fbase = f - fl;  // first feature (weight row) of this CTA's 128-row tile
-  if (g.vec_store && (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_F32 || g.epi == SX_EPI_SWIGLU_IL)) {
+  if (g.vec_store &&
+      (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_F32 || g.epi == SX_EPI_SWIGLU_IL || g.epi == SX_EPI_RS_BF16)) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) xs[j * 128 + fl] = v[j];
     epi_bar();
     const int tid = fl;  // 0..127
-    if (g.epi == SX_EPI_BF16) {
+    if (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_RS_BF16) {
       // 16 tokens x 16 groups of 8 features = 256 items, 2 per thread
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
@@ -164,7 +165,14 @@ SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float 
         const int t = t0 + j, f0 = fbase + grp * 8;
         if (t < g.M) {
           const float* src = xs + j * 128 + grp * 8;
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + (long long)t * g.ldo + f0;
+          __nv_bfloat16* o;
+          if (g.epi == SX_EPI_RS_BF16) {  // owner's inbox over peer memory: 16-B stores into its slice
+            const int owner = f0 / g.rs_slice;
+            o = reinterpret_cast<__nv_bfloat16* const*>(g.out)[owner] +
+                ((long long)g.rs_rank * g.M + t) * g.rs_slice + (f0 - owner * g.rs_slice);
+          } else {
+            o = reinterpret_cast<__nv_bfloat16*>(g.out) + (long long)t * g.ldo + f0;
+          }
           if (f0 + 8 <= g.Nf) {
             uint4 pk;
             pk.x = pack_bf16x2(src[0], src[1]);
@@ -888,6 +896,7 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.out = out;
   g.ldo = ldo;
   g.vec_store = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
+  if (epi == SX_EPI_RS_BF16) g.vec_store = (rs_slice % 128 == 0) ? 1 : 0;  // inbox rows are 16-B aligned slices
   if (epi == SX_EPI_SWIGLU_IL && (Nf % 128)) g.vec_store = 0;
   g.rs_rank = rs_rank;
   g.rs_world = rs_world;
