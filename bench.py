@@ -354,7 +354,7 @@ def main():
     from paper_2406_02532_b200 import engine as Eng
 
     Eng.STAGES = Eng.StageTimer()
-    launches0 = _lib.load().sx_launch_count()
+    launches0 = _lib.load().sx_launch_count() + Kern.GRAPH_KERNELS[0]
     streamed0 = target.streamer.bytes if offload else 0
     it0, tok0, dc0 = sess.stats.target_calls, len(sess.tokens), sess.stats.draft_calls
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -370,7 +370,7 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
-    launches = _lib.load().sx_launch_count() - launches0
+    launches = _lib.load().sx_launch_count() + Kern.GRAPH_KERNELS[0] - launches0  # direct + graph-replayed
     prof = Kern.PROFILER
     stages = {k: v / args.steps for k, v in Eng.STAGES.totals().items()}
     Eng.STAGES = None

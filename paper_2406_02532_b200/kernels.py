@@ -29,6 +29,8 @@ _ws_cache: dict[tuple[int, int], torch.Tensor] = {}
 
 # host<->device bytes moved by the engine's control path (bench.py's e2e accounting)
 IO = {"h2d": 0, "d2h": 0}
+# kernels of this library launched by CUDA-graph replays (sx_launch_count sees only the capture)
+GRAPH_KERNELS = [0]
 
 
 class GemmProfiler:

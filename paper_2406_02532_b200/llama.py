@@ -471,11 +471,14 @@ class LlamaModel(LanguageModel):
         if self._g1 is None and self._g1_warm:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
+            n0 = _lib.load().sx_launch_count()
             with torch.cuda.graph(g):
                 self._g1_out = self.forward(1, tok, pos, 0, slot, 0, dl, 0, None, 0, None, 0, 0)
+            self._g1_kernels = _lib.load().sx_launch_count() - n0
             self._g1 = g
         if self._g1 is not None:
             self._g1.replay()
+            K.GRAPH_KERNELS[0] += self._g1_kernels
             out = self._g1_out
             self.stats["forward_tokens"] += 1
             self.stats["forwards"] += 1
@@ -666,11 +669,14 @@ class _LlamaDraftSession:
                 return ctl
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
+            n0 = _lib.load().sx_launch_count()
             with torch.cuda.graph(g):
                 self._fixed_forward()
                 ws.launch_round(m.buf.logits[: ws.B], mode, temp, top_p)
+            g.sx_kernels = _lib.load().sx_launch_count() - n0
             ws._graphs[key] = g
         g.replay()
+        K.GRAPH_KERNELS[0] += g.sx_kernels
         ctl = ws.read_ctl()
         self._record(snap)
         return ctl
