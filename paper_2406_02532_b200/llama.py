@@ -648,6 +648,15 @@ class _LlamaDraftSession:
     # -- fused round: fixed-shape draft forward over all B batch rows (rows past
     # batch_n are padding that writes only the scratch slot) + scoring + update,
     # replayed as one CUDA graph per (model, workspace, scoring mode).
+    def _bucket(self) -> int:
+        """Rows the fixed-shape round runs: the smallest power of two (>= 32)
+        covering the current batch, capped at B -- deep trees expand a few
+        frontier nodes per round; padding every round to B wasted the draft."""
+        B, n = self.ws.B, 32
+        while n < self.batch_n and n < B:
+            n *= 2
+        return min(n, B)
+
     def run_round(self, mode: int, temp: float, top_p: float) -> dict:
         m, ws = self.m, self.ws
         if self.first or not m.use_graphs or ws.B > m.buf.n:
@@ -656,14 +665,15 @@ class _LlamaDraftSession:
         snap = self._snapshot() if self.rec is not None else None
         if not hasattr(ws, "_graphs"):
             ws._graphs = {}
-        key = (m._uid, mode, temp, top_p)
+        n = self._bucket()
+        key = (m._uid, mode, temp, top_p, n)
         g = ws._graphs.get(key)
         if g is None:
             if key not in getattr(ws, "_graph_warm", set()):
                 # one eager fixed-shape round first (sets kernel attributes, tensor maps, scratch)
                 ws._graph_warm = getattr(ws, "_graph_warm", set()) | {key}
-                self._fixed_forward()
-                ws.launch_round(m.buf.logits[: ws.B], mode, temp, top_p)
+                self._fixed_forward(n)
+                ws.launch_round(m.buf.logits[:n], mode, temp, top_p)
                 ctl = ws.read_ctl()
                 self._record(snap)
                 return ctl
@@ -671,8 +681,8 @@ class _LlamaDraftSession:
             g = torch.cuda.CUDAGraph()
             n0 = _lib.load().sx_launch_count()
             with torch.cuda.graph(g):
-                self._fixed_forward()
-                ws.launch_round(m.buf.logits[: ws.B], mode, temp, top_p)
+                self._fixed_forward(n)
+                ws.launch_round(m.buf.logits[:n], mode, temp, top_p)
             g.sx_kernels = _lib.load().sx_launch_count() - n0
             ws._graphs[key] = g
         g.replay()
@@ -696,10 +706,10 @@ class _LlamaDraftSession:
             self.slot_path[slots[b]] = path
             self.rec[self.prefix + path] = rows[b].copy()
 
-    def _fixed_forward(self) -> None:
-        ws, B = self.ws, self.ws.B
-        self.m.forward(B, ws.batch_tokens(), ws.batch_pos(), 0, ws.batch_slots(), 0, ws.batch_dense(), 0,
-                       ws.batch_anc(), 0, ws.batch_anc_len(), ws.D + 1, 0)
+    def _fixed_forward(self, n: int) -> None:
+        ws = self.ws
+        self.m.forward(n, ws.batch_tokens()[:n], ws.batch_pos()[:n], 0, ws.batch_slots()[:n], 0,
+                       ws.batch_dense()[:n], 0, ws.batch_anc()[:n], 0, ws.batch_anc_len()[:n], ws.D + 1, 0)
 
     def advance(self, ctl) -> None:
         self.batch_n = ctl["batch_n"]
