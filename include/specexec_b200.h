@@ -64,7 +64,8 @@ enum {
   SX_EPI_SWIGLU_IL = 4,   /* W = [gate; up] interleaved in 64-row blocks (rows 128j..128j+63 =
                              gate features 64j.., rows 128j+64.. = up of the same features);
                              out bf16 [M, N/2] = silu(gate) * up   (N % 128 == 0)      */
-  SX_EPI_RS_BF16 = 5      /* internal: the reduce-scatter epilogue of sx_gemm_bf16_rs        */
+  SX_EPI_RS_BF16 = 5,     /* internal: the reduce-scatter epilogue of sx_gemm_bf16_rs        */
+  SX_EPI_QKV_ROPE = 6     /* internal: the RoPE + KV-scatter epilogue of sx_gemm_qkv_rope    */
 };
 /* 0 = auto (default: CTA-pair cta_group::2 tiles for M >= 256 tokens), 1 = single-CTA only, 2 = pair when legal */
 SX_API int sx_gemm_set_pair_mode(int mode);
@@ -82,6 +83,15 @@ SX_API int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* out,
  * every rank's y [M, N] (the all-gather half). Deterministic; identical on all ranks. */
 SX_API int sx_gemm_bf16_rs(const void* W, const void* X, void* const* peer_inbox, int rank, int world, float* ws,
                            long long ws_floats, int M, int N, int K, int splits_req, cudaStream_t stream);
+/* QKV projection with RoPE and the KV-cache scatter fused into the epilogue
+ * (replaces sx_gemm_bf16 + sx_rope_kv): W [(H + 2 KVH) * 128, K] (q heads, k
+ * heads, v heads); each 128-row tile is one head, rotated (rotate-half, position
+ * pos_base + pos[t], tables [max_pos, 64]) from the fp32 accumulator and stored
+ * to q [M, H, 128] or to cache slot slot_base + slot[t] of K / V [KVH][slots][128]. */
+SX_API int sx_gemm_qkv_rope(const void* W, const void* X, float* ws, long long ws_floats, int M, int H, int KVH, int K,
+                            const int* pos, int pos_base, const int* slot, int slot_base, const float* cos_t,
+                            const float* sin_t, void* q, void* kcache, void* vcache, long long slots, int splits_req,
+                            cudaStream_t stream);
 SX_API int sx_tp_reduce_bcast(const void* inbox, int rank, int world, int M, int N, void* const* peer_y, int y_bf16,
                               cudaStream_t stream);
 

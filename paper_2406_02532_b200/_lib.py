@@ -72,6 +72,11 @@ SIGNATURES: dict[str, tuple] = {
     "sx_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
     "sx_add_rmsnorm": (_c_int, [_vp, _vp, _c_int, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
     "sx_gemm_bf16_rs": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _vp, _c_ll, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "sx_gemm_qkv_rope": (
+        _c_int,
+        [_vp, _vp, _vp, _c_ll, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp,
+         _c_ll, _c_int, _vp],
+    ),
     "sx_tp_reduce_bcast": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp]),
     "sx_rope_kv": (
         _c_int,
@@ -88,7 +93,7 @@ SIGNATURES: dict[str, tuple] = {
 ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1
 SCORE_RAW, SCORE_ARGMAX, SCORE_WARP = 0, 1, 2
 
-EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL, EPI_RS_BF16 = 0, 1, 2, 3, 4, 5
+EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL, EPI_RS_BF16, EPI_QKV_ROPE = 0, 1, 2, 3, 4, 5, 6
 
 _lib = None
 

@@ -58,6 +58,16 @@ struct GemmArgs {
   // half of the all-reduce, written by the epilogue over NVLink as tiles finish
   int rs_rank, rs_world, rs_slice;
   int vec_store;  // 1: output rows 16-B aligned -> smem-transposed epilogue with 16-B stores
+  // SX_EPI_QKV_ROPE: rows = [q heads | k heads | v heads] x 128; each 128-row tile is one head
+  const int* rope_pos;
+  const int* rope_slot;
+  int rope_pos_base, rope_slot_base, rope_H, rope_KVH;
+  const float* rope_cos;
+  const float* rope_sin;
+  __nv_bfloat16* rope_q;
+  __nv_bfloat16* rope_kc;
+  __nv_bfloat16* rope_vc;
+  long long rope_slots;
   int* flags;      // stream-K partial-ready flags [ctas * CG]
   float* part;     // stream-K partials [ctas * CG][dual?2:1][BN][128]
   int debug_no_tma;  // SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
@@ -151,13 +161,57 @@ SX_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 
 SX_DEV void epilogue_store(const GemmArgs& g, const float (&v)[16], const float (&v2)[16], int f, int fl, bool fok,
                            int t0, float* xs) {
   const int fbase = f - fl;  // first feature (weight row) of this CTA's 128-row tile
-  if (g.vec_store &&
-      (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_F32 || g.epi == SX_EPI_SWIGLU_IL || g.epi == SX_EPI_RS_BF16)) {
+  if (g.vec_store && (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_F32 || g.epi == SX_EPI_SWIGLU_IL ||
+                      g.epi == SX_EPI_RS_BF16 || g.epi == SX_EPI_QKV_ROPE)) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) xs[j * 128 + fl] = v[j];
     epi_bar();
     const int tid = fl;  // 0..127
-    if (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_RS_BF16) {
+    if (g.epi == SX_EPI_QKV_ROPE) {
+      // this tile = head hh for 16 tokens; thread: token j, dims d0..d0+7 and their +64 partners
+      const int hh = fbase >> 7;
+      const int j = tid >> 3, d0 = (tid & 7) * 8;
+      const int t = t0 + j;
+      if (t < g.M && fbase < g.Nf) {
+        const float* x = xs + j * 128;
+        const long long sl = g.rope_slot_base + (g.rope_slot ? g.rope_slot[t] : t);
+        __nv_bfloat16* dst;
+        if (hh < g.rope_H)
+          dst = g.rope_q + ((long long)t * g.rope_H + hh) * 128;
+        else if (hh < g.rope_H + g.rope_KVH)
+          dst = g.rope_kc + ((long long)(hh - g.rope_H) * g.rope_slots + sl) * 128;
+        else
+          dst = g.rope_vc + ((long long)(hh - g.rope_H - g.rope_KVH) * g.rope_slots + sl) * 128;
+        float lo[8], hi[8];
+        if (hh < g.rope_H + g.rope_KVH) {  // rotate-half RoPE (HF convention) at position p
+          const long long p = g.rope_pos_base + (g.rope_pos ? g.rope_pos[t] : t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float c = g.rope_cos[p * 64 + d0 + i], sn = g.rope_sin[p * 64 + d0 + i];
+            const float x0 = x[d0 + i], x1 = x[d0 + 64 + i];
+            lo[i] = x0 * c - x1 * sn;
+            hi[i] = x1 * c + x0 * sn;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            lo[i] = x[d0 + i];
+            hi[i] = x[d0 + 64 + i];
+          }
+        }
+        uint4 a, b;
+        a.x = pack_bf16x2(lo[0], lo[1]);
+        a.y = pack_bf16x2(lo[2], lo[3]);
+        a.z = pack_bf16x2(lo[4], lo[5]);
+        a.w = pack_bf16x2(lo[6], lo[7]);
+        b.x = pack_bf16x2(hi[0], hi[1]);
+        b.y = pack_bf16x2(hi[2], hi[3]);
+        b.z = pack_bf16x2(hi[4], hi[5]);
+        b.w = pack_bf16x2(hi[6], hi[7]);
+        *reinterpret_cast<uint4*>(dst + d0) = a;
+        *reinterpret_cast<uint4*>(dst + d0 + 64) = b;
+      }
+    } else if (g.epi == SX_EPI_BF16 || g.epi == SX_EPI_RS_BF16) {
       // 16 tokens x 16 groups of 8 features = 256 items, 2 per thread
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
@@ -829,7 +883,30 @@ extern "C" int sx_gemm_plan(int M, int Nf, int K, int dual, int splits_req, int*
 
 static int gemm_launch(const void* W, const void* W2, const void* X, void* out, float* ws, long long ws_floats, int M,
                        int Nf, int K, long long ldo, int epi, int splits_req, int rs_rank, int rs_world, int rs_slice,
-                       cudaStream_t stream);
+                       cudaStream_t stream, const GemmArgs* rope = nullptr);
+
+extern "C" int sx_gemm_qkv_rope(const void* W, const void* X, float* ws, long long ws_floats, int M, int H, int KVH,
+                                int K, const int* pos, int pos_base, const int* slot, int slot_base, const float* cos_t,
+                                const float* sin_t, void* q, void* kcache, void* vcache, long long slots,
+                                int splits_req, cudaStream_t stream) {
+  if (H <= 0 || KVH <= 0) return arg_error("sx_gemm_qkv_rope: H, KVH must be > 0");
+  if (!q || !kcache || !vcache || !cos_t || !sin_t) return arg_error("sx_gemm_qkv_rope: NULL output / table");
+  GemmArgs r{};
+  r.rope_pos = pos;
+  r.rope_slot = slot;
+  r.rope_pos_base = pos_base;
+  r.rope_slot_base = slot_base;
+  r.rope_H = H;
+  r.rope_KVH = KVH;
+  r.rope_cos = cos_t;
+  r.rope_sin = sin_t;
+  r.rope_q = reinterpret_cast<__nv_bfloat16*>(q);
+  r.rope_kc = reinterpret_cast<__nv_bfloat16*>(kcache);
+  r.rope_vc = reinterpret_cast<__nv_bfloat16*>(vcache);
+  r.rope_slots = slots;
+  const int Nf = (H + 2 * KVH) * 128;
+  return gemm_launch(W, nullptr, X, q, ws, ws_floats, M, Nf, K, Nf, SX_EPI_QKV_ROPE, splits_req, 0, 1, Nf, stream, &r);
+}
 
 extern "C" int sx_gemm_bf16_rs(const void* W, const void* X, void* const* peer_inbox, int rank, int world, float* ws,
                                long long ws_floats, int M, int Nf, int K, int splits_req, cudaStream_t stream) {
@@ -843,16 +920,18 @@ extern "C" int sx_gemm_bf16_rs(const void* W, const void* X, void* const* peer_i
 
 extern "C" int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* out, float* ws, long long ws_floats,
                             int M, int Nf, int K, long long ldo, int epi, int splits_req, cudaStream_t stream) {
-  if (epi == SX_EPI_RS_BF16) return arg_error("sx_gemm: the reduce-scatter epilogue is sx_gemm_bf16_rs");
+  if (epi == SX_EPI_RS_BF16 || epi == SX_EPI_QKV_ROPE)
+    return arg_error("sx_gemm: epilogue %d has its own entry point (sx_gemm_bf16_rs / sx_gemm_qkv_rope)", epi);
   return gemm_launch(W, W2, X, out, ws, ws_floats, M, Nf, K, ldo, epi, splits_req, 0, 1, Nf, stream);
 }
 
 static int gemm_launch(const void* W, const void* W2, const void* X, void* out, float* ws,
                        long long ws_floats, int M, int Nf, int K, long long ldo, int epi, int splits_req, int rs_rank,
-                       int rs_world, int rs_slice, cudaStream_t stream) {
+                       int rs_world, int rs_slice, cudaStream_t stream, const GemmArgs* rope) {
   const int dual = W2 != nullptr;
   if (dual != (epi == SX_EPI_SWIGLU_BF16)) return arg_error("sx_gemm: SWIGLU epilogue needs W2 and vice versa");
-  if (epi < 0 || epi > SX_EPI_RS_BF16) return arg_error("sx_gemm: bad epilogue %d", epi);
+  if (epi < 0 || epi > SX_EPI_QKV_ROPE) return arg_error("sx_gemm: bad epilogue %d", epi);
+  if ((epi == SX_EPI_QKV_ROPE) != (rope != nullptr)) return arg_error("sx_gemm: QKV+RoPE epilogue via sx_gemm_qkv_rope");
   if (epi == SX_EPI_SWIGLU_IL && (Nf % 128) != 0)
     return arg_error("sx_gemm: interleaved SwiGLU needs N %% 128 == 0 (N=%d)", Nf);
   const int ncols = epi == SX_EPI_SWIGLU_IL ? Nf / 2 : Nf;
@@ -897,6 +976,21 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.ldo = ldo;
   g.vec_store = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
   if (epi == SX_EPI_RS_BF16) g.vec_store = (rs_slice % 128 == 0) ? 1 : 0;  // inbox rows are 16-B aligned slices
+  if (rope) {
+    g.rope_pos = rope->rope_pos;
+    g.rope_slot = rope->rope_slot;
+    g.rope_pos_base = rope->rope_pos_base;
+    g.rope_slot_base = rope->rope_slot_base;
+    g.rope_H = rope->rope_H;
+    g.rope_KVH = rope->rope_KVH;
+    g.rope_cos = rope->rope_cos;
+    g.rope_sin = rope->rope_sin;
+    g.rope_q = rope->rope_q;
+    g.rope_kc = rope->rope_kc;
+    g.rope_vc = rope->rope_vc;
+    g.rope_slots = rope->rope_slots;
+    g.vec_store = 1;  // head rows of 128 bf16, 16-B aligned
+  }
   if (epi == SX_EPI_SWIGLU_IL && (Nf % 128)) g.vec_store = 0;
   g.rs_rank = rs_rank;
   g.rs_world = rs_world;

@@ -171,6 +171,33 @@ from ._lib import ROWS_LOGITS_F32, ROWS_PROBS_F64, SCORE_ARGMAX, SCORE_RAW, SCOR
 _scratch_cache: dict[tuple[int, str], torch.Tensor] = {}
 
 
+def gemm_qkv_rope(x: torch.Tensor, w: torch.Tensor, H: int, KVH: int, pos, pos_base: int, slot, slot_base: int,
+                  cos: torch.Tensor, sin: torch.Tensor, q: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor,
+                  slots: int, splits: int = 0) -> None:
+    """QKV projection whose epilogue applies RoPE and scatters K / V into the
+    cache (sx_gemm_qkv_rope): q [M, H, 128] and the cache rows are written
+    directly from the fp32 accumulators."""
+    _require_cuda(x, w, q, kc, vc)
+    M, Kd = x.shape
+    N = w.shape[0]
+    if N != (H + 2 * KVH) * 128:
+        raise ValueError(f"gemm_qkv_rope: weight rows {N} != (H + 2 KVH) * 128")
+    _, _, ws_need = gemm_plan(M, N, Kd, False, splits)
+    ws = _workspace(ws_need, x.device)
+    prof = PROFILER
+    if prof is not None and torch.cuda.is_current_stream_capturing():
+        prof = None
+    if prof is not None:
+        e0 = prof.event()
+        e0.record()
+    call("sx_gemm_qkv_rope", ptr(w), ptr(x), ptr(ws), ws.numel() if ws is not None else 0, M, H, KVH, Kd, ptr(pos),
+         pos_base, ptr(slot), slot_base, ptr(cos), ptr(sin), ptr(q), ptr(kc), ptr(vc), slots, splits, stream_ptr())
+    if prof is not None:
+        e1 = prof.event()
+        e1.record()
+        prof.rec.append((M, N, Kd, 0, e0, e1))
+
+
 def gemm_rs(x: torch.Tensor, w: torch.Tensor, peer_inbox: torch.Tensor, rank: int, world: int, splits: int = 0) -> None:
     """Row-parallel projection fused with the reduce-scatter half of its
     all-reduce (sx_gemm_bf16_rs): the epilogue writes each feature slice of

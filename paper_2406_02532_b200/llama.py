@@ -359,6 +359,7 @@ class LlamaModel(LanguageModel):
         self.committed: list[int] = []  # tokens whose KV is in slots [0, len)
         self.record: list[dict] | None = None  # test hook: per build, prefix -> fp32 logits row
         self.use_graphs = True  # draft rounds and one-token chains as CUDA graphs
+        self.fuse_rope = True  # RoPE + KV-cache scatter fused into the QKV GEMM epilogue
         self._one_args = torch.zeros(4, dtype=torch.int32, device=self.device)
         self._g1 = None
         self._g1_out = None
@@ -394,9 +395,13 @@ class LlamaModel(LanguageModel):
                 _lib.call("sx_rmsnorm", p(x), p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
             else:  # residual add of the previous layer's down projection, fused into this norm
                 _lib.call("sx_add_rmsnorm", p(x), p(y), ybf, p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
-            K.gemm(h, L["wqkv"], out=b.qkv[:n])
-            _lib.call("sx_rope_kv", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, H, KVH,
-                      p(self.cos), p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
+            if self.fuse_rope:  # RoPE + KV scatter in the QKV GEMM epilogue
+                K.gemm_qkv_rope(h, L["wqkv"], H, KVH, pos, pos_base, slot, slot_base, self.cos, self.sin, b.q[:n],
+                                kc, vc, self.slots)
+            else:
+                K.gemm(h, L["wqkv"], out=b.qkv[:n])
+                _lib.call("sx_rope_kv", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, H, KVH,
+                          p(self.cos), p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
             _lib.call("sx_tree_attention", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
                       anc_base, p(anc_len), A, p(b.att), n, H, KVH, st)
             if self.tp_fused:

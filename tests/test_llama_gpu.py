@@ -178,3 +178,23 @@ def test_large_tree_replay_bit_exact(cuda, V, K_, D_, B_):
     assert [(n.parent, n.token) for n in g.nodes] == [(n.parent, n.token) for n in o.nodes]
     assert [n.edge_logprob for n in g.nodes] == [n.edge_logprob for n in o.nodes]
     assert g.rounds == o.rounds
+
+
+def test_fused_qkv_rope_matches_separate_kernels(pair):
+    """sx_gemm_qkv_rope (RoPE + KV scatter in the QKV GEMM epilogue, from the fp32
+    accumulators) vs the separate GEMM (bf16 qkv) + rope_kv kernels: logits and
+    cache rows agree to bf16 rounding."""
+    _, target = pair
+    prefix = tuple(int(t) for t in np.random.default_rng(42).integers(0, 32000, size=90))
+    out = {}
+    for fused in (False, True):
+        target.fuse_rope = fused
+        target.committed.clear()
+        rows = target.prefix_rows(prefix)[0].clone()
+        out[fused] = (rows, target.kc[:, :, : len(prefix) - 1].float().clone(),
+                      target.vc[:, :, : len(prefix) - 1].float().clone())
+    target.fuse_rope = True
+    (ra, ka, va), (rb, kb, vb) = out[False], out[True]
+    assert (ra - rb).abs().max().item() < TOL
+    assert (ka - kb).abs().max().item() <= 2e-2 * max(1.0, ka.abs().max().item())
+    assert (va - vb).abs().max().item() <= 2e-2 * max(1.0, va.abs().max().item())

@@ -1,5 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_llama_gpu.py tests/test_specinfer_gpu.py tests/test_beam_gpu.py -x -q > gpurun_out/pytest_q.log 2>&1
-timeout 900 python bench.py --synthetic 4 --no-cpu-baseline > gpurun_out/bench_c2_sharp.json 2> gpurun_out/bench_c2_sharp.err
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
