@@ -11,9 +11,10 @@
 //                itself; <= max_depth + 1 entries).
 // One flash-attention main loop on tensor cores (bf16 mma.sync m16n8k16, fp32
 // online softmax, cp.async double-buffered K/V tiles, XOR-swizzled shared
-// memory) covers both parts: the dense tiles of the committed prefix, then
-// "ancestor tiles" gathered by slot -- the concatenated ancestor lists of the
-// CTA's tokens (<= D+1 keys each), each row masked to its own segment. GQA:
+// memory) covers both parts in one key space: the committed prefix [0, maxlen)
+// followed by the ancestor keys gathered by slot -- the concatenated ancestor
+// lists of the CTA's tokens (<= D+1 keys each), each row masked to its own
+// segment -- so the ancestors fill the last partial committed tile. GQA:
 // one CTA serves one KV head and 64 query rows = (64 / G) tokens x G heads.
 #include "capi_util.h"
 #include "common.cuh"
@@ -135,22 +136,22 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
   cp_async_commit();
   __syncthreads();
   const int maxlen = sm.maxlen;
-  const int ndense = (maxlen + kKeyTile - 1) / kKeyTile;
-  const int ntiles = ndense + (n_anc + kKeyTile - 1) / kKeyTile;
+  // one key space: committed slots [0, maxlen) followed by the ancestor keys
+  // [maxlen, maxlen + n_anc) -- the ancestors fill the last partial dense tile
+  const int ntiles = (maxlen + n_anc + kKeyTile - 1) / kKeyTile;
 
-  // tiles [0, ndense): committed slots; tiles [ndense, ntiles): ancestor slots
   auto load_kv = [&](int tile, int buf) {
     const uint32_t ks = smem_u32(sm.ks[buf]), vs = smem_u32(sm.vs[buf]);
     for (int i = tid; i < kKeyTile * 16; i += blockDim.x) {
       const int r = i >> 4, c = i & 15;
+      const int key = tile * kKeyTile + r;
       long long slot;
       bool ok;
-      if (tile < ndense) {
-        const int key = tile * kKeyTile + r;
-        ok = key < maxlen;
-        slot = ok ? key : 0;
+      if (key < maxlen) {
+        ok = true;
+        slot = key;
       } else {
-        const int k = (tile - ndense) * kKeyTile + r;
+        const int k = key - maxlen;
         ok = k < n_anc;
         slot = ok ? sm.aslot[k] : 0;
       }
@@ -207,19 +208,21 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
         mma_bf16(s[nt], qf[ks + 1], b2, b3);
       }
     }
-    // mask (dense: key < dense_len; ancestors: the row's own segment) + scale + online softmax
-    const bool dense = kt < ndense;
-    const int kb = dense ? kt * kKeyTile : (kt - ndense) * kKeyTile;
-    const int lo_a = dense ? 0 : sa_lo, hi_a = dense ? dl_a : sa_hi;
-    const int lo_b = dense ? 0 : sb_lo, hi_b = dense ? dl_b : sb_hi;
+    // mask: committed key < dense_len of the row, or an ancestor key in the row's own segment
+    const int kb = kt * kKeyTile;
+    const int alo_a = maxlen + sa_lo, ahi_a = maxlen + sa_hi, alo_b = maxlen + sb_lo, ahi_b = maxlen + sb_hi;
     float mx_a = -INFINITY, mx_b = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
       const int key = kb + nt * 8 + (lane & 3) * 2;
-      s[nt][0] = (key >= lo_a && key < hi_a) ? s[nt][0] * a.scale_log2 : -INFINITY;
-      s[nt][1] = (key + 1 >= lo_a && key + 1 < hi_a) ? s[nt][1] * a.scale_log2 : -INFINITY;
-      s[nt][2] = (key >= lo_b && key < hi_b) ? s[nt][2] * a.scale_log2 : -INFINITY;
-      s[nt][3] = (key + 1 >= lo_b && key + 1 < hi_b) ? s[nt][3] * a.scale_log2 : -INFINITY;
+      const bool a0 = key < dl_a || (key >= alo_a && key < ahi_a);
+      const bool a1 = key + 1 < dl_a || (key + 1 >= alo_a && key + 1 < ahi_a);
+      const bool b0 = key < dl_b || (key >= alo_b && key < ahi_b);
+      const bool b1 = key + 1 < dl_b || (key + 1 >= alo_b && key + 1 < ahi_b);
+      s[nt][0] = a0 ? s[nt][0] * a.scale_log2 : -INFINITY;
+      s[nt][1] = a1 ? s[nt][1] * a.scale_log2 : -INFINITY;
+      s[nt][2] = b0 ? s[nt][2] * a.scale_log2 : -INFINITY;
+      s[nt][3] = b1 ? s[nt][3] * a.scale_log2 : -INFINITY;
       mx_a = fmaxf(mx_a, fmaxf(s[nt][0], s[nt][1]));
       mx_b = fmaxf(mx_b, fmaxf(s[nt][2], s[nt][3]));
     }

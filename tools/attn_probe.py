@@ -1,0 +1,44 @@
+"""Tree-attention timing vs key tiles: N queries (64 heads, 8 KV heads), committed
+context of `ctx` slots, `A` ancestor slots per query (root + self for A=2)."""
+import pathlib
+import sys
+
+import torch
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+from paper_2406_02532_b200 import _lib  # noqa: E402
+
+p = _lib.ptr
+
+
+def run(N, ctx, A, H=64, KVH=8, reps=20):
+    slots = ctx + N + 8
+    q = torch.randn(N, H, 128, device="cuda").bfloat16()
+    kc = torch.randn(KVH, slots, 128, device="cuda").bfloat16()
+    vc = torch.randn_like(kc)
+    out = torch.empty(N, H, 128, device="cuda", dtype=torch.bfloat16)
+    anc = torch.zeros(N, max(A, 1), dtype=torch.int32, device="cuda")
+    if A >= 1:
+        anc[:, 0] = 0
+    if A >= 2:
+        anc[:, 1] = torch.arange(1, N + 1, dtype=torch.int32, device="cuda")
+    alen = torch.full((N,), A, dtype=torch.int32, device="cuda")
+    st = _lib.stream_ptr()
+
+    def call():
+        _lib.call("sx_tree_attention", p(q), p(kc), p(vc), slots, None, ctx, p(anc) if A else None, ctx,
+                  p(alen) if A else None, max(A, 1) if A else 0, p(out), N, H, KVH, st)
+
+    call()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        call()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps * 1e3
+
+
+for N, ctx, A in [(1025, 130, 2), (1025, 130, 0), (1025, 64, 0), (1025, 256, 0), (1025, 512, 0), (1025, 1024, 0),
+                  (2049, 130, 2), (513, 130, 2), (1025, 130, 17)]:
+    print(f"N={N:5d} ctx={ctx:5d} A={A:2d}: {run(N, ctx, A):7.1f} us", flush=True)
