@@ -37,7 +37,7 @@ WORKLOADS = {
     # B=1024: the tree is identical for every B; a wide batch makes the
     # draft rounds M=1024 tensor-core GEMMs (2 draft calls / iteration instead of 5)
     "c2": ("llama2-7b", "llama2-70b", 1024, 16, 1024, 0.0, 1.0),
-    "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 256, 0.0, 1.0),
+    "c5-l3": ("llama3-8b", "llama3-70b", 1024, 16, 1024, 0.0, 1.0),
     # C4: 70B target tensor-parallel over the N GPUs (--gpus N), K=4096
     "c4": ("llama2-7b", "llama2-70b", 4096, 16, 1024, 0.0, 1.0),
     "tiny": ("tiny-draft", "tiny", 128, 16, 8, 0.0, 1.0),
