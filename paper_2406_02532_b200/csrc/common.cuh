@@ -106,6 +106,16 @@ SX_DEV void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
 }
 // Programmatic dependent launch: wait for the preceding grid (and its memory)
 SX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// TMA load multicast to the CTAs of `mask` in the cluster (same smem offset;
+// complete_tx lands on each destination CTA's barrier at the same offset)
+SX_DEV void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask,
+                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
 SX_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -149,6 +159,14 @@ SX_DEV void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint3
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Multicast commit (cta_group::1): arrive on the barrier at the same offset in every CTA of `mask`
+SX_DEV void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.

@@ -58,6 +58,9 @@ struct GemmArgs {
   // half of the all-reduce, written by the epilogue over NVLink as tiles finish
   int rs_rank, rs_world, rs_slice;
   int vec_store;  // 1: output rows 16-B aligned -> smem-transposed epilogue with 16-B stores
+  int mc;         // single-CTA tiles: cluster of mc CTAs on consecutive weight tiles sharing one token
+                  // tile, each loading 1/mc of it with TMA multicast (1 = off)
+  uint32_t b_full_bytes;  // one 64-wide atom of the whole token tile (mc > 1)
   // SX_EPI_QKV_ROPE: rows = [q heads | k heads | v heads] x 128; each 128-row tile is one head
   const int* rope_pos;
   const int* rope_slot;
@@ -445,7 +448,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = warp_id();
   const int lane = lane_id();
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
-  const int unit = blockIdx.x / CG;
+  const int MC = CG == 1 ? g.mc : 1;
+  const uint32_t mrank = MC > 1 ? cluster_ctarank() : 0u;  // position in the multicast cluster
+  const int unit = blockIdx.x / (CG * MC);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapA);
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch_desc(&mapB);
     for (int s = 0; s < g.stages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], MC);  // multicast: a stage is free once every CTA's MMA released it
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -468,10 +473,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tmem_alloc_2sm(tmem_base_smem, g.tmem_cols);
   }
   tc_fence_before();
-  if constexpr (CG == 1)
-    __syncthreads();
+  if (CG == 2 || MC > 1)
+    cluster_sync();  // peers' barriers are initialised before any multicast / remote arrive
   else
-    cluster_sync();
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       SegIter it0(g, unit);
       int tile, kb0, kb1;
       if (it0.next(g, tile, kb0, kb1) && elect_one()) {
-        const int frow = (tile / g.tiles_t) * 128 * CG + (int)rank * 128;
+        const int frow = ((tile / g.tiles_t) * MC + (int)mrank) * 128 * CG + (int)rank * 128;
         const int n = min(kb1 - kb0, g.stages);
         for (int kb = kb0; kb < kb0 + n; ++kb)
           for (int j = 0; j < KPB; ++j) {
@@ -507,11 +512,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int issued = 0;
     SegIter it(g, unit);
     int tile, kb0, kb1;
+    const int bslice = g.BN / MC;  // token rows this CTA loads (and multicasts when MC > 1)
     while (it.next(g, tile, kb0, kb1)) {
       const int tt = tile % g.tiles_t;
-      const int tf = tile / g.tiles_t;
+      const int tf = (tile / g.tiles_t) * MC + (int)mrank;
       const int frow = tf * 128 * CG + (int)rank * 128;
-      const int trow = tt * g.BN + (int)rank * bhalf;
+      const int trow = tt * g.BN + (int)rank * bhalf + (int)mrank * bslice;
       for (int kb = kb0; kb < kb1; ++kb, ++issued) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * g.stage_bytes;
@@ -525,7 +531,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               const int kc = (kb * KPB + j) * 64;
               tma_load<CG>(sa + j * g.a_bytes, &mapA, &full_bar[stage], kc, frow, pol_w);
               if (DUAL) tma_load<CG>(sa + (KPB + j) * g.a_bytes, &mapA2, &full_bar[stage], kc, frow, pol_w);
-              tma_load<CG>(sa + a_off + j * g.b_bytes, &mapB, &full_bar[stage], kc, trow, pol_x);
+              if (CG == 1 && MC > 1)  // my slice of the shared token tile, to every CTA of the cluster
+                tma_load_2d_mc(sa + a_off + j * g.b_bytes + mrank * bslice * 128, &mapB, &full_bar[stage], kc, trow,
+                               (uint16_t)((1u << MC) - 1), pol_x);
+              else
+                tma_load<CG>(sa + a_off + j * g.b_bytes, &mapB, &full_bar[stage], kc, trow, pol_x);
             }
           }
         }
@@ -573,7 +583,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (DUAL) mma<CG>(d0 + g.BN, da + KPB * a_atom + 2 * k, db + 2 * k, idesc, acc_flag);
               }
             }
-            commit<CG>(&empty_bar[stage]);
+            if (CG == 1 && MC > 1)
+              tc_commit_mc(&empty_bar[stage], (uint16_t)((1u << MC) - 1));  // release the stage in every CTA
+            else
+              commit<CG>(&empty_bar[stage]);
           }
           __syncwarp();
           if (++stage == g.stages) {
@@ -601,7 +614,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int tile, kb0, kb1;
     while (it.next(g, tile, kb0, kb1)) {
       const int tt = tile % g.tiles_t;
-      const int tf = tile / g.tiles_t;
+      const int tf = (tile / g.tiles_t) * MC + (int)mrank;
       const int f = tf * 128 * CG + (int)rank * 128 + fl;
       const bool fok = f < g.Nf;
       int mode = 0, h0 = 0, hs = 1, hn = 0;
@@ -640,7 +653,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();
+  if (CG == 2 || MC > 1) cluster_sync();  // no CTA leaves while peers may still multicast / arrive into it
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 1)
@@ -685,7 +698,7 @@ static int pick_bn(int M, int cap) {
 }
 
 struct Plan {
-  int cg, kpb, bn, tiles_f, tiles_t, tiles, kb_total, ctas, streamk;
+  int cg, mc, kpb, bn, tiles_f, tiles_t, tiles, kb_total, ctas, streamk;
   int dp_rounds, tail_tiles, tail_splits;
   int stages;
   uint32_t a_bytes, b_bytes, stage_bytes;
@@ -822,13 +835,31 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
     if (sched_req != 3 && p.kb_total * kpb / s < 48) mode = 0;
   }
   p.streamk = mode;
+  // TMA multicast of the token tile (single-CTA, whole tiles): a cluster of mc
+  // CTAs on consecutive weight tiles loads 1/mc of the shared token tile each and
+  // multicasts it, so the token operand is not re-read from L2 per weight tile.
+  // Opt-in (mc_req 2 / 4): on the 7B draft shapes at M = 256 the lock-stepped
+  // clusters measured slower than independent CTAs (qkv 41 -> 64 us, gate/up
+  // 97 -> 114 us, tools/gemm_plan_sweep.py), so the planner does not pick it.
+  p.mc = 1;
+  {
+    const int mc_req = (req >> 16) & 7;
+    int mc = 1;
+    if (mc_req >= 2) mc = mc_req;
+    while (mc > 1 && ((p.bn / mc) % 8 != 0 || p.cg != 1 || mode != 0 || mc > p.tiles_f)) mc >>= 1;
+    if (mc > 1) {
+      p.mc = mc;
+      p.tiles = ((p.tiles_f + mc - 1) / mc) * p.tiles_t;  // cluster (group) tiles
+    }
+  }
   if (mode == 1) {
     p.ctas = P;
     if ((long long)p.tiles * p.kb_total < p.ctas) p.ctas = (int)((long long)p.tiles * p.kb_total);
   } else if (mode == 2) {
     p.ctas = p.dp_rounds > 0 ? P : p.tail_tiles * p.tail_splits;
   } else {
-    p.ctas = p.tiles < P ? p.tiles : P;
+    const int units = P / p.mc;
+    p.ctas = p.tiles < units ? p.tiles : units;
   }
   p.ws_floats = mode ? kFlagFloats + (long long)p.ctas * p.cg * (dual ? 2 : 1) * p.bn * 128 : 0;
   return p;
@@ -844,13 +875,14 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& ma2, const CUte
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(g.ctas * CG);
+  const int cl = CG * (CG == 1 ? g.mc : 1);  // cluster: CTA pair, or the multicast group
+  cfg.gridDim = dim3(g.ctas * cl);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.x = cl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol.wait in the kernel)
@@ -947,7 +979,7 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   CUtensorMap ma, ma2, mb;
   if ((st = make_tmap_bf16_kmajor(&ma, W, Nf, K, K, 128))) return st;
   if ((st = make_tmap_bf16_kmajor(&ma2, dual ? W2 : W, Nf, K, K, 128))) return st;
-  if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, p.bn / p.cg))) return st;
+  if ((st = make_tmap_bf16_kmajor(&mb, X, M, K, K, p.bn / (p.cg * p.mc)))) return st;
 
   GemmArgs g{};
   g.M = M;
@@ -994,6 +1026,7 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
     g.vec_store = 1;  // head rows of 128 bf16, 16-B aligned
   }
   if (epi == SX_EPI_SWIGLU_IL && (Nf % 128)) g.vec_store = 0;
+  g.mc = p.mc;
   g.rs_rank = rs_rank;
   g.rs_world = rs_world;
   g.rs_slice = rs_slice;

@@ -173,3 +173,27 @@ def test_gemm_strided_output_edges(cuda, epi, M, N, Kd, ldo):
     tol = 1e-3 * Kd ** 0.5 if epi == K.EPI_F32 else 2e-2 * max(1.0, ref.abs().max().item())
     assert (buf[:, :N].float() - ref).abs().max().item() < tol
     assert (buf[:, N:] == 7.0).all()
+
+
+@pytest.mark.parametrize("mc", [0, 2, 4])
+@pytest.mark.parametrize("M,N,Kd,epi", [(128, 4096, 1024, K.EPI_BF16), (256, 2944, 512, K.EPI_F32), (96, 1408, 256, K.EPI_SWIGLU_IL),
+                                        (200, 1000, 384, K.EPI_BF16)])
+def test_gemm_token_multicast_clusters(cuda, mc, M, N, Kd, epi):
+    """Single-CTA tiles in clusters of mc CTAs sharing the token tile through TMA
+    multicast (req bits 16-18; 0 = the planner's choice), incl. ragged clusters
+    (N not a multiple of mc x 128 rows)."""
+    from paper_2406_02532_b200.llama import split_gate_up
+
+    g = torch.Generator(device=cuda).manual_seed(M * 3 + N + mc)
+    x = torch.randn(M, Kd, generator=g, device=cuda).bfloat16()
+    w = (torch.randn(N, Kd, generator=g, device=cuda) * 0.05).bfloat16()
+    req = (1 | (1 << 4) | (mc << 16)) if mc else 0  # whole tiles, single-CTA, forced multicast width
+    y = K.gemm(x, w, epi=epi, splits=req)
+    torch.cuda.synchronize()
+    if epi == K.EPI_SWIGLU_IL:
+        wg, wu = split_gate_up(w)
+        ref = torch.nn.functional.silu(_ref(x, wg)) * _ref(x, wu)
+    else:
+        ref = _ref(x, w)
+    tol = 1e-3 * Kd ** 0.5 if epi == K.EPI_F32 else 2e-2 * max(1.0, ref.abs().max().item())
+    assert (y.float() - ref).abs().max().item() < tol
