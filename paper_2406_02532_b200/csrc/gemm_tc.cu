@@ -707,19 +707,23 @@ struct Plan {
 
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024 - 8192;  // align pad, barriers, epilogue tile
 
-static bool use_pair(int M, int Nf, int dual, int cg_req) {
-  if (Nf < 256) return false;
+// Returns the token-tile cap to use with CTA-pair tiles, or 0 for single-CTA tiles.
+static int pair_cap(int M, int Nf, int dual, int cg_req) {
+  const int cap = dual ? 128 : bn_cap_single();
+  if (Nf < 256) return 0;
   const int mode = cg_req ? cg_req : g_pair_mode;
-  if (mode == 1) return false;
-  if (mode == 2) return true;
-  // auto: the target pass over the tree (hundreds of tokens) is MMA-bound and
-  // the pair halves the B-operand smem traffic per SM -- when its 256-row tiles
-  // still give >= 1.5 waves over the 74 pairs. Thin draft batches stream
-  // weights and keep the single-CTA schedule (narrow token tiles, stream-K).
-  if (M < 256) return false;
-  const int bn = pick_bn(M, dual ? 128 : bn_cap_single());
-  const long long tiles = (long long)((Nf + 255) / 256) * ((M + bn - 1) / bn);
-  return tiles * 2 >= 3 * (kNumSMs / 2);
+  if (mode == 1) return 0;
+  if (mode == 2) return cap;
+  // auto: pair tiles halve the B-operand smem traffic per SM; take them when they
+  // still give >= 1.5 waves over the 74 pairs -- with the widest token tile for
+  // the tree pass (hundreds of tokens), or with 128-token tiles for a batch of
+  // 128-511 tokens (7B SwiGLU at M = 256: 97 -> 59 us vs narrow single-CTA
+  // tiles, tools/gemm_plan_sweep.py). Thinner batches stay single-CTA.
+  if (M < 128) return 0;
+  auto tiles = [&](int bn) { return (long long)((Nf + 255) / 256) * ((M + bn - 1) / bn); };
+  if (M >= 256 && tiles(pick_bn(M, cap)) * 2 >= 3 * (kNumSMs / 2)) return cap;
+  if (M < 512 && cap >= 128 && tiles(pick_bn(M, 128)) * 2 >= 3 * (kNumSMs / 2)) return 128;
+  return 0;
 }
 
 // req = sched | cg << 4 | (bn_cap / 16) << 8 (a plan request; 0 = all auto):
@@ -737,10 +741,11 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
   const int sched_req = req & 15;
   const int cg_req = (req >> 4) & 3;
   const int bn_req = ((req >> 8) & 255) * 16;
-  p.cg = use_pair(M, Nf, dual, cg_req) ? 2 : 1;
+  const int pcap = pair_cap(M, Nf, dual, cg_req);
+  p.cg = pcap ? 2 : 1;
   const int P = kNumSMs / p.cg;  // scheduling units
   const int fr = 128 * p.cg;     // weight rows per tile
-  int cap = dual ? 128 : bn_cap_single();
+  int cap = pcap ? pcap : (dual ? 128 : bn_cap_single());
   if (bn_req > 0) cap = bn_req < cap ? bn_req : cap;
   p.bn = pick_bn(M, cap);
   p.tiles_f = (Nf + fr - 1) / fr;
