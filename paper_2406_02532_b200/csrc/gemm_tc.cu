@@ -831,13 +831,18 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
     p.dp_rounds = p.tiles / P;
     p.tail_tiles = p.tiles - p.dp_rounds * P;
     int s = p.tail_tiles > 0 ? P / p.tail_tiles : 1;
+    // the owner's fixup (reading s-1 partial tiles) must stay small next to a
+    // tail item: measured a loss at 21 64-wide k-blocks per item (o-proj), a gain
+    // at 64+ -- so split only as far as items keep >= 48 k-blocks (e.g. the 70B
+    // SwiGLU: 10 tail tiles of 128 k-blocks -> 2 splits, not 7)
+    if (sched_req != 3) {
+      const int s_fix = p.kb_total * kpb / 48;
+      if (s > s_fix) s = s_fix;
+    }
     if (s > p.kb_total) s = p.kb_total;
     if (s < 1) s = 1;
     p.tail_splits = s;
     if (p.tail_tiles == 0 || s == 1) mode = 0;  // nothing to balance
-    // the owner's fixup (reading s-1 partial tiles) must stay small next to a
-    // tail item: measured a loss at 21 64-wide k-blocks per item (o-proj), a gain at 64+
-    if (sched_req != 3 && p.kb_total * kpb / s < 48) mode = 0;
   }
   p.streamk = mode;
   // TMA multicast of the token tile (single-CTA, whole tiles): a cluster of mc
