@@ -96,7 +96,7 @@ struct SegIter {
     c = unit;
     r = 0;
     tail_done = false;
-    if (mode == 1) {
+    if (mode == 1 || mode == 3) {  // (mode 3: the stream-K ranges of the tail, after the whole-tile rounds)
       pos = (g.work * c) / g.ctas;
       end = (g.work * (c + 1)) / g.ctas;
     } else {
@@ -105,6 +105,21 @@ struct SegIter {
     }
   }
   SX_DEV bool next(const GemmArgs& g, int& tile, int& kb0, int& kb1) {
+    if (mode == 3) {
+      if (r < g.dp_rounds) {  // whole tiles first
+        tile = r * g.ctas + c;
+        kb0 = 0;
+        kb1 = g.kb_total;
+        ++r;
+        return true;
+      }
+      if (pos >= end) return false;
+      tile = g.dp_rounds * g.ctas + (int)(pos / g.kb_total);
+      kb0 = (int)(pos % g.kb_total);
+      kb1 = (int)min((long long)g.kb_total, kb0 + (end - pos));
+      pos += kb1 - kb0;
+      return true;
+    }
     if (mode == 1) {
       if (pos >= end) return false;
       tile = (int)(pos / g.kb_total);
@@ -622,10 +637,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mode = 1;  // helper: publishes a partial for the tile's owner
       } else if (kb1 < g.kb_total) {
         mode = 2;  // owner: the rest of the tile is summed by other units (same rank)
-        if (g.streamk == 1) {
+        if (g.streamk == 1 || g.streamk == 3) {
+          const long long t_lin = g.streamk == 3 ? tile - (long long)g.dp_rounds * g.ctas : tile;
           h0 = (unit + 1) * CG + (int)rank;
           hs = CG;
-          hn = sk_unit_of(g, (long long)tile * g.kb_total + g.kb_total - 1) - unit;
+          hn = sk_unit_of(g, t_lin * g.kb_total + g.kb_total - 1) - unit;
         } else {
           h0 = (unit + g.tail_tiles) * CG + (int)rank;
           hs = g.tail_tiles * CG;
@@ -814,8 +830,8 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
   const int waves = (p.tiles + P - 1) / P;
   const double eff = (double)p.tiles / ((double)waves * P);
   int mode = 0;
-  if (sched_req == 2 || sched_req == 3) {
-    mode = sched_req - 1;
+  if (sched_req == 2 || sched_req == 3 || sched_req == 4) {
+    mode = sched_req == 4 ? 2 : sched_req - 1;  // 4: force the stream-K tail (resolved below)
   } else if (sched_req != 1 && eff < 0.95) {
     // several token tiles: waves + K-split tail (keeps the weight tile shared in
     // L2). One token tile: stream-K pays off only for thin token tiles (M <= 64:
@@ -842,7 +858,17 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
     if (s > p.kb_total) s = p.kb_total;
     if (s < 1) s = 1;
     p.tail_splits = s;
-    if (p.tail_tiles == 0 || s == 1) mode = 0;  // nothing to balance
+    if (p.tail_tiles == 0) {
+      mode = 0;  // nothing to balance
+    } else if (sched_req == 4) {
+      mode = p.dp_rounds > 0 ? 3 : 1;  // forced stream-K tail (no whole rounds: plain stream-K)
+    } else if (s == 1) {
+      // more tail tiles than half the units: no even split -- balance the tail
+      // with stream-K ranges instead (each unit ~tail_tiles / P of a tile), when
+      // the ranges keep >= 32 64-wide k-blocks
+      const long long per = (long long)p.tail_tiles * p.kb_total * kpb / P;
+      mode = (sched_req == 4 || per >= 32) && p.dp_rounds > 0 ? 3 : 0;
+    }
   }
   p.streamk = mode;
   // TMA multicast of the token tile (single-CTA, whole tiles): a cluster of mc
@@ -867,6 +893,8 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
     if ((long long)p.tiles * p.kb_total < p.ctas) p.ctas = (int)((long long)p.tiles * p.kb_total);
   } else if (mode == 2) {
     p.ctas = p.dp_rounds > 0 ? P : p.tail_tiles * p.tail_splits;
+  } else if (mode == 3) {
+    p.ctas = P;
   } else {
     const int units = P / p.mc;
     p.ctas = p.tiles < units ? p.tiles : units;
@@ -1001,7 +1029,8 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.kb_total = p.kb_total;
   g.tiles = p.tiles;
   g.streamk = p.streamk;
-  g.work = (long long)p.tiles * p.kb_total;
+  // stream-K work: all (tile, k-block) pairs (mode 1) or only those of the tail (mode 3)
+  g.work = (long long)(p.streamk == 3 ? p.tail_tiles : p.tiles) * p.kb_total;
   g.ctas = p.ctas;
   g.dp_rounds = p.dp_rounds;
   g.tail_tiles = p.tail_tiles;

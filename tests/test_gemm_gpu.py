@@ -83,7 +83,7 @@ def test_gemm_pair_vs_single(cuda, mode, M, N, Kd):
         _lib.call("sx_gemm_set_pair_mode", 0)  # library default: auto
 
 
-@pytest.mark.parametrize("sched", [1, 2, 3, 0])
+@pytest.mark.parametrize("sched", [1, 2, 3, 4, 0])
 @pytest.mark.parametrize("M,N,Kd,dual", [(1025, 8192, 1024, False), (1025, 4480, 512, True), (200, 3072, 2048, False),
                                           (96, 1024, 4096, True)])
 def test_gemm_schedules_agree(cuda, sched, M, N, Kd, dual):
