@@ -863,11 +863,11 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
     } else if (sched_req == 4) {
       mode = p.dp_rounds > 0 ? 3 : 1;  // forced stream-K tail (no whole rounds: plain stream-K)
     } else if (s == 1) {
-      // more tail tiles than half the units: no even split -- balance the tail
-      // with stream-K ranges instead (each unit ~tail_tiles / P of a tile), when
-      // the ranges keep >= 32 64-wide k-blocks
-      const long long per = (long long)p.tail_tiles * p.kb_total * kpb / P;
-      mode = (sched_req == 4 || per >= 32) && p.dp_rounds > 0 ? 3 : 0;
+      // more tail tiles than half the units: whole tiles. (A stream-K tail --
+      // sched 4 -- balances it but measured slower: 70B qkv 129 -> 143 us, o 105 ->
+      // 115 us, C2 149 -> 158 ms/iteration; the partial fixups cost more than the
+      // idle tail.)
+      mode = 0;
     }
   }
   p.streamk = mode;
