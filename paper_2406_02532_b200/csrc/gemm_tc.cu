@@ -10,25 +10,37 @@
 // forward per tree round (stage 1) -- the dense contractions behind the
 // reference's `LanguageModel.next_distributions` (pkg/src/speckit/models.py:47-52).
 //
-// Structure: persistent, warp-specialised, one CTA per SM.
-//   warp 0      TMA producer   (weights + tokens tiles, 128B swizzle, mbarrier ring)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+// Structure: persistent, warp-specialised, one CTA (or CTA pair) per SM.
+//   warp 0      TMA producer   (weights + token tiles, 128B swizzle, mbarrier ring;
+//                               two 64-wide k-blocks per stage, KPB = 2)
+//   warp 1      TMEM allocator + the tcgen05.mma issuer (warp-uniform loop, elect.sync)
 //   warps 2..5  epilogue       (tcgen05.ld -> registers -> fused epilogue -> global)
 // Accumulators are double-buffered in TMEM when they fit so the epilogue of one
 // tile overlaps the main loop of the next.
 //
-// Scheduling: whole output tiles round-robin over the CTAs when that fills the
-// machine evenly, otherwise STREAM-K: the (tile, k-block) iteration space is cut
-// into 148 equal contiguous ranges, one per CTA. A tile split across CTAs is
-// finished by the CTA holding its first k-block (the "owner", which reaches it
-// last); the others publish fp32 partials + a flag, and the owner adds them in
-// CTA order -- deterministic, no atomics on data. This removes the wave tail of
-// shapes like 320 tiles on 148 SMs (o / down projections at K+1 = 1025 tokens)
-// and replaces split-K for the weight-streaming draft shapes.
+// Tile shapes (template CG): CG = 2 is a CTA pair (cta_group::2, a 2-CTA
+// cluster): 256 weight rows per tile, each CTA stages half the token tile, one
+// MMA issued by the even CTA covers both -- half the token-operand traffic per
+// weight row, used for tree passes (128..~1k tokens). CG = 1 is a single CTA with
+// 16..256-token tiles for thin draft batches and the one-token root / chain
+// steps (optionally in 2/4-CTA clusters that multicast the token tile, opt-in).
+// `make_plan` picks CG, the token-tile width (a wave-cost search over widths for
+// pair shapes) and the schedule.
 //
-// Epilogues: bf16 store, fp32 store (logits), fp32 residual add, and a fused
-// SwiGLU "dual" mode where a second weight matrix (up-projection) is multiplied
-// into a second accumulator and the epilogue writes silu(gate) * up.
+// Scheduling (`SegIter`): 0 whole tiles round-robin; 1 STREAM-K, the (tile,
+// k-block) space cut into one contiguous range per CTA; 2 whole-tile waves and
+// a K-split tail; 3 whole-tile waves and a stream-K tail (explicit request
+// only). A tile split across CTAs is finished by its "owner" (the CTA holding
+// its first k-block); the others publish fp32 partials + a flag and the owner
+// adds them in a fixed order -- deterministic, no atomics on data.
+//
+// Epilogues (`epilogue_store`): bf16, fp32 (logits), fp32 residual add,
+// SwiGLU over an interleaved gate/up weight (SX_EPI_SWIGLU_IL: the up rows of
+// each 16-row group are exchanged through shared memory), the legacy dual-
+// accumulator SwiGLU (DUAL), reduce-scatter into peer inboxes over NVLink
+// (SX_EPI_RS_BF16) and QKV with RoPE applied and K / V scattered into the cache
+// (SX_EPI_QKV_ROPE). Stores go through a 16-token x 128-feature fp32 smem tile
+// so each thread writes 16-byte runs along the feature dimension.
 #include "capi_util.h"
 #include "common.cuh"
 #include "specexec_b200.h"

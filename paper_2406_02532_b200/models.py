@@ -94,6 +94,8 @@ class _WorkspaceCache:
     """Tree workspaces by (K, B, V, D), per host thread (independent generation
     runs, e.g. tensor-parallel ranks as threads, never share device state)."""
 
+    MAX_IDLE_BYTES = 1 << 30
+
     def __init__(self):
         self._tls = threading.local()
 
@@ -104,7 +106,9 @@ class _WorkspaceCache:
         key = (budget, B, V, D)
         ws = cache.get(key)
         if ws is None:
-            if len(cache) > 4:
+            # bound the device memory parked in idle workspaces (budget sweeps
+            # build one per K; at K >= 2048 each is gigabytes next to a 70B target)
+            if len(cache) > 4 or sum(w.buf.numel() for w in cache.values()) > self.MAX_IDLE_BYTES:
                 cache.clear()
             ws = K.TreeWorkspace(budget, B, V, D)
             cache[key] = ws

@@ -53,21 +53,32 @@ def main():
     V = PRESETS[a.target].vocab
     prompt = tuple(int(t) for t in np.random.default_rng(1000).integers(0, V, size=128))
     recs = []
+    out = pathlib.Path(a.out) if a.out else None
+    if out:
+        out.write_text("")
+
+    def run(method, budget, cfg):
+        if method == "sx":
+            params = sx.BuilderParams(budget, a.depth, a.batch)
+            toks, st = sx.generate_specexec(prompt, draft, target, params, cfg,
+                                            warp_scores=a.scoring == "warped")
+            return toks, st, sx.stats_record("sx", cfg, st, budget, a.depth, a.batch)
+        br = sx.branching_for_budget(budget, a.si_depth)
+        toks, st = sx.generate_specinfer(prompt, draft, target, br, cfg)
+        return toks, st, sx.stats_record("si", cfg, st, sx.schedule_size(br), len(br), br[0])
+
     for method in a.methods.split(","):
         for budget in budgets:
+            try:  # untimed warm-up: CUDA-graph capture and workspace allocation for this budget
+                run(method, budget, sx.SamplingConfig(a.t, a.top_p, seed=10_000, max_new_tokens=4))
+            except torch.OutOfMemoryError as e:
+                print(f"# {method} K={budget}: out of memory ({str(e).splitlines()[0]})", flush=True)
+                break
             for seed in range(a.seeds):
                 cfg = sx.SamplingConfig(a.t, a.top_p, seed=seed, max_new_tokens=a.tokens)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                if method == "sx":
-                    params = sx.BuilderParams(budget, a.depth, a.batch)
-                    toks, st = sx.generate_specexec(prompt, draft, target, params, cfg,
-                                                    warp_scores=a.scoring == "warped")
-                    rec = sx.stats_record("sx", cfg, st, budget, a.depth, a.batch)
-                else:
-                    br = sx.branching_for_budget(budget, a.si_depth)
-                    toks, st = sx.generate_specinfer(prompt, draft, target, br, cfg)
-                    rec = sx.stats_record("si", cfg, st, sx.schedule_size(br), len(br), br[0])
+                toks, st, rec = run(method, budget, cfg)
                 torch.cuda.synchronize()
                 el = time.perf_counter() - t0
                 rec.update({"budget": budget, "tokens_per_s": len(toks) / el, "seconds": el,
@@ -76,14 +87,17 @@ def main():
                             "scoring": a.scoring if method == "sx" else "warped"})
                 recs.append(rec)
                 print(json.dumps(rec), flush=True)
+                if out:
+                    with out.open("a") as f:
+                        f.write(json.dumps(rec) + "\n")
     print("# method budget  gen_rate  tokens/s")
     for method in a.methods.split(","):
         for budget in budgets:
             rs = [r for r in recs if r["method"] == method and r["budget"] == budget]
+            if not rs:
+                continue
             print(f"# {method:4s} {budget:6d} {np.mean([r['generation_rate'] for r in rs]):8.3f} "
                   f"{np.mean([r['tokens_per_s'] for r in rs]):9.2f}")
-    if a.out:
-        pathlib.Path(a.out).write_text("".join(json.dumps(r) + "\n" for r in recs))
 
 
 if __name__ == "__main__":
