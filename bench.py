@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--tp-comm", choices=["fused", "nccl"], default="fused",
                     help="TP reduction: GEMM epilogue reduce-scatter over peer memory (falls back to NCCL if "
                          "symmetric memory is unavailable) or NCCL all-reduce")
+    ap.add_argument("--attn", choices=["auto", "mma", "tc"], default="auto",
+                    help="tree attention kernel: by shape (default), the mma.sync loop only, tcgen05 only (A/B)")
     return ap.parse_args()
 
 
@@ -328,6 +330,7 @@ def main():
         comm = NcclComm()
     srank = 0 if tp else rank  # TP ranks share one generation stream (same prompt and seed)
     t_init = time.time()
+    _lib.call("sx_attention_set_impl", {"auto": 0, "mma": 1, "tc": 2}[args.attn])
     max_new = 100000
     ctx_cap = args.prompt_len + (args.warmup + args.steps) * (D + 1) * 3 + 64
     offload = args.workload in OFFLOAD

@@ -216,6 +216,10 @@ SX_API int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const int* 
 SX_API int sx_tree_attention(const void* q, const void* kcache, const void* vcache, long long slots,
                              const int* dense_len, int dense_const, const int* anc, int anc_base, const int* anc_len,
                              int A, void* out, int N, int H, int KVH, cudaStream_t stream);
+/* Attention kernel selection: 0 = by shape (default: the tcgen05/TMEM kernel
+ * unless the batch is a small MHA batch or a one-token step), 1 = the 64-row
+ * mma.sync flash loop only, 2 = the tcgen05 kernel only (A/B measurement). */
+SX_API int sx_attention_set_impl(int impl);
 /* ------------------------------------------------ KS: weight streaming (stage 3)
  * Async copy of `bytes` between pinned host memory and device memory on
  * `stream` (to_device = 1: H2D), after waiting on `wait_event` (may be NULL) and

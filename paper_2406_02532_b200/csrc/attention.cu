@@ -9,9 +9,12 @@
 //                for causal prefill chunks dense_len = own slot + 1), and
 //   anc[0..n)  : an explicit list of extra KV slots (root + tree ancestors +
 //                itself; <= max_depth + 1 entries).
-// One flash-attention main loop on tensor cores (bf16 mma.sync m16n8k16, fp32
+// Two kernels share that key-space scheme: the tcgen05 kernel (128 rows per
+// CTA, S and O accumulated in TMEM; below) for tree passes and prefill, and a
+// 64-row mma.sync flash loop for small MHA batches and one-token steps
+// (selection in sx_tree_attention). The mma.sync loop: bf16 m16n8k16, fp32
 // online softmax, cp.async double-buffered K/V tiles, XOR-swizzled shared
-// memory) covers both parts in one key space: the committed prefix [0, maxlen)
+// memory; one key space: the committed prefix [0, maxlen)
 // followed by the ancestor keys gathered by slot -- the concatenated ancestor
 // lists of the CTA's tokens (<= D+1 keys each), each row masked to its own
 // segment -- so the ancestors fill the last partial committed tile. GQA:
@@ -291,6 +294,294 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// tcgen05 variant: 128 query rows per CTA ((128 / G) tokens x G heads of one KV
+// head), the whole tile in one MMA per 16-wide k step, accumulators in TMEM.
+//
+//   S  (TMEM cols [0, 64))    = Q K^T            M=128 N=64  K=128 (8 MMAs)
+//   O  (TMEM cols [64, 192)) += P V              M=128 N=128 K=64  (4 MMAs)
+//
+// Thread r of the 4 warps owns query row r = TMEM lane r: it reads its S row
+// (tcgen05.ld), masks and exponentiates it, and writes its P row (bf16) into the
+// K buffer of the same tile (K is dead once S has been computed). The running
+// max is only moved when it grows by more than 2^8 (rescaling O in TMEM is a
+// ld/scale/st round trip), so P values stay <= 256. Q, K, V and P live in smem
+// in the canonical 128B-swizzled layouts: Q / K / P K-major (rows of 64 bf16),
+// V MN-major (a key's 128 dims are two 128-byte rows, LBO = 8 KB between them),
+// so V is read straight from the cache layout without a transpose. K/V tiles
+// (committed slots, then the ancestor slots gathered by id) are double-buffered
+// with cp.async; tile kt+1 is fetched while tile kt is in softmax and P V.
+constexpr int kTcRows = 128;
+constexpr int kTcThreads = 128;
+constexpr uint32_t kTcTmemCols = 256;
+constexpr float kRescaleThresh = 8.f;  // log2 units
+
+struct TcSmemHdr {
+  uint64_t bar_s, bar_o;
+  uint32_t tmem;
+  int maxlen;
+  int dlen[kTcRows];
+  int seg[kTcRows + 1];
+};
+// dynamic smem: [2 KB header][Q 32 KB][K 2 x 16 KB][V 2 x 16 KB][ancestor slots]
+constexpr int kTcQOff = 2048, kTcKOff = kTcQOff + 32768, kTcVOff = kTcKOff + 32768, kTcAncOff = kTcVOff + 32768;
+
+SX_DEV uint32_t sw128(int row, int chunk) {  // byte offset of 16-byte chunk (0..7) of a 128-byte row
+  return row * 128 + ((chunk ^ (row & 7)) << 4);
+}
+SX_DEV uint64_t desc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+SX_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+SX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 64 consecutive fp32 columns of this thread's TMEM lane, waited in the same asm block
+SX_DEV void tmem_ld64_wait(uint32_t taddr, float (&v)[64]) {
+  uint32_t (&r)[64] = reinterpret_cast<uint32_t (&)[64]>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
+      "%32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, "
+      "%48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  TcSmemHdr& hd = *reinterpret_cast<TcSmemHdr*>(base);
+  int* aslot = reinterpret_cast<int*>(base + kTcAncOff);
+  const uint32_t qs = smem_u32(base + kTcQOff), ks0 = smem_u32(base + kTcKOff), vs0 = smem_u32(base + kTcVOff);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int kvh = blockIdx.y;
+  const int t0 = blockIdx.x * a.QB;
+  const __nv_bfloat16* kbase = a.kc + (long long)kvh * a.slots * kHd;
+  const __nv_bfloat16* vbase = a.vc + (long long)kvh * a.slots * kHd;
+
+  if (tid == 0) {
+    hd.maxlen = 0;
+    mbar_init(&hd.bar_s, 1);
+    mbar_init(&hd.bar_o, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&hd.tmem, kTcTmemCols);
+  __syncthreads();
+  {
+    const int t = t0 + tid / a.G;
+    const int dl = t < a.N ? (a.dense_len ? a.dense_len[t] : a.dense_const) : 0;
+    hd.dlen[tid] = dl;
+    atomicMax(&hd.maxlen, dl);
+  }
+  if (tid < a.QB) {
+    const int t = t0 + tid;
+    hd.seg[tid + 1] = (t < a.N && a.anc_len) ? a.anc_len[t] : 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    hd.seg[0] = 0;
+    for (int i = 1; i <= a.QB; ++i) hd.seg[i] += hd.seg[i - 1];
+  }
+  __syncthreads();
+  const int n_anc = hd.seg[a.QB];
+  for (int i = tid; i < a.QB * a.A; i += kTcThreads) {
+    const int tl = i / a.A, j = i % a.A, t = t0 + tl;
+    if (t < a.N && j < hd.seg[tl + 1] - hd.seg[tl]) aslot[hd.seg[tl] + j] = a.anc_base + a.anc[(long long)t * a.A + j];
+  }
+  // Q: row r = token-major, head-minor; 16-byte chunk c of the row -> region c / 8
+  for (int i = tid; i < kTcRows * 16; i += kTcThreads) {
+    const int r = i >> 4, c = i & 15;
+    const int t = t0 + r / a.G, h = kvh * a.G + r % a.G;
+    const __nv_bfloat16* src = a.q + ((long long)(t < a.N ? t : 0) * a.H + h) * kHd + c * 8;
+    cp_async16(qs + (c >> 3) * 16384 + sw128(r, c & 7), src, t < a.N ? 16 : 0);
+  }
+  __syncthreads();  // aslot visible to the K/V loaders
+  static_assert(sizeof(TcSmemHdr) <= kTcQOff, "attention smem header overlaps Q");
+  const int maxlen = hd.maxlen;
+  const int ntiles = (maxlen + n_anc + kKeyTile - 1) / kKeyTile;
+
+  // thread: 16-byte chunk c of key rows r0, r0 + 8, ..., r0 + 56 (same swizzle phase for all 8)
+  const int lc = tid & 15, lr0 = tid >> 4;
+  const uint32_t loff = (lc >> 3) * 8192 + sw128(lr0, lc & 7);
+  auto load_kv = [&](int tile) {
+    const int buf = tile & 1;
+    const uint32_t kd = ks0 + buf * 16384 + loff, vd = vs0 + buf * 16384 + loff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int key = tile * kKeyTile + lr0 + 8 * k;
+      int slot = key;
+      bool ok = true;
+      if (key >= maxlen) {
+        const int j = key - maxlen;
+        ok = j < n_anc;
+        slot = ok ? aslot[j] : 0;
+      }
+      const long long off = (long long)slot * kHd + lc * 8;
+      cp_async16(kd + k * 1024, kbase + off, ok ? 16 : 0);
+      cp_async16(vd + k * 1024, vbase + off, ok ? 16 : 0);
+    }
+  };
+  if (ntiles > 0) load_kv(0);
+  cp_async_commit();  // group: Q + tile 0
+  if (ntiles > 1) load_kv(1);
+  cp_async_commit();  // group: tile 1 (possibly empty)
+
+  const uint32_t tmem = hd.tmem;
+  const uint32_t t_s = tmem, t_o = tmem + 64;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const int r = tid;
+  const int dl = hd.dlen[r];
+  const int slo = maxlen + hd.seg[r / a.G], shi = maxlen + hd.seg[r / a.G + 1];
+  constexpr uint32_t idesc_s = idesc_bf16_f32(kTcRows, kKeyTile);
+  constexpr uint32_t idesc_o = idesc_bf16_f32(kTcRows, kHd) | (1u << 16);  // B (V) MN-major
+  float m_used = -1e30f, l = 0.f;
+  const float scale = a.scale_log2;
+
+  for (int kt = 0; kt < ntiles; ++kt) {
+    const int buf = kt & 1;
+    const uint32_t kb = ks0 + buf * 16384, vb = vs0 + buf * 16384;
+    if (kt == 0) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {  // S = Q K^T
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint64_t da = desc_sw128(qs + (j >> 2) * 16384 + (j & 3) * 32, 16, 1024);
+        const uint64_t db = desc_sw128(kb + (j >> 2) * 8192 + (j & 3) * 32, 16, 1024);
+        tc_mma_bf16(t_s, da, db, idesc_s, j > 0);
+      }
+      tc_commit(&hd.bar_s);
+    }
+    if (kt >= 1) {  // P V of tile kt-1 done: its K (holding P) and V buffers are free
+      mbar_wait(&hd.bar_o, (kt - 1) & 1);
+      if (kt + 1 < ntiles) load_kv(kt + 1);
+      cp_async_commit();
+    }
+    mbar_wait(&hd.bar_s, kt & 1);
+    tc_fence_after();
+    float sv[64];
+    tmem_ld64_wait(t_s + lane_off, sv);
+    // mask + scale, row max with 8 independent partial maxima (short dependency chains)
+    const int kbase_i = kt * kKeyTile;
+    float pm[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
+    // branch-free mask: key < dl (committed prefix) or key in [slo, shi) (own ancestor segment)
+    const int dlr = dl - kbase_i, slr = slo - kbase_i, shr = shi - kbase_i;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const bool ok = (j < dlr) | ((j >= slr) & (j < shr));
+      sv[j] = ok ? sv[j] * scale : -INFINITY;
+      pm[j & 7] = fmaxf(pm[j & 7], sv[j]);
+    }
+    const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+    const bool move = mx > m_used + kRescaleThresh;
+    const float m_new = move ? mx : m_used;
+    const float factor = move ? exp2f(m_used - m_new) : 1.f;
+    const bool scale_o = move && l > 0.f;  // O holds only zeros while l == 0
+    l *= factor;
+    m_used = m_new;
+    if (__any_sync(0xffffffff, scale_o) && kt > 0) {  // warp-collective TMEM round trip
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t u[16];
+        tmem_ld16(t_o + lane_off + c * 16, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * (scale_o ? factor : 1.f));
+        tmem_st16(t_o + lane_off + c * 16, u);
+      }
+      tmem_st_wait();
+    }
+    // P row r -> the K buffer of this tile (K-major, 64 keys = one 128-byte row)
+    uint8_t* prow = base + kTcKOff + buf * 16384;
+    float ps[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      uint32_t w[4];
+      float s8 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float p0 = exp2f(sv[c * 8 + 2 * j] - m_used), p1 = exp2f(sv[c * 8 + 2 * j + 1] - m_used);
+        s8 += p0 + p1;
+        w[j] = pack_bf16(p0, p1);
+      }
+      ps[c] = s8;
+      *reinterpret_cast<uint4*>(prow + sw128(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    l += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {  // O += P V
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t da = desc_sw128(kb + j * 32, 16, 1024);
+        const uint64_t db = desc_sw128(vb + j * 2048, 8192, 1024);
+        tc_mma_bf16(t_o, da, db, idesc_o, kt > 0 || j > 0);
+      }
+      tc_commit(&hd.bar_o);
+    }
+  }
+  // epilogue: O / l -> bf16 row of the output
+  const int t = t0 + r / a.G;
+  __nv_bfloat16* dst = a.out + ((long long)t * a.H + kvh * a.G + r % a.G) * kHd;
+  if (ntiles > 0) {
+    mbar_wait(&hd.bar_o, (ntiles - 1) & 1);
+    tc_fence_after();
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t u[16];
+    if (ntiles > 0) {
+      tmem_ld16(t_o + lane_off + c * 16, u);
+      tmem_ld_wait();
+    }
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      w[j] = ntiles > 0 ? pack_bf16(__uint_as_float(u[2 * j]) * inv, __uint_as_float(u[2 * j + 1]) * inv) : 0u;
+    if (t < a.N) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst + c * 16);
+      d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTcTmemCols);
+}
+
+static int g_attn_impl = 0;  // 0 by shape, 1 mma.sync only, 2 tcgen05 only
+
 }  // namespace sx
 
 using namespace sx;
@@ -320,7 +611,33 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   a.G = G;
   a.QB = kAttRows / G;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)kHd);
-  if (A < 0 || (long long)(kAttRows / G) * A > kMaxAncKeys)
+  if (A < 0) return arg_error("attention: negative ancestor width %d", A);
+  // Kernel choice (tools/attn_probe.py): the tcgen05 kernel wins whenever its
+  // 128-row CTAs fill the machine or the group is wide; with MHA (G = 1) on a
+  // small batch its CTAs carry 128 tokens' ancestor lists each (2x the serial
+  // key tiles of the 64-row kernel) on < 148 CTAs, and one-token steps leave
+  // most of its 128 rows idle -- there the 64-row mma.sync loop is faster.
+  const int tc_qb = kTcRows % G ? 0 : kTcRows / G;
+  const long long tc_ctas = tc_qb ? (long long)((N + tc_qb - 1) / tc_qb) * KVH : 0;
+  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && N >= tc_qb / 2 && (tc_ctas >= 148 || G >= 4);
+  if (use_tc || g_attn_impl == 2) {
+    if (kTcRows % G) return arg_error("attention: group size %d must divide %d", G, kTcRows);
+    a.QB = kTcRows / G;
+    const long long anc_bytes = 4LL * a.QB * (A > 0 ? A : 0);
+    if (anc_bytes > 64 * 1024)
+      return arg_error("attention: %d tokens x %d ancestors exceed the per-CTA ancestor list", a.QB, A);
+    const size_t smem = 1024 + kTcAncOff + (size_t)((anc_bytes + 15) & ~15LL);
+    static size_t attr_tc = 0;
+    if (smem > attr_tc) {
+      cudaFuncSetAttribute(tree_attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_tc = smem;
+    }
+    dim3 grid((N + a.QB - 1) / a.QB, KVH);
+    tree_attention_tc_kernel<<<grid, kTcThreads, smem, stream>>>(a);
+    SX_CHECK_LAUNCH("tree_attention_tc_kernel");
+    return SX_OK;
+  }
+  if ((long long)(kAttRows / G) * A > kMaxAncKeys)
     return arg_error("attention: %d tokens x %d ancestors exceed %d ancestor keys per CTA", kAttRows / G, A, kMaxAncKeys);
   const size_t smem = sizeof(AttnSmem);
   static bool attr = false;
@@ -331,5 +648,11 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   dim3 grid((N + a.QB - 1) / a.QB, KVH);
   tree_attention_kernel<<<grid, kAttWarps * 32, smem, stream>>>(a);
   SX_CHECK_LAUNCH("tree_attention_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_attention_set_impl(int impl) {
+  if (impl < 0 || impl > 2) return arg_error("attention impl %d (0 by shape, 1 mma.sync, 2 tcgen05)", impl);
+  g_attn_impl = impl;
   return SX_OK;
 }

@@ -1,0 +1,140 @@
+"""Tree attention (`sx_tree_attention`, csrc/attention.cu) against an fp32 torch
+restatement of the flattened ancestor mask (pkg/src/speckit/tree.py:208-219):
+query t sees KV slots [0, dense_len[t]) plus its ancestor list. Each kernel
+forced (mma.sync, tcgen05) and the by-shape default, on GQA groups 1 / 4 / 8, tree passes,
+causal prefill, one-token chains, empty rows and long contexts that move the
+running max across tiles."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2406_02532_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+p = _lib.ptr
+
+
+def reference(q, kc, vc, dense, anc, alen, anc_base):
+    N, H, D = q.shape
+    KVH = kc.shape[0]
+    G = H // KVH
+    qf, kf, vf = q.float(), kc.float(), vc.float()
+    out = torch.zeros(N, H, D, device=q.device)
+    for t in range(N):
+        keys = list(range(int(dense[t]))) + [anc_base + int(x) for x in anc[t, : int(alen[t])]]
+        if not keys:
+            continue
+        idx = torch.tensor(keys, device=q.device)
+        k, v = kf[:, idx], vf[:, idx]  # [KVH, n, D]
+        s = torch.einsum("kgd,knd->kgn", qf[t].view(KVH, G, D), k) / math.sqrt(D)
+        out[t] = torch.einsum("kgn,knd->kgd", torch.softmax(s, -1), v).reshape(H, D)
+    return out
+
+
+def random_tree(rng, n, max_depth):
+    parent, depth = [-1], [0]
+    for i in range(1, n):
+        ok = [j for j in range(max(0, i - 64), i) if depth[j] < max_depth] or [0]
+        par = ok[int(rng.integers(0, len(ok)))]
+        parent.append(par)
+        depth.append(depth[par] + 1)
+    paths = []
+    for i in range(n):
+        path, x = [], i
+        while x != -1:
+            path.append(x)
+            x = parent[x]
+        paths.append(path[::-1])
+    return paths
+
+
+def run(impl, q, kc, vc, dense, dense_const, anc, alen, anc_base, A):
+    N, H, _ = q.shape
+    out = torch.empty_like(q)
+    _lib.call("sx_attention_set_impl", impl)
+    try:
+        _lib.call("sx_tree_attention", p(q), p(kc), p(vc), kc.shape[1], p(dense) if dense is not None else None,
+                  dense_const, p(anc) if anc is not None else None, anc_base, p(alen) if alen is not None else None,
+                  A, p(out), N, H, kc.shape[0], _lib.stream_ptr())
+    finally:
+        _lib.call("sx_attention_set_impl", 0)
+    torch.cuda.synchronize()
+    return out.float()
+
+
+def make(N, H, KVH, slots, seed, kscale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = torch.randn(N, H, 128, device="cuda", generator=g).bfloat16()
+    kc = (torch.randn(KVH, slots, 128, device="cuda", generator=g) * kscale).bfloat16()
+    vc = torch.randn(KVH, slots, 128, device="cuda", generator=g).bfloat16()
+    return q, kc, vc
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("H,KVH,N,ctx,D", [(64, 8, 1025, 130, 16), (32, 8, 300, 70, 16), (32, 32, 257, 200, 16),
+                                           (64, 8, 37, 0, 5)])
+def test_tree_pass(cuda, impl, H, KVH, N, ctx, D):
+    rng = np.random.default_rng(N + ctx)
+    paths = random_tree(rng, N, D)
+    A = D + 1
+    anc = np.zeros((N, A), dtype=np.int32)
+    alen = np.zeros(N, dtype=np.int32)
+    for t, path in enumerate(paths):
+        anc[t, : len(path)] = path
+        alen[t] = len(path)
+    q, kc, vc = make(N, H, KVH, ctx + N + 8, seed=N)
+    dense = torch.full((N,), ctx, dtype=torch.int32, device="cuda")
+    anc_t, alen_t = torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda()
+    got = run(impl, q, kc, vc, dense, 0, anc_t, alen_t, ctx, A)
+    exp = reference(q, kc, vc, dense.cpu(), anc, alen, ctx)
+    torch.testing.assert_close(got, exp, atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("H,KVH,N", [(64, 8, 128), (32, 32, 200), (32, 8, 1)])
+def test_causal_prefill_and_chain(cuda, impl, H, KVH, N):
+    base = 50 if N == 1 else 0  # one-token chain step at slot 50
+    q, kc, vc = make(N, H, KVH, base + N + 4, seed=7 + N)
+    dense = torch.arange(base + 1, base + N + 1, dtype=torch.int32, device="cuda")
+    got = run(impl, q, kc, vc, dense, 0, None, None, 0, 0)
+    exp = reference(q, kc, vc, dense.cpu(), np.zeros((N, 0), np.int32), np.zeros(N, np.int32), 0)
+    torch.testing.assert_close(got, exp, atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2])
+def test_empty_rows_and_dense_const(cuda, impl):
+    N, H, KVH = 20, 16, 2
+    q, kc, vc = make(N, H, KVH, 300, seed=3)
+    # dense_const for all rows, ancestor lists of varying length (some empty)
+    alen = np.array([i % 4 for i in range(N)], dtype=np.int32)
+    anc = np.zeros((N, 3), dtype=np.int32)
+    for t in range(N):
+        anc[t, : alen[t]] = [(t * 7 + j) % 40 for j in range(alen[t])]
+    got = run(impl, q, kc, vc, None, 90, torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda(), 200, 3)
+    exp = reference(q, kc, vc, [90] * N, anc, alen, 200)
+    torch.testing.assert_close(got, exp, atol=2e-2, rtol=2e-2)
+    # rows with no keys at all produce zeros
+    dense0 = torch.zeros(N, dtype=torch.int32, device="cuda")
+    z = run(impl, q, kc, vc, dense0, 0, torch.from_numpy(anc).cuda(), torch.zeros(N, dtype=torch.int32, device="cuda"),
+            200, 3)
+    assert torch.count_nonzero(z) == 0
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2])
+def test_long_context_running_max(cuda, impl):
+    """Keys grow in magnitude along the context, so the row max keeps rising
+    across key tiles (exercises the lazy O rescale of the tcgen05 kernel)."""
+    N, H, KVH, ctx = 17, 64, 8, 2000
+    q, kc, vc = make(N, H, KVH, ctx + N, seed=11)
+    ramp = torch.linspace(0.2, 3.0, ctx + N, device="cuda").view(1, -1, 1)
+    kc = (kc.float() * ramp).bfloat16()
+    q = (q.float() * 2).bfloat16()
+    dense = torch.full((N,), ctx, dtype=torch.int32, device="cuda")
+    anc = np.arange(N, dtype=np.int32).reshape(N, 1)
+    alen = np.ones(N, dtype=np.int32)
+    got = run(impl, q, kc, vc, dense, 0, torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda(), ctx, 1)
+    exp = reference(q, kc, vc, dense.cpu(), anc, alen, ctx)
+    torch.testing.assert_close(got, exp, atol=2e-2, rtol=2e-2)

@@ -39,6 +39,21 @@ def run(N, ctx, A, H=64, KVH=8, reps=20):
     return s.elapsed_time(e) / reps * 1e3
 
 
-for N, ctx, A in [(1025, 130, 2), (1025, 130, 0), (1025, 64, 0), (1025, 256, 0), (1025, 512, 0), (1025, 1024, 0),
-                  (2049, 130, 2), (513, 130, 2), (1025, 130, 17)]:
-    print(f"N={N:5d} ctx={ctx:5d} A={A:2d}: {run(N, ctx, A):7.1f} us", flush=True)
+CASES = [(64, 8, 1025, 130, 2), (64, 8, 1025, 130, 17), (64, 8, 1025, 512, 0), (64, 8, 1025, 1024, 0),
+         (64, 8, 2049, 130, 17), (64, 8, 4097, 200, 17), (32, 32, 1024, 160, 17), (32, 32, 256, 160, 17),
+         (32, 8, 1024, 160, 17), (64, 8, 1, 300, 0), (32, 32, 1, 300, 0)]
+
+
+def main():
+    for H, KVH, N, ctx, A in CASES:
+        t = []
+        for impl in (2, 1):
+            _lib.call("sx_attention_set_impl", impl)
+            t.append(run(N, ctx, A, H, KVH))
+        _lib.call("sx_attention_set_impl", 0)
+        print(f"H={H:3d} KVH={KVH:3d} N={N:5d} ctx={ctx:5d} A={A:2d}: tcgen05 {t[0]:7.1f} us   "
+              f"mma.sync {t[1]:7.1f} us", flush=True)
+
+
+if __name__ == "__main__":
+    main()
