@@ -347,6 +347,11 @@ SX_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+SX_DEV float ex2_approx(float x) {  // MUFU.EX2 without the denormal fix-ups of exp2f; ex2(-inf) = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 SX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // 64 consecutive fp32 columns of this thread's TMEM lane, waited in the same asm block
 SX_DEV void tmem_ld64_wait(uint32_t taddr, float (&v)[64]) {
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
       float s8 = 0.f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float p0 = exp2f(sv[c * 8 + 2 * j] - m_used), p1 = exp2f(sv[c * 8 + 2 * j + 1] - m_used);
+        const float p0 = ex2_approx(sv[c * 8 + 2 * j] - m_used), p1 = ex2_approx(sv[c * 8 + 2 * j + 1] - m_used);
         s8 += p0 + p1;
         w[j] = pack_bf16(p0, p1);
       }
@@ -627,11 +632,7 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
     if (anc_bytes > 64 * 1024)
       return arg_error("attention: %d tokens x %d ancestors exceed the per-CTA ancestor list", a.QB, A);
     const size_t smem = 1024 + kTcAncOff + (size_t)((anc_bytes + 15) & ~15LL);
-    static size_t attr_tc = 0;
-    if (smem > attr_tc) {
-      cudaFuncSetAttribute(tree_attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr_tc = smem;
-    }
+    if (int st = ensure_smem_attr((const void*)tree_attention_tc_kernel, (int)smem)) return st;
     dim3 grid((N + a.QB - 1) / a.QB, KVH);
     tree_attention_tc_kernel<<<grid, kTcThreads, smem, stream>>>(a);
     SX_CHECK_LAUNCH("tree_attention_tc_kernel");
@@ -640,11 +641,7 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   if ((long long)(kAttRows / G) * A > kMaxAncKeys)
     return arg_error("attention: %d tokens x %d ancestors exceed %d ancestor keys per CTA", kAttRows / G, A, kMaxAncKeys);
   const size_t smem = sizeof(AttnSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tree_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  if (int st = ensure_smem_attr((const void*)tree_attention_kernel, (int)smem)) return st;
   dim3 grid((N + a.QB - 1) / a.QB, KVH);
   tree_attention_kernel<<<grid, kAttWarps * 32, smem, stream>>>(a);
   SX_CHECK_LAUNCH("tree_attention_kernel");

@@ -86,3 +86,20 @@ int make_tmap_bf16_kmajor(CUtensorMap* out, const void* ptr, int64_t rows, int64
 }
 
 }  // namespace sx
+
+namespace sx {
+int ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> set;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "ensure_smem_attr");
+  std::lock_guard<std::mutex> lock(mu);
+  int& cur = set[{fn, dev}];
+  if (cur >= bytes) return SX_OK;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+  cur = bytes;
+  return SX_OK;
+}
+}  // namespace sx

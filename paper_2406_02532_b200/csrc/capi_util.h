@@ -26,6 +26,11 @@ int cuda_status(cudaError_t e, const char* where);
 // 2D row-major bf16 matrix [rows, cols] (cols contiguous, row pitch `ld`
 // elements) -> tensor map with a {64, box_rows} box and 128B swizzle.
 // Cached by (ptr, rows, cols, ld, box_rows).
+// Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT device
+// (the attribute is per device: one process may drive several GPUs, e.g.
+// tensor-parallel thread-ranks). Thread-safe; a no-op once set at >= bytes.
+int ensure_smem_attr(const void* fn, int bytes);
+
 int make_tmap_bf16_kmajor(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
                           int box_rows);
 

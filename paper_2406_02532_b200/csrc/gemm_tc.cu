@@ -919,11 +919,7 @@ template <int CG, bool DUAL, int KPB>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& ma2, const CUtensorMap& mb, const GemmArgs& g,
                        size_t smem, cudaStream_t stream) {
   auto kern = gemm_tc_kernel<CG, DUAL, KPB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  if (int st = ensure_smem_attr((const void*)kern, 227 * 1024)) return st;
   cudaLaunchConfig_t cfg{};
   const int cl = CG * (CG == 1 ? g.mc : 1);  // cluster: CTA pair, or the multicast group
   cfg.gridDim = dim3(g.ctas * cl);

@@ -262,7 +262,7 @@ extern "C" int sx_kv_compact(void* kcache, void* vcache, int layers, long long l
   if (n > 192) return arg_error("kv_compact: at most 192 rows per call (got %d)", n);
   const size_t smem = (size_t)2 * n * 16 * sizeof(uint4);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kv_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (int st = ensure_smem_attr((const void*)kv_compact_kernel, (int)smem)) return st;
   kv_compact_kernel<<<dim3(KVH, layers), 256, smem, stream>>>(reinterpret_cast<__nv_bfloat16*>(kcache),
                                                                reinterpret_cast<__nv_bfloat16*>(vcache), layer_stride,
                                                                slots, KVH, src, dst, n);

@@ -138,12 +138,7 @@ extern "C" int sx_sample_rows_idx(const double* w, long long ld, int V, const in
                                   int* out_tok, double* out_logq, cudaStream_t stream) {
   if (n <= 0) return SX_OK;
   if (V < 1) return arg_error("sample_rows_idx: V must be >= 1");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute((const void*)sample_rows_idx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(RowSmem));
-    attr = true;
-  }
+  if (int st = ensure_smem_attr((const void*)sample_rows_idx_kernel, (int)sizeof(RowSmem))) return st;
   sample_rows_idx_kernel<<<n, kRowThreads, sizeof(RowSmem), stream>>>(w, ld, V, row_ids, u, out_tok, out_logq);
   SX_CHECK_LAUNCH("sample_rows_idx_kernel");
   return SX_OK;
@@ -157,12 +152,7 @@ extern "C" int sx_specinfer_verify(const void* trows, int row_kind, long long ld
   if (row_kind != SX_ROWS_LOGITS_F32 && row_kind != SX_ROWS_PROBS_F64)
     return arg_error("specinfer_verify: bad row kind");
   if (temperature < 0 || !(top_p > 0 && top_p <= 1)) return arg_error("specinfer_verify: bad warp");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute((const void*)specinfer_verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(RowSmem));
-    attr = true;
-  }
+  if (int st = ensure_smem_attr((const void*)specinfer_verify_kernel, (int)sizeof(RowSmem))) return st;
   auto al = [](long long x) { return (x + 255) & ~255LL; };
   uint8_t* b = reinterpret_cast<uint8_t*>(scratch);
   SiScratch s;

@@ -769,12 +769,8 @@ extern "C" int sx_beam_step(const double* q, long long ldq, int V, int nb, const
   if ((long long)nb * beam_size > kBeamSortMax)
     return arg_error("beam_step: %d beams x beam_size %d exceed the %d-entry single-CTA sort", nb, beam_size,
                      kBeamSortMax);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(beam_row_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
-    cudaFuncSetAttribute(beam_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBeamSortMax * 20);
-    attr = true;
-  }
+  if (int st = ensure_smem_attr((const void*)beam_row_topk_kernel, (int)sizeof(RowSmem))) return st;
+  if (int st = ensure_smem_attr((const void*)beam_select_kernel, kBeamSortMax * 20)) return st;
   const long long e = (long long)nb * V;
   auto al = [](long long x) { return (x + 255) & ~255LL; };
   uint8_t* s = reinterpret_cast<uint8_t*>(scratch);
@@ -838,13 +834,9 @@ extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* r
   if (ld < V) return arg_error("tree: row stride %lld < V %d", ld, V);
   TreeLayout L = tree_layout(K, B, V, D);
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(tree_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(tree_warp_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
-    cudaFuncSetAttribute(tree_argmax_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
-    attrs = true;
-  }
+  if (int st = ensure_smem_attr((const void*)tree_update_kernel, 227 * 1024)) return st;
+  if (int st = ensure_smem_attr((const void*)tree_warp_rows_kernel, (int)sizeof(RowSmem))) return st;
+  if (int st = ensure_smem_attr((const void*)tree_argmax_score_kernel, (int)sizeof(RowSmem))) return st;
   if (score_mode == SX_SCORE_ARGMAX) {
     tree_argmax_score_kernel<<<B, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld);
     SX_CHECK_LAUNCH("tree_argmax_score_kernel");

@@ -140,9 +140,7 @@ __global__ void sample_rows_kernel(const double* w, long long ld, int V, const d
   if (threadIdx.x == 0) out[i] = tok;
 }
 
-static void set_rowsmem_attr(const void* fn) {
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
-}
+static int set_rowsmem_attr(const void* fn) { return ensure_smem_attr(fn, (int)sizeof(RowSmem)); }
 
 }  // namespace sx
 
@@ -160,11 +158,7 @@ extern "C" int sx_verify_walk(const void* rows, int row_kind, long long ld, int 
   if (V < 1 || max_steps < 1) return arg_error("verify_walk: V and max_steps must be >= 1");
   if (row_kind != SX_ROWS_LOGITS_F32 && row_kind != SX_ROWS_PROBS_F64) return arg_error("verify_walk: bad row kind");
   if (temperature < 0 || !(top_p > 0 && top_p <= 1)) return arg_error("verify_walk: bad warp");
-  static bool attr = false;
-  if (!attr) {
-    set_rowsmem_attr((const void*)verify_walk_kernel);
-    attr = true;
-  }
+  if (int st = set_rowsmem_attr((const void*)verify_walk_kernel)) return st;
   auto al = [](long long x) { return (x + 255) & ~255LL; };
   uint8_t* s = reinterpret_cast<uint8_t*>(scratch);
   WalkScratch ws;
@@ -185,11 +179,7 @@ extern "C" int sx_warp_rows(const void* rows, int row_kind, long long ld, int V,
                             cudaStream_t stream) {
   if (n <= 0) return SX_OK;
   if (temperature < 0 || !(top_p > 0 && top_p <= 1)) return arg_error("warp_rows: bad warp");
-  static bool attr = false;
-  if (!attr) {
-    set_rowsmem_attr((const void*)warp_rows_kernel);
-    attr = true;
-  }
+  if (int st = set_rowsmem_attr((const void*)warp_rows_kernel)) return st;
   // scratch: n * (2 keys + 2 idx) per element
   uint8_t* s = reinterpret_cast<uint8_t*>(scratch);
   const long long e = (long long)n * V;
@@ -229,11 +219,7 @@ extern "C" int sx_argmax_rows(const void* rows, int row_kind, long long ld, int 
 extern "C" int sx_sample_rows(const double* w, long long ld, int V, const double* u, int n, int* out,
                               cudaStream_t stream) {
   if (n <= 0) return SX_OK;
-  static bool attr = false;
-  if (!attr) {
-    set_rowsmem_attr((const void*)sample_rows_kernel);
-    attr = true;
-  }
+  if (int st = set_rowsmem_attr((const void*)sample_rows_kernel)) return st;
   sample_rows_kernel<<<n, kRowThreads, sizeof(RowSmem), stream>>>(w, ld, V, u, out);
   SX_CHECK_LAUNCH("sample_rows_kernel");
   return SX_OK;
