@@ -42,7 +42,11 @@ def main():
     ap.add_argument("--methods", default="sx,si")
     ap.add_argument("--scoring", choices=["raw", "warped"], default="raw")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--attn", choices=["auto", "mma", "tc"], default="auto")
     a = ap.parse_args()
+    from paper_2406_02532_b200 import _lib
+
+    _lib.call("sx_attention_set_impl", {"auto": 0, "mma": 1, "tc": 2}[a.attn])
     budgets = [int(b) for b in a.budgets.split(",")]
     syn = SyntheticBias(seed=99, rank=64, scale=a.synthetic) if a.synthetic > 0 else None
     K = max(budgets)
