@@ -303,9 +303,11 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
 //   S  (TMEM cols [0, 64))    = Q K^T            M=128 N=64  K=128 (8 MMAs)
 //   O  (TMEM cols [64, 192)) += P V              M=128 N=128 K=64  (4 MMAs)
 //
-// Thread r of the 4 warps owns query row r = TMEM lane r: it reads its S row
-// (tcgen05.ld), masks and exponentiates it, and writes its P row (bf16) into the
-// K buffer of the same tile (K is dead once S has been computed). When the row
+// Two threads own query row r = TMEM lane r (warps w and w + 4 share a lane
+// quadrant), one per half of the 64 key columns / 128 output dims: each reads
+// its half of the S row (tcgen05.ld), masks and exponentiates it (the row max
+// is exchanged through shared memory), and writes its half of the P row (bf16)
+// into the K buffer of the same tile (K is dead once S has been computed). When the row
 // max grows, O is rescaled in TMEM (a warp-collective ld/scale/st round trip,
 // skipped by warps whose rows kept their max). Q, K, V and P live in smem
 // in the canonical 128B-swizzled layouts: Q / K / P K-major (rows of 64 bf16),
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const At
 // (committed slots, then the ancestor slots gathered by id) are double-buffered
 // with cp.async; tile kt+1 is fetched while tile kt is in softmax and P V.
 constexpr int kTcRows = 128;
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;  // 2 threads per query row (column halves)
 constexpr uint32_t kTcTmemCols = 256;
 // Move the running max (and rescale O in TMEM) whenever it grows. A lazy
 // threshold of 8 (FA4-style, P <= 256) was measured: no speed-up on the
@@ -328,9 +330,10 @@ struct TcSmemHdr {
   int maxlen;
   int dlen[kTcRows];
   int seg[kTcRows + 1];
+  float red[2][kTcRows];  // per-half row max / final row sum exchange
 };
-// dynamic smem: [2 KB header][Q 32 KB][K 2 x 16 KB][V 2 x 16 KB][ancestor slots]
-constexpr int kTcQOff = 2048, kTcKOff = kTcQOff + 32768, kTcVOff = kTcKOff + 32768, kTcAncOff = kTcVOff + 32768;
+// dynamic smem: [3 KB header][Q 32 KB][K 2 x 16 KB][V 2 x 16 KB][ancestor slots]
+constexpr int kTcQOff = 3072, kTcKOff = kTcQOff + 32768, kTcVOff = kTcKOff + 32768, kTcAncOff = kTcVOff + 32768;
 
 SX_DEV uint32_t sw128(int row, int chunk) {  // byte offset of 16-byte chunk (0..7) of a 128-byte row
   return row * 128 + ((chunk ^ (row & 7)) << 4);
@@ -358,6 +361,21 @@ SX_DEV float ex2_approx(float x) {  // MUFU.EX2 without the denormal fix-ups of 
   return y;
 }
 SX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 32 consecutive fp32 columns of this thread's TMEM lane, waited in the same asm block
+SX_DEV void tmem_ld32_wait(uint32_t taddr, float (&v)[32]) {
+  uint32_t (&r)[32] = reinterpret_cast<uint32_t (&)[32]>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
 // 64 consecutive fp32 columns of this thread's TMEM lane, waited in the same asm block
 SX_DEV void tmem_ld64_wait(uint32_t taddr, float (&v)[64]) {
   uint32_t (&r)[64] = reinterpret_cast<uint32_t (&)[64]>(v);
@@ -380,8 +398,8 @@ SX_DEV void tmem_ld64_wait(uint32_t taddr, float (&v)[64]) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const AttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+__global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   TcSmemHdr& hd = *reinterpret_cast<TcSmemHdr*>(base);
   int* aslot = reinterpret_cast<int*>(base + kTcAncOff);
@@ -400,8 +418,17 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(&hd.tmem, kTcTmemCols);
+  // Q first (its own cp.async group): the load overlaps the per-token metadata below.
+  // Row r = token-major, head-minor; 16-byte chunk c of the row -> region c / 8.
+  for (int i = tid; i < kTcRows * 16; i += kTcThreads) {
+    const int r = i >> 4, c = i & 15;
+    const int t = t0 + r / a.G, h = kvh * a.G + r % a.G;
+    const __nv_bfloat16* src = a.q + ((long long)(t < a.N ? t : 0) * a.H + h) * kHd + c * 8;
+    cp_async16(qs + (c >> 3) * 16384 + sw128(r, c & 7), src, t < a.N ? 16 : 0);
+  }
+  cp_async_commit();
   __syncthreads();
-  {
+  if (tid < kTcRows) {
     const int t = t0 + tid / a.G;
     const int dl = t < a.N ? (a.dense_len ? a.dense_len[t] : a.dense_const) : 0;
     hd.dlen[tid] = dl;
@@ -422,27 +449,20 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
     const int tl = i / a.A, j = i % a.A, t = t0 + tl;
     if (t < a.N && j < hd.seg[tl + 1] - hd.seg[tl]) aslot[hd.seg[tl] + j] = a.anc_base + a.anc[(long long)t * a.A + j];
   }
-  // Q: row r = token-major, head-minor; 16-byte chunk c of the row -> region c / 8
-  for (int i = tid; i < kTcRows * 16; i += kTcThreads) {
-    const int r = i >> 4, c = i & 15;
-    const int t = t0 + r / a.G, h = kvh * a.G + r % a.G;
-    const __nv_bfloat16* src = a.q + ((long long)(t < a.N ? t : 0) * a.H + h) * kHd + c * 8;
-    cp_async16(qs + (c >> 3) * 16384 + sw128(r, c & 7), src, t < a.N ? 16 : 0);
-  }
   __syncthreads();  // aslot visible to the K/V loaders
   static_assert(sizeof(TcSmemHdr) <= kTcQOff, "attention smem header overlaps Q");
   const int maxlen = hd.maxlen;
   const int ntiles = (maxlen + n_anc + kKeyTile - 1) / kKeyTile;
 
-  // thread: 16-byte chunk c of key rows r0, r0 + 8, ..., r0 + 56 (same swizzle phase for all 8)
+  // thread: 16-byte chunk c of key rows r0, r0 + 16, r0 + 32, r0 + 48 (same swizzle phase)
   const int lc = tid & 15, lr0 = tid >> 4;
   const uint32_t loff = (lc >> 3) * 8192 + sw128(lr0, lc & 7);
   auto load_kv = [&](int tile) {
     const int buf = tile & 1;
     const uint32_t kd = ks0 + buf * 16384 + loff, vd = vs0 + buf * 16384 + loff;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int key = tile * kKeyTile + lr0 + 8 * k;
+    for (int k = 0; k < kKeyTile * 16 / kTcThreads; ++k) {
+      const int key = tile * kKeyTile + lr0 + (kTcThreads / 16) * k;
       int slot = key;
       bool ok = true;
       if (key >= maxlen) {
@@ -451,19 +471,19 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
         slot = ok ? aslot[j] : 0;
       }
       const long long off = (long long)slot * kHd + lc * 8;
-      cp_async16(kd + k * 1024, kbase + off, ok ? 16 : 0);
-      cp_async16(vd + k * 1024, vbase + off, ok ? 16 : 0);
+      cp_async16(kd + k * (kTcThreads / 16) * 128, kbase + off, ok ? 16 : 0);
+      cp_async16(vd + k * (kTcThreads / 16) * 128, vbase + off, ok ? 16 : 0);
     }
   };
   if (ntiles > 0) load_kv(0);
-  cp_async_commit();  // group: Q + tile 0
+  cp_async_commit();  // group: tile 0
   if (ntiles > 1) load_kv(1);
   cp_async_commit();  // group: tile 1 (possibly empty)
 
   const uint32_t tmem = hd.tmem;
   const uint32_t t_s = tmem, t_o = tmem + 64;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  const int r = tid;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;  // TMEM lane quadrant = warp % 4
+  const int r = tid & (kTcRows - 1), half = tid >> 7;  // row, column half (keys / O dims)
   const int dl = hd.dlen[r];
   const int slo = maxlen + hd.seg[r / a.G], shi = maxlen + hd.seg[r / a.G + 1];
   constexpr uint32_t idesc_s = idesc_bf16_f32(kTcRows, kKeyTile);
@@ -495,45 +515,44 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
     }
     mbar_wait(&hd.bar_s, kt & 1);
     tc_fence_after();
-    float sv[64];
-    tmem_ld64_wait(t_s + lane_off, sv);
-    // mask + scale, row max with 8 independent partial maxima (short dependency chains)
-    const int kbase_i = kt * kKeyTile;
-    float pm[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
-    // branch-free mask: key < dl (committed prefix) or key in [slo, shi) (own ancestor segment)
+    float sv[32];
+    tmem_ld32_wait(t_s + lane_off + half * 32, sv);
+    // mask + scale (branch-free: key < dl, or key in the row's own ancestor segment), partial max
+    const int kbase_i = kt * kKeyTile + half * 32;
     const int dlr = dl - kbase_i, slr = slo - kbase_i, shr = shi - kbase_i;
+    float pm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
+    for (int j = 0; j < 32; ++j) {
       const bool ok = (j < dlr) | ((j >= slr) & (j < shr));
       sv[j] = ok ? sv[j] * scale : -INFINITY;
-      pm[j & 7] = fmaxf(pm[j & 7], sv[j]);
+      pm[j & 3] = fmaxf(pm[j & 3], sv[j]);
     }
-    const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+    hd.red[half][r] = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
+    __syncthreads();
+    const float mx = fmaxf(hd.red[0][r], hd.red[1][r]);  // identical in both halves
     const bool move = mx > m_used + a.rescale_thresh;
     const float m_new = move ? mx : m_used;
     const float factor = move ? exp2f(m_used - m_new) : 1.f;
-    const bool scale_o = move && l > 0.f;  // O holds only zeros while l == 0
     l *= factor;
     m_used = m_new;
-    if (__any_sync(0xffffffff, scale_o) && kt > 0) {  // warp-collective TMEM round trip
+    if (__any_sync(0xffffffff, move) && kt > 0) {  // warp-collective TMEM round trip over this half of O
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t u[16];
-        tmem_ld16(t_o + lane_off + c * 16, u);
+        const uint32_t ta = t_o + lane_off + half * 64 + c * 16;
+        tmem_ld16(ta, u);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * (scale_o ? factor : 1.f));
-        tmem_st16(t_o + lane_off + c * 16, u);
+        for (int j = 0; j < 16; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * factor);
+        tmem_st16(ta, u);
       }
       tmem_st_wait();
     }
-    // P row r -> the K buffer of this tile (K-major, 64 keys = one 128-byte row)
+    // P (this half's 32 keys = 16-byte chunks 4*half .. 4*half+3 of row r) -> the K buffer of this tile
     uint8_t* prow = base + kTcKOff + buf * 16384;
-    float ps[8];
+    float ps[4];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < 4; ++c) {
       uint32_t w[4];
       float s8 = 0.f;
 #pragma unroll
@@ -543,9 +562,9 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
         w[j] = pack_bf16(p0, p1);
       }
       ps[c] = s8;
-      *reinterpret_cast<uint4*>(prow + sw128(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(prow + sw128(r, half * 4 + c)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    l += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+    l += (ps[0] + ps[1]) + (ps[2] + ps[3]);  // this half's share of the row sum
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -560,19 +579,22 @@ __global__ void __launch_bounds__(kTcThreads) tree_attention_tc_kernel(const Att
       tc_commit(&hd.bar_o);
     }
   }
-  // epilogue: O / l -> bf16 row of the output
+  // epilogue: O / l -> bf16; each thread stores its half (64 dims) of row r
+  hd.red[half][r] = l;
+  __syncthreads();
+  const float lt = hd.red[0][r] + hd.red[1][r];
   const int t = t0 + r / a.G;
-  __nv_bfloat16* dst = a.out + ((long long)t * a.H + kvh * a.G + r % a.G) * kHd;
+  __nv_bfloat16* dst = a.out + ((long long)t * a.H + kvh * a.G + r % a.G) * kHd + half * 64;
   if (ntiles > 0) {
     mbar_wait(&hd.bar_o, (ntiles - 1) & 1);
     tc_fence_after();
   }
-  const float inv = l > 0.f ? 1.f / l : 0.f;
+  const float inv = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
+  for (int c = 0; c < 4; ++c) {
     uint32_t u[16];
     if (ntiles > 0) {
-      tmem_ld16(t_o + lane_off + c * 16, u);
+      tmem_ld16(t_o + lane_off + half * 64 + c * 16, u);
       tmem_ld_wait();
     }
     uint32_t w[8];
@@ -623,14 +645,13 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)kHd);
   a.rescale_thresh = kRescaleThresh;
   if (A < 0) return arg_error("attention: negative ancestor width %d", A);
-  // Kernel choice (tools/attn_probe.py): the tcgen05 kernel wins whenever its
-  // 128-row CTAs fill the machine or the group is wide; with MHA (G = 1) on a
-  // small batch its CTAs carry 128 tokens' ancestor lists each (2x the serial
-  // key tiles of the 64-row kernel) on < 148 CTAs, and one-token steps leave
-  // most of its 128 rows idle -- there the 64-row mma.sync loop is faster.
+  // Kernel choice (tools/attn_probe.py): the tcgen05 kernel wins everywhere
+  // except narrow groups (G < 4) on mid-size batches (64 < N, fewer than 148
+  // CTAs): there each of its CTAs carries 128 tokens' ancestor lists (2x the
+  // serial key tiles of the 64-row kernel) and the 64-row mma.sync loop wins.
   const int tc_qb = kTcRows % G ? 0 : kTcRows / G;
   const long long tc_ctas = tc_qb ? (long long)((N + tc_qb - 1) / tc_qb) * KVH : 0;
-  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && N >= tc_qb / 2 && (tc_ctas >= 148 || G >= 4);
+  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && (G >= 4 || N <= 64 || tc_ctas >= 148);
   if (use_tc || g_attn_impl == 2) {
     if (kTcRows % G) return arg_error("attention: group size %d must divide %d", G, kTcRows);
     a.QB = kTcRows / G;
