@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sequential", action="store_true", help="skip the sequential-decoding speed-up denominator")
     ap.add_argument("--parallel", choices=["tp", "replicas"], default="tp",
                     help="N>1: tensor-parallel target (one stream) or N independent replicas")
     ap.add_argument("--reduce", choices=["bf16", "fp32"], default="bf16", help="TP all-reduce precision")
@@ -457,6 +458,31 @@ def main():
                "h2d_bytes_per_step": int(h2d / n_it), "d2h_bytes_per_step": int((Kern.IO["d2h"] + 4 * len(toks2)) / n_it),
                "iterations": n_it, "includes": "prompt prefill, tree builds, target passes, walks, host sync per round"}
 
+    # ---------------- the speed-up denominator: sequential decoding on the same GPU(s)
+    # (generate_sequential, engine.py:134-148): one target pass
+    # per token through the one-token CUDA graph, prompt KV already cached.
+    seq = None
+    if not args.no_sequential:
+        n_seq = 2 if offload else 16
+        cfg_w = sx.SamplingConfig(temp, top_p, seed=srank + 11, max_new_tokens=2)
+        cfg_s = sx.SamplingConfig(temp, top_p, seed=srank + 11, max_new_tokens=2 + n_seq)
+        sx.generate_sequential(prompt, target, cfg_w)  # warm: prompt sync, graph capture
+        times = []
+        for c in (cfg_w, cfg_s):
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sx.generate_sequential(prompt, target, c)
+            torch.cuda.synchronize()
+            times.append(max_over_ranks(time.perf_counter() - t0, world))
+        rate = n_seq / max(1e-9, times[1] - times[0])
+        if not tp:
+            rate = sum_over_ranks(rate, world)
+        seq = {"tokens_per_s": rate, "tokens_timed": n_seq, "ms_per_token": 1e3 / (rate if tp else rate / world),
+               "speedup_of_value": value / rate,
+               "note": "target-only decoding, one token per target pass (CUDA graph), prompt KV cached; "
+                       "difference of a (2 + n)- and a 2-token run"}
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args, (dname, tname, K, D, B), accepted_per_iter, draft_calls / max(1, iters), K,
@@ -484,6 +510,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cb,
             "e2e": e2e,
+            "sequential": seq,
             "gpu_launches": launches,
             "clocks": clk,
             "init_seconds": init_s,

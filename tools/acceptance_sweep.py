@@ -62,6 +62,9 @@ def main():
         out.write_text("")
 
     def run(method, budget, cfg):
+        if method == "seq":  # the speed-up denominator: one target pass per token
+            toks, st = sx.generate_sequential(prompt, target, cfg)
+            return toks, st, sx.stats_record("seq", cfg, st, 0, 0, 0)
         if method == "sx":
             params = sx.BuilderParams(budget, a.depth, a.batch)
             toks, st = sx.generate_specexec(prompt, draft, target, params, cfg,
@@ -72,7 +75,7 @@ def main():
         return toks, st, sx.stats_record("si", cfg, st, sx.schedule_size(br), len(br), br[0])
 
     for method in a.methods.split(","):
-        for budget in budgets:
+        for budget in (budgets if method != "seq" else [0]):
             try:  # untimed warm-up: CUDA-graph capture and workspace allocation for this budget
                 run(method, budget, sx.SamplingConfig(a.t, a.top_p, seed=10_000, max_new_tokens=4))
             except torch.OutOfMemoryError as e:
@@ -96,12 +99,23 @@ def main():
                         f.write(json.dumps(rec) + "\n")
     print("# method budget  gen_rate  tokens/s")
     for method in a.methods.split(","):
-        for budget in budgets:
+        for budget in (budgets if method != "seq" else [0]):
             rs = [r for r in recs if r["method"] == method and r["budget"] == budget]
             if not rs:
                 continue
             print(f"# {method:4s} {budget:6d} {np.mean([r['generation_rate'] for r in rs]):8.3f} "
                   f"{np.mean([r['tokens_per_s'] for r in rs]):9.2f}")
+    seq = [r["tokens_per_s"] for r in recs if r["method"] == "seq"]
+    if seq:
+        base = float(np.mean(seq))
+        for method in a.methods.split(","):
+            if method == "seq":
+                continue
+            for budget in budgets:
+                rs = [r for r in recs if r["method"] == method and r["budget"] == budget]
+                if rs:
+                    print(f"# speedup {method:4s} {budget:6d} {np.mean([r['tokens_per_s'] for r in rs]) / base:6.2f}x "
+                          f"vs sequential ({base:.2f} tokens/s)")
 
 
 if __name__ == "__main__":
