@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sequential", action="store_true", help="skip the sequential-decoding speed-up denominator")
+    ap.add_argument("--offload-buffers", type=int, default=8,
+                    help="offload mode: HBM staging slots of the per-layer weight ring (2 = double buffering)")
     ap.add_argument("--parallel", choices=["tp", "replicas"], default="tp",
                     help="N>1: tensor-parallel target (one stream) or N independent replicas")
     ap.add_argument("--reduce", choices=["bf16", "fp32"], default="bf16", help="TP all-reduce precision")
@@ -336,7 +338,7 @@ def main():
     ctx_cap = args.prompt_len + (args.warmup + args.steps) * (D + 1) * 3 + 64
     offload = args.workload in OFFLOAD
     target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn,
-                        offload=offload, tp=comm, reduce_bf16=args.reduce == "bf16",
+                        offload=offload, offload_buffers=args.offload_buffers, tp=comm, reduce_bf16=args.reduce == "bf16",
                         tp_fused=None if args.tp_comm == "fused" else False)
     draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
                        synthetic=syn)
@@ -501,7 +503,8 @@ def main():
                        "parallelism": (f"tp{world} target ({'fused GEMM reduce-scatter over peer memory' if target.tp_fused else 'NCCL all-reduce'}, {args.reduce}), draft replicated"
                                        if tp else f"replicas x{world}") if world > 1 else "1 GPU",
                        "l2": f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)",
-                       "prompt_len": args.prompt_len},
+                       "prompt_len": args.prompt_len,
+                       **({"offload_buffers": target.streamer.nbuf} if offload else {})},
             "accepted_tokens_per_iter": accepted_per_iter,
             "draft_calls_per_iter": draft_calls / max(1, iters),
             "stage_ms_per_step": stages,

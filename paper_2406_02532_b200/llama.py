@@ -203,13 +203,15 @@ class LlamaWeights:
 
 
 class LayerStreamer:
-    """Stage 3: double-buffered per-layer weight streaming from pinned host RAM.
+    """Stage 3: per-layer weight streaming from pinned host RAM through a ring of
+    `nbuf` HBM staging buffers (nbuf = 2 is plain double buffering).
 
     Copies run on a dedicated stream (copy engines) through sx_stream_copy; the
     k-th copy lands in staging buffer k % nbuf after the compute stream released
     it. Layers are issued in cyclic order, so finishing layer L-1 of one pass
     immediately starts loading layers 0..nbuf-1 of the next pass -- they stream
-    in while the draft builds the next tree (the paper's prefetch)."""
+    in while the draft builds the next tree (the paper's prefetch); a ring deep
+    enough to cover the draft phase keeps the host link busy all iteration."""
 
     def __init__(self, weights: LlamaWeights, device, nbuf: int = 2):
         self.w = weights
@@ -294,8 +296,13 @@ class LlamaModel(LanguageModel):
         tp=None,
         reduce_bf16: bool = True,
         tp_fused: bool | None = None,
+        offload_buffers: int = 8,
     ):
-        """tp: a communicator (tp.NcclComm / tp.ThreadComm) -> this model is rank
+        """offload_buffers: HBM staging slots of the layer streamer (offload mode);
+        beyond the 2 a double buffer needs, the extra slots let the host link keep
+        streaming the next pass's first layers for the whole draft-tree build
+        (8 x 1.7 GB covers ~250 ms of PCIe time at 55 GB/s).
+        tp: a communicator (tp.NcclComm / tp.ThreadComm) -> this model is rank
         tp.rank's tensor-parallel shard of the target (tp.py); the partial sums
         of the o / down projections are all-reduced in bf16 (reduce_bf16) or fp32.
         tp_fused: instead of a separate all-reduce, the projection's GEMM epilogue
@@ -322,7 +329,7 @@ class LlamaModel(LanguageModel):
         self.H = cfg.heads // (self.tp.world if self.tp else 1)  # local query / KV heads
         self.KVH = cfg.kv_heads // (self.tp.world if self.tp else 1)
         self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload, shard=self.shard)
-        self.streamer = LayerStreamer(self.w, self.device) if offload else None
+        self.streamer = LayerStreamer(self.w, self.device, nbuf=max(2, min(offload_buffers, cfg.layers))) if offload else None
         self.slots = max_ctx
         self.kc = torch.zeros((cfg.layers, self.KVH, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
         self.vc = torch.zeros_like(self.kc)

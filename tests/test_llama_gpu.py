@@ -141,13 +141,17 @@ def test_specexec_equals_sequential_greedy(pair):
     assert got == seq
 
 
-def test_offloaded_target_matches_resident(pair):
+@pytest.mark.parametrize("nbuf", [2, 3, 8])
+def test_offloaded_target_matches_resident(pair, nbuf):
     """Stage 3: the same weights streamed per layer from pinned host memory give
-    bit-identical logits and tokens (same kernels, same order of operations)."""
+    bit-identical logits and tokens (same kernels, same order of operations),
+    for a plain double buffer, a ring that does not divide the layer count and
+    a ring deeper than the tiny model's layers (clamped)."""
     draft, _ = pair
     syn = SyntheticBias(seed=7, rank=64, scale=4.0)
     res = LlamaModel("tiny", seed=11, max_ctx=2048, max_tokens=512, synthetic=syn)
-    off = LlamaModel("tiny", seed=11, max_ctx=2048, max_tokens=512, synthetic=syn, offload=True)
+    off = LlamaModel("tiny", seed=11, max_ctx=2048, max_tokens=512, synthetic=syn, offload=True, offload_buffers=nbuf)
+    assert off.streamer.nbuf == min(nbuf, off.cfg.layers)
     prefix = tuple(range(300, 340))
     assert torch.equal(res.prefix_rows(prefix), off.prefix_rows(prefix))
     cfg = sx.SamplingConfig(0.6, 0.9, seed=5, max_new_tokens=30)
