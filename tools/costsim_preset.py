@@ -32,8 +32,10 @@ def main():
     target_bytes = c3["roofline"]["bytes_per_step"]
     draft_calls = c3["draft_calls_per_iter"]
     draft_step = c3["stage_ms_per_step"]["draft"] / 1e3 / max(1.0, draft_calls)
-    # LayerStreamer: its ring of staging slots loads the next pass's first layers while the draft runs
-    prefetch = float(c3["config"].get("offload_buffers", 2)) / 80.0
+    # LayerStreamer: its ring of staging slots loads the next pass's first layers while the draft
+    # runs -- as many as the ring holds or the draft phase leaves time for, whichever is less
+    ring = float(c3["config"].get("offload_buffers", 2)) / 80.0
+    prefetch = min(ring, (c3["stage_ms_per_step"]["draft"] / 1e3) * bw / c3["roofline"]["bytes_per_step"])
     preset = {"target_bytes": target_bytes, "bandwidth": bw, "compute_rate": compute_rate,
               "draft_bytes": 13.48e9, "fixed_overhead": 0.0, "prefetch_fraction": prefetch,
               "draft_step_time": draft_step}
