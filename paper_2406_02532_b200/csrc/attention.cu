@@ -651,7 +651,8 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   // serial key tiles of the 64-row kernel) and the 64-row mma.sync loop wins.
   const int tc_qb = kTcRows % G ? 0 : kTcRows / G;
   const long long tc_ctas = tc_qb ? (long long)((N + tc_qb - 1) / tc_qb) * KVH : 0;
-  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && (G >= 4 || N <= 64 || tc_ctas >= 148);
+  const bool mma_fits = (long long)(kAttRows / G) * A <= kMaxAncKeys;  // its static ancestor list
+  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && (G >= 4 || N <= 64 || tc_ctas >= 148 || !mma_fits);
   if (use_tc || g_attn_impl == 2) {
     if (kTcRows % G) return arg_error("attention: group size %d must divide %d", G, kTcRows);
     a.QB = kTcRows / G;

@@ -161,3 +161,25 @@ def test_tcgen05_error_matches_mma_sync(cuda):
         err[impl] = (got - exp).abs()
     assert float(err[2].max()) <= 1.25 * float(err[1].max()) + 1e-3, (float(err[2].max()), float(err[1].max()))
     assert float(err[2].mean()) <= 1.1 * float(err[1].mean()) + 1e-5, (float(err[2].mean()), float(err[1].mean()))
+
+
+def test_deep_ancestor_lists_mha(cuda):
+    """MHA batch with 40-entry ancestor lists (max_depth 39): past the 64-row
+    kernel's static ancestor capacity, so the by-shape choice must take the
+    tcgen05 kernel (dynamic ancestor list) and still match the reference."""
+    rng = np.random.default_rng(9)
+    N, H, KVH, ctx, D = 200, 8, 8, 64, 39
+    paths = random_tree(rng, N, D)
+    A = D + 1
+    anc = np.zeros((N, A), np.int32)
+    alen = np.zeros(N, np.int32)
+    for t, path in enumerate(paths):
+        anc[t, : len(path)] = path
+        alen[t] = len(path)
+    q, kc, vc = make(N, H, KVH, ctx + N + 8, seed=4)
+    dense = torch.full((N,), ctx, dtype=torch.int32, device="cuda")
+    got = run(0, q, kc, vc, dense, 0, torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda(), ctx, A)
+    exp = reference(q, kc, vc, dense.cpu(), anc, alen, ctx)
+    torch.testing.assert_close(got, exp, atol=2e-2, rtol=2e-2)
+    with pytest.raises(ValueError):
+        run(1, q, kc, vc, dense, 0, torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda(), ctx, A)
