@@ -1079,7 +1079,8 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.rs_slice = rs_slice;
   g.flags = p.streamk ? reinterpret_cast<int*>(ws) : nullptr;
   g.part = p.streamk ? ws + kFlagFloats : nullptr;
-  g.debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
+  static const int debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
+  g.debug_no_tma = debug_no_tma;
 
   const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + 1024 + 8192;
 #define SX_GEMM_LAUNCH(CG, DU, KP) \
