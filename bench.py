@@ -468,22 +468,23 @@ def main():
         n_seq = 2 if offload else 16
         cfg_w = sx.SamplingConfig(temp, top_p, seed=srank + 11, max_new_tokens=2)
         cfg_s = sx.SamplingConfig(temp, top_p, seed=srank + 11, max_new_tokens=2 + n_seq)
-        sx.generate_sequential(prompt, target, cfg_w)  # warm: prompt sync, graph capture
-        times = []
-        for c in (cfg_w, cfg_s):
-            barrier(world)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            sx.generate_sequential(prompt, target, c)
-            torch.cuda.synchronize()
-            times.append(max_over_ranks(time.perf_counter() - t0, world))
+        sx.generate_sequential(prompt, target, cfg_s)  # warm: prompt sync, graph capture
+        times = [float("inf"), float("inf")]
+        for _ in range(1 if offload else 3):  # min of repeats: host-side jitter off the difference
+            for i, c in enumerate((cfg_w, cfg_s)):
+                barrier(world)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                sx.generate_sequential(prompt, target, c)
+                torch.cuda.synchronize()
+                times[i] = min(times[i], max_over_ranks(time.perf_counter() - t0, world))
         rate = n_seq / max(1e-9, times[1] - times[0])
         if not tp:
             rate = sum_over_ranks(rate, world)
         seq = {"tokens_per_s": rate, "tokens_timed": n_seq, "ms_per_token": 1e3 / (rate if tp else rate / world),
                "speedup_of_value": value / rate,
                "note": "target-only decoding, one token per target pass (CUDA graph), prompt KV cached; "
-                       "difference of a (2 + n)- and a 2-token run"}
+                       "difference of a (2 + n)- and a 2-token run, min of 3 each"}
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
