@@ -216,6 +216,16 @@ SX_API int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const int* 
 SX_API int sx_tree_attention(const void* q, const void* kcache, const void* vcache, long long slots,
                              const int* dense_len, int dense_const, const int* anc, int anc_base, const int* anc_len,
                              int A, void* out, int N, int H, int KVH, cudaStream_t stream);
+/* Same, with a workspace for the key-split path of the tcgen05 kernel (small
+ * grids: one-token steps, small batches): ws_bytes >= sx_tree_attention_ws_bytes
+ * (0 = the shape needs none; NULL / too small = no split). The workspace must be
+ * zero-filled before its first use (it holds arrival counters the kernel resets);
+ * one workspace per stream. */
+SX_API long long sx_tree_attention_ws_bytes(int N, int H, int KVH);
+SX_API int sx_tree_attention_ws(const void* q, const void* kcache, const void* vcache, long long slots,
+                                const int* dense_len, int dense_const, const int* anc, int anc_base,
+                                const int* anc_len, int A, void* out, int N, int H, int KVH, void* ws,
+                                long long ws_bytes, cudaStream_t stream);
 /* Attention kernel selection: 0 = by shape (default: the tcgen05/TMEM kernel
  * unless the batch is a small MHA batch or a one-token step), 1 = the 64-row
  * mma.sync flash loop only, 2 = the tcgen05 kernel only (A/B measurement). */

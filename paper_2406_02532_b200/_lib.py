@@ -86,6 +86,11 @@ SIGNATURES: dict[str, tuple] = {
         _c_int,
         [_vp, _vp, _vp, _c_ll, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp],
     ),
+    "sx_tree_attention_ws": (
+        _c_int,
+        [_vp, _vp, _vp, _c_ll, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp],
+    ),
+    "sx_tree_attention_ws_bytes": (_c_ll, [_c_int, _c_int, _c_int]),
     "sx_attention_set_impl": (_c_int, [_c_int]),
     "sx_stream_copy": (_c_int, [_vp, _vp, _c_ll, _c_int, _vp, _vp, _vp]),
     "sx_kv_compact": (_c_int, [_vp, _vp, _c_int, _c_ll, _c_ll, _c_int, _vp, _vp, _c_int, _vp]),

@@ -45,6 +45,9 @@ struct AttnArgs {
   int N, H, KVH, G, QB;
   float scale_log2;
   float rescale_thresh;  // tcgen05 kernel: move the running max only when it grows by more (log2 units)
+  int splits;            // tcgen05 kernel: key splits (gridDim.z); > 1 writes partials to `part`
+  float* part;           // [q tiles][KVH][splits][128 rows][kPartStride] fp32 (O, m, l)
+  int* counters;         // [q tiles][KVH] split arrival counts (zero between launches)
 };
 
 SX_DEV uint32_t swz(int row, int col) {  // byte offset inside a [rows][128] bf16 tile
@@ -323,6 +326,8 @@ constexpr uint32_t kTcTmemCols = 256;
 // SpecExec shapes (<= 8 % on 1k-key contexts) but 1.6-2x the max abs error of
 // the exact-max path vs an fp32 reference (tools/attn_err.py), so exact it is.
 constexpr float kRescaleThresh = 0.f;  // log2 units
+constexpr int kPartStride = kHd + 4;   // per-row partial: O[128], m, l (+2 pad: 16-byte rows)
+constexpr int kMaxSplits = 8;
 
 struct TcSmemHdr {
   uint64_t bar_s, bar_o;
@@ -331,6 +336,7 @@ struct TcSmemHdr {
   int dlen[kTcRows];
   int seg[kTcRows + 1];
   float red[2][kTcRows];  // per-half row max / final row sum exchange
+  int last;               // key split: this CTA arrived last and merges
 };
 // dynamic smem: [3 KB header][Q 32 KB][K 2 x 16 KB][V 2 x 16 KB][ancestor slots]
 constexpr int kTcQOff = 3072, kTcKOff = kTcQOff + 32768, kTcVOff = kTcKOff + 32768, kTcAncOff = kTcVOff + 32768;
@@ -398,6 +404,68 @@ SX_DEV void tmem_ld64_wait(uint32_t taddr, float (&v)[64]) {
       : "memory");
 }
 
+
+// Key-split bookkeeping (tcgen05 kernel, gridDim.z > 1). Every CTA of a
+// (q tile, KV head) counts its arrival; the last one merges the partials of the
+// working splits and resets the counter for the next launch (no second kernel).
+SX_DEV bool split_arrive(const AttnArgs& a, TcSmemHdr& hd, int kvh, int zsplit) {
+  int* cnt = a.counters + (long long)blockIdx.x * gridDim.y + kvh;
+  __threadfence();  // this CTA's partial rows visible device-wide before the count
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(cnt, 1);
+    hd.last = old == zsplit - 1;
+    if (hd.last) *cnt = 0;
+  }
+  __syncthreads();
+  if (hd.last) __threadfence();
+  return hd.last;
+}
+
+// O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s, M = max over splits that saw
+// a key of the row; two threads per row, one per 64-dim half.
+SX_DEV void merge_splits(const AttnArgs& a, TcSmemHdr& hd, int kvh, int zsplit, int nsplit) {
+  const int tid = threadIdx.x, r = tid & (kTcRows - 1), half = tid >> 7;
+  const int t = blockIdx.x * a.QB + r / a.G;
+  if (t >= a.N) return;
+  const float* base = a.part + (((long long)blockIdx.x * gridDim.y + kvh) * zsplit * kTcRows + r) * kPartStride;
+  const long long sstride = (long long)kTcRows * kPartStride;
+  float M = -1e30f;
+  for (int s = 0; s < nsplit; ++s) {
+    const volatile float* ps = base + s * sstride;
+    if (ps[kHd + 1] > 0.f) M = fmaxf(M, ps[kHd]);
+  }
+  float acc[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+  float L = 0.f;
+  for (int s = 0; s < nsplit; ++s) {
+    const float* ps = base + s * sstride;
+    const float l_s = __ldcg(ps + kHd + 1);
+    if (!(l_s > 0.f)) continue;  // no key of this row in the split
+    const float w = exp2f(__ldcg(ps + kHd) - M);
+    L += w * l_s;
+    const float4* o4 = reinterpret_cast<const float4*>(ps + half * 64);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float4 v = __ldcg(o4 + j);
+      acc[4 * j] += w * v.x;
+      acc[4 * j + 1] += w * v.y;
+      acc[4 * j + 2] += w * v.z;
+      acc[4 * j + 3] += w * v.w;
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* dst = a.out + ((long long)t * a.H + kvh * a.G + r % a.G) * kHd + half * 64;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t w4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w4[j] = pack_bf16(acc[c * 8 + 2 * j] * inv, acc[c * 8 + 2 * j + 1] * inv);
+    reinterpret_cast<uint4*>(dst)[c] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
 __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -417,7 +485,6 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
     mbar_init(&hd.bar_o, 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(&hd.tmem, kTcTmemCols);
   // Q first (its own cp.async group): the load overlaps the per-token metadata below.
   // Row r = token-major, head-minor; 16-byte chunk c of the row -> region c / 8.
   for (int i = tid; i < kTcRows * 16; i += kTcThreads) {
@@ -452,13 +519,29 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   __syncthreads();  // aslot visible to the K/V loaders
   static_assert(sizeof(TcSmemHdr) <= kTcQOff, "attention smem header overlaps Q");
   const int maxlen = hd.maxlen;
-  const int ntiles = (maxlen + n_anc + kKeyTile - 1) / kKeyTile;
+  const int ntiles_all = (maxlen + n_anc + kKeyTile - 1) / kKeyTile;
+  // key split (gridDim.z > 1): the first `nsplit` of the launched splits take
+  // >= 4 key tiles each (fewer splits for short contexts -- a split costs a
+  // CTA prologue and a partial round trip); this CTA takes tiles [kt0, kt0 + ntiles)
+  const int zsplit = gridDim.z, split = blockIdx.z;
+  const int nsplit = zsplit > 1 ? max(1, min(zsplit, ntiles_all / 4)) : 1;
+  if (split >= nsplit) {  // idle split: no TMEM, no partial -- only the arrival count
+    cp_async_wait<0>();
+    if (split_arrive(a, hd, kvh, zsplit) && nsplit > 1) merge_splits(a, hd, kvh, zsplit, nsplit);
+    return;
+  }
+  const int kt0 = (int)(((long long)ntiles_all * split) / nsplit);
+  const int ntiles = (int)(((long long)ntiles_all * (split + 1)) / nsplit) - kt0;
+  if (warp == 0) tmem_alloc(&hd.tmem, kTcTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   // thread: 16-byte chunk c of key rows r0, r0 + 16, r0 + 32, r0 + 48 (same swizzle phase)
   const int lc = tid & 15, lr0 = tid >> 4;
   const uint32_t loff = (lc >> 3) * 8192 + sw128(lr0, lc & 7);
-  auto load_kv = [&](int tile) {
-    const int buf = tile & 1;
+  auto load_kv = [&](int tile, int local) {
+    const int buf = local & 1;
     const uint32_t kd = ks0 + buf * 16384 + loff, vd = vs0 + buf * 16384 + loff;
 #pragma unroll
     for (int k = 0; k < kKeyTile * 16 / kTcThreads; ++k) {
@@ -475,9 +558,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
       cp_async16(vd + k * (kTcThreads / 16) * 128, vbase + off, ok ? 16 : 0);
     }
   };
-  if (ntiles > 0) load_kv(0);
+  if (ntiles > 0) load_kv(kt0, 0);
   cp_async_commit();  // group: tile 0
-  if (ntiles > 1) load_kv(1);
+  if (ntiles > 1) load_kv(kt0 + 1, 1);
   cp_async_commit();  // group: tile 1 (possibly empty)
 
   const uint32_t tmem = hd.tmem;
@@ -491,10 +574,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   float m_used = -1e30f, l = 0.f;
   const float scale = a.scale_log2;
 
-  for (int kt = 0; kt < ntiles; ++kt) {
-    const int buf = kt & 1;
+  for (int i = 0; i < ntiles; ++i) {
+    const int kt = kt0 + i, buf = i & 1;
     const uint32_t kb = ks0 + buf * 16384, vb = vs0 + buf * 16384;
-    if (kt == 0) cp_async_wait<1>();
+    if (i == 0) cp_async_wait<1>();
     else cp_async_wait<0>();
     fence_proxy_async();
     __syncthreads();
@@ -508,12 +591,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
       }
       tc_commit(&hd.bar_s);
     }
-    if (kt >= 1) {  // P V of tile kt-1 done: its K (holding P) and V buffers are free
-      mbar_wait(&hd.bar_o, (kt - 1) & 1);
-      if (kt + 1 < ntiles) load_kv(kt + 1);
+    if (i >= 1) {  // P V of the previous tile done: its K (holding P) and V buffers are free
+      mbar_wait(&hd.bar_o, (i - 1) & 1);
+      if (i + 1 < ntiles) load_kv(kt + 1, i + 1);
       cp_async_commit();
     }
-    mbar_wait(&hd.bar_s, kt & 1);
+    mbar_wait(&hd.bar_s, i & 1);
     tc_fence_after();
     float sv[32];
     tmem_ld32_wait(t_s + lane_off + half * 32, sv);
@@ -535,7 +618,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
     const float factor = move ? exp2f(m_used - m_new) : 1.f;
     l *= factor;
     m_used = m_new;
-    if (__any_sync(0xffffffff, move) && kt > 0) {  // warp-collective TMEM round trip over this half of O
+    if (__any_sync(0xffffffff, move) && i > 0) {  // warp-collective TMEM round trip over this half of O
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t u[16];
@@ -574,21 +657,31 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
       for (int j = 0; j < 4; ++j) {
         const uint64_t da = desc_sw128(kb + j * 32, 16, 1024);
         const uint64_t db = desc_sw128(vb + j * 2048, 8192, 1024);
-        tc_mma_bf16(t_o, da, db, idesc_o, kt > 0 || j > 0);
+        tc_mma_bf16(t_o, da, db, idesc_o, i > 0 || j > 0);
       }
       tc_commit(&hd.bar_o);
     }
   }
-  // epilogue: O / l -> bf16; each thread stores its half (64 dims) of row r
+  // epilogue: O / l -> bf16; each thread stores its half (64 dims) of row r.
+  // Key split: the unnormalised O half, plus (m, l) of the row, go to the
+  // workspace instead and attn_combine_kernel merges the splits.
   hd.red[half][r] = l;
   __syncthreads();
   const float lt = hd.red[0][r] + hd.red[1][r];
   const int t = t0 + r / a.G;
-  __nv_bfloat16* dst = a.out + ((long long)t * a.H + kvh * a.G + r % a.G) * kHd + half * 64;
   if (ntiles > 0) {
     mbar_wait(&hd.bar_o, (ntiles - 1) & 1);
     tc_fence_after();
   }
+  float* prow_ws = nullptr;
+  if (nsplit > 1) {
+    prow_ws = a.part + ((((long long)blockIdx.x * gridDim.y + kvh) * zsplit + split) * kTcRows + r) * kPartStride;
+    if (half == 0) {
+      prow_ws[kHd] = m_used;
+      prow_ws[kHd + 1] = lt;
+    }
+  }
+  __nv_bfloat16* dst = a.out + ((long long)t * a.H + kvh * a.G + r % a.G) * kHd + half * 64;
   const float inv = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -596,6 +689,15 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
     if (ntiles > 0) {
       tmem_ld16(t_o + lane_off + half * 64 + c * 16, u);
       tmem_ld_wait();
+    }
+    if (prow_ws) {
+      float4* d4 = reinterpret_cast<float4*>(prow_ws + half * 64 + c * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        d4[j] = ntiles > 0 ? make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]),
+                                         __uint_as_float(u[4 * j + 2]), __uint_as_float(u[4 * j + 3]))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
     }
     uint32_t w[8];
 #pragma unroll
@@ -610,7 +712,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, kTcTmemCols);
+  if (zsplit > 1 && split_arrive(a, hd, kvh, zsplit) && nsplit > 1) merge_splits(a, hd, kvh, zsplit, nsplit);
 }
+
+
 
 static int g_attn_impl = 0;  // 0 by shape, 1 mma.sync only, 2 tcgen05 only
 
@@ -618,13 +723,32 @@ static int g_attn_impl = 0;  // 0 by shape, 1 mma.sync only, 2 tcgen05 only
 
 using namespace sx;
 
-extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* vcache, long long slots,
-                                 const int* dense_len, int dense_const, const int* anc, int anc_base,
-                                 const int* anc_len, int A, void* out, int N, int H, int KVH, cudaStream_t stream) {
+// key splits of the tcgen05 kernel for a grid of `ctas` CTAs: enough to put
+// ~2 CTAs on every SM when the grid alone cannot
+static int attn_splits(long long ctas) {
+  if (ctas >= 148) return 1;
+  const long long s = (2 * 148 + ctas - 1) / ctas;
+  return (int)(s < kMaxSplits ? s : kMaxSplits);
+}
+
+extern "C" long long sx_tree_attention_ws_bytes(int N, int H, int KVH) {
+  if (N <= 0 || KVH <= 0 || H % KVH || kTcRows % (H / KVH)) return 0;
+  const int qb = kTcRows / (H / KVH);
+  const long long ctas = (long long)((N + qb - 1) / qb) * KVH;
+  const int S = attn_splits(ctas);
+  // [arrival counters, 256-B aligned][partials]; the counters must be zero on first use
+  return S > 1 ? ((ctas * 4 + 255) & ~255LL) + ctas * S * kTcRows * kPartStride * (long long)sizeof(float) : 0;
+}
+
+extern "C" int sx_tree_attention_ws(const void* q, const void* kcache, const void* vcache, long long slots,
+                                    const int* dense_len, int dense_const, const int* anc, int anc_base,
+                                    const int* anc_len, int A, void* out, int N, int H, int KVH, void* ws,
+                                    long long ws_bytes, cudaStream_t stream) {
   if (N <= 0) return SX_OK;
   if (KVH <= 0 || H % KVH) return arg_error("attention: H (%d) must be a multiple of KVH (%d)", H, KVH);
   const int G = H / KVH;
   if (G > kAttRows || kAttRows % G) return arg_error("attention: group size %d must divide %d", G, kAttRows);
+  if (A < 0) return arg_error("attention: negative ancestor width %d", A);
   AttnArgs a;
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
   a.kc = reinterpret_cast<const __nv_bfloat16*>(kcache);
@@ -644,24 +768,35 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   a.QB = kAttRows / G;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)kHd);
   a.rescale_thresh = kRescaleThresh;
-  if (A < 0) return arg_error("attention: negative ancestor width %d", A);
-  // Kernel choice (tools/attn_probe.py): the tcgen05 kernel wins everywhere
-  // except narrow groups (G < 4) on mid-size batches (64 < N, fewer than 148
-  // CTAs): there each of its CTAs carries 128 tokens' ancestor lists (2x the
-  // serial key tiles of the 64-row kernel) and the 64-row mma.sync loop wins.
+  a.splits = 1;
+  a.part = nullptr;
+  a.counters = nullptr;
+  // Kernel choice (tools/attn_probe.py): the tcgen05 kernel, with its key tiles
+  // split over up to 8 CTAs when the grid is smaller than the machine (needs the
+  // workspace, sx_tree_attention_ws_bytes). Narrow groups (G < 4) on mid-size
+  // batches (128 < N, < 148 CTAs; 64 < N without a workspace) take the 64-row
+  // mma.sync loop: each tcgen05 CTA would carry 128 tokens' ancestor lists.
   const int tc_qb = kTcRows % G ? 0 : kTcRows / G;
   const long long tc_ctas = tc_qb ? (long long)((N + tc_qb - 1) / tc_qb) * KVH : 0;
+  const long long need = sx_tree_attention_ws_bytes(N, H, KVH);
+  const bool split_ok = need > 0 && ws != nullptr && ws_bytes >= need;
   const bool mma_fits = (long long)(kAttRows / G) * A <= kMaxAncKeys;  // its static ancestor list
-  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && (G >= 4 || N <= 64 || tc_ctas >= 148 || !mma_fits);
+  const bool mma_wins = G < 4 && N > (split_ok ? 128 : 64) && tc_ctas < 148;
+  const bool use_tc = g_attn_impl == 0 && tc_qb > 0 && (!mma_wins || !mma_fits);
   if (use_tc || g_attn_impl == 2) {
     if (kTcRows % G) return arg_error("attention: group size %d must divide %d", G, kTcRows);
     a.QB = kTcRows / G;
     const long long anc_bytes = 4LL * a.QB * (A > 0 ? A : 0);
     if (anc_bytes > 64 * 1024)
       return arg_error("attention: %d tokens x %d ancestors exceed the per-CTA ancestor list", a.QB, A);
+    if (split_ok) {
+      a.splits = attn_splits(tc_ctas);
+      a.counters = reinterpret_cast<int*>(ws);
+      a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((tc_ctas * 4 + 255) & ~255LL));
+    }
     const size_t smem = 1024 + kTcAncOff + (size_t)((anc_bytes + 15) & ~15LL);
     if (int st = ensure_smem_attr((const void*)tree_attention_tc_kernel, (int)smem)) return st;
-    dim3 grid((N + a.QB - 1) / a.QB, KVH);
+    dim3 grid((N + a.QB - 1) / a.QB, KVH, a.splits);
     tree_attention_tc_kernel<<<grid, kTcThreads, smem, stream>>>(a);
     SX_CHECK_LAUNCH("tree_attention_tc_kernel");
     return SX_OK;
@@ -674,6 +809,13 @@ extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* 
   tree_attention_kernel<<<grid, kAttWarps * 32, smem, stream>>>(a);
   SX_CHECK_LAUNCH("tree_attention_kernel");
   return SX_OK;
+}
+
+extern "C" int sx_tree_attention(const void* q, const void* kcache, const void* vcache, long long slots,
+                                 const int* dense_len, int dense_const, const int* anc, int anc_base,
+                                 const int* anc_len, int A, void* out, int N, int H, int KVH, cudaStream_t stream) {
+  return sx_tree_attention_ws(q, kcache, vcache, slots, dense_len, dense_const, anc, anc_base, anc_len, A, out, N, H,
+                              KVH, nullptr, 0, stream);
 }
 
 extern "C" int sx_attention_set_impl(int impl) {

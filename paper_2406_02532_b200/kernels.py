@@ -7,6 +7,7 @@ sizes to ``libspecexec_b200.so``. Nothing here computes on the CPU.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -95,7 +96,9 @@ def gemm_plan(M: int, N: int, K: int, dual: bool = False, splits: int = 0) -> tu
 def _workspace(n_floats: int, device: torch.device) -> torch.Tensor | None:
     if n_floats <= 0:
         return None
-    key = (device.index or 0, 0)
+    # per device AND host thread: stream-K flags / partials must not be shared by
+    # GEMMs running concurrently on different streams (tensor-parallel thread-ranks)
+    key = (device.index or 0, threading.get_ident())
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < n_floats:
         if ws is not None:
@@ -168,7 +171,7 @@ def gemm(
 
 from ._lib import ROWS_LOGITS_F32, ROWS_PROBS_F64, SCORE_ARGMAX, SCORE_RAW, SCORE_WARP  # noqa: E402
 
-_scratch_cache: dict[tuple[int, str], torch.Tensor] = {}
+_scratch_cache: dict[tuple[int, str, int], torch.Tensor] = {}
 
 
 def gemm_qkv_rope(x: torch.Tensor, w: torch.Tensor, H: int, KVH: int, pos, pos_base: int, slot, slot_base: int,
@@ -212,13 +215,16 @@ def gemm_rs(x: torch.Tensor, w: torch.Tensor, peer_inbox: torch.Tensor, rank: in
          M, N, Kd, splits, stream_ptr())
 
 
-def scratch(nbytes: int, device: torch.device, tag: str) -> torch.Tensor:
-    key = (device.index or 0, tag)
+def scratch(nbytes: int, device: torch.device, tag: str, zero: bool = False) -> torch.Tensor:
+    """Per (device, tag, host thread) scratch buffer, grown on demand; `zero`:
+    zero-filled when (re)allocated (kernels that keep counters in it reset them
+    themselves after each launch)."""
+    key = (device.index or 0, tag, threading.get_ident())
     buf = _scratch_cache.get(key)
     if buf is None or buf.numel() < nbytes:
         if buf is not None:
             _keep_alive.append(buf)
-        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        buf = (torch.zeros if zero else torch.empty)(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
         _scratch_cache[key] = buf
     return buf
 

@@ -395,6 +395,8 @@ class LlamaModel(LanguageModel):
         tp, ybf = self.tp, int(self.reduce_bf16)
         epi_y = K.EPI_BF16 if ybf else K.EPI_F32
         H, KVH = self.H, self.KVH
+        attn_ws_bytes = int(_lib.load().sx_tree_attention_ws_bytes(n, H, KVH))  # key-split partials (small grids)
+        attn_ws = K.scratch(attn_ws_bytes, self.device, "attn", zero=True) if attn_ws_bytes > 0 else None
         for li in range(cfg.layers):
             L = self.streamer.acquire(li) if self.streamer is not None else w.layers[li]
             kc, vc = self.kc[li], self.vc[li]
@@ -409,8 +411,8 @@ class LlamaModel(LanguageModel):
                 K.gemm(h, L["wqkv"], out=b.qkv[:n])
                 _lib.call("sx_rope_kv", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, H, KVH,
                           p(self.cos), p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
-            _lib.call("sx_tree_attention", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
-                      anc_base, p(anc_len), A, p(b.att), n, H, KVH, st)
+            _lib.call("sx_tree_attention_ws", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
+                      anc_base, p(anc_len), A, p(b.att), n, H, KVH, p(attn_ws), attn_ws_bytes, st)
             if self.tp_fused:
                 self._fused_reduce(b.att[:n], L["wo"], n)
             else:

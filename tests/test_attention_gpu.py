@@ -51,14 +51,18 @@ def random_tree(rng, n, max_depth):
     return paths
 
 
-def run(impl, q, kc, vc, dense, dense_const, anc, alen, anc_base, A):
+def run(impl, q, kc, vc, dense, dense_const, anc, alen, anc_base, A, split=True):
+    """split: pass the key-split workspace (tcgen05 kernel on small grids)."""
     N, H, _ = q.shape
+    KVH = kc.shape[0]
     out = torch.empty_like(q)
+    nws = int(_lib.load().sx_tree_attention_ws_bytes(N, H, KVH)) if split else 0
+    ws = torch.zeros(max(nws, 1), dtype=torch.uint8, device=q.device)  # arrival counters start at 0
     _lib.call("sx_attention_set_impl", impl)
     try:
-        _lib.call("sx_tree_attention", p(q), p(kc), p(vc), kc.shape[1], p(dense) if dense is not None else None,
+        _lib.call("sx_tree_attention_ws", p(q), p(kc), p(vc), kc.shape[1], p(dense) if dense is not None else None,
                   dense_const, p(anc) if anc is not None else None, anc_base, p(alen) if alen is not None else None,
-                  A, p(out), N, H, kc.shape[0], _lib.stream_ptr())
+                  A, p(out), N, H, KVH, p(ws) if nws else None, nws, _lib.stream_ptr())
     finally:
         _lib.call("sx_attention_set_impl", 0)
     torch.cuda.synchronize()
@@ -183,3 +187,31 @@ def test_deep_ancestor_lists_mha(cuda):
     torch.testing.assert_close(got, exp, atol=2e-2, rtol=2e-2)
     with pytest.raises(ValueError):
         run(1, q, kc, vc, dense, 0, torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda(), ctx, A)
+
+
+@pytest.mark.parametrize("H,KVH,N,ctx,D", [(64, 8, 1, 300, 0), (32, 32, 1, 700, 0), (64, 8, 37, 130, 16),
+                                           (32, 32, 256, 160, 16), (32, 8, 200, 2000, 3)])
+def test_key_split_matches_unsplit(cuda, H, KVH, N, ctx, D):
+    """Small grids run the tcgen05 kernel with its key tiles split over several
+    CTAs and merged by attn_combine_kernel: same result as one CTA per tile
+    row (and as the fp32 reference)."""
+    assert _lib.load().sx_tree_attention_ws_bytes(N, H, KVH) > 0
+    rng = np.random.default_rng(N + ctx)
+    A = D + 1
+    anc = np.zeros((N, A), np.int32)
+    alen = np.zeros(N, np.int32)
+    if D > 0:
+        for t, path in enumerate(random_tree(rng, N, D)):
+            anc[t, : len(path)] = path
+            alen[t] = len(path)
+    else:
+        alen[:] = 1
+        anc[:, 0] = np.arange(N)
+    q, kc, vc = make(N, H, KVH, ctx + N + 8, seed=N + 1)
+    dense = torch.full((N,), ctx, dtype=torch.int32, device="cuda")
+    args = (q, kc, vc, dense, 0, torch.from_numpy(anc).cuda(), torch.from_numpy(alen).cuda(), ctx, A)
+    got_split = run(2, *args, split=True)
+    got_one = run(2, *args, split=False)
+    exp = reference(q, kc, vc, dense.cpu(), anc, alen, ctx)
+    torch.testing.assert_close(got_split, exp, atol=2e-2, rtol=2e-2)
+    torch.testing.assert_close(got_split, got_one, atol=1e-2, rtol=1e-2)
