@@ -1,5 +1,6 @@
 #!/bin/bash
-# A/B: epilogue-warp back-off while the mainloop runs (power under the 1 kW cap)
+# A/B (historical): epilogue-warp back-off while the mainloop runs (power under the 1 kW cap).
+# The SX_GEMM_EPI_SLEEP knob was removed after this measurement (no effect); kept as the recipe of profiles/r1/gemm_epi_sleep_ab.log
 mkdir -p gpurun_out
 rm -f gpurun_out/sleep_ab.log
 for ns in 0 1000 0 1000 0 4000; do
