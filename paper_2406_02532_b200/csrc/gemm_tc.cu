@@ -780,9 +780,11 @@ static Plan make_plan(int M, int Nf, int K, int dual, int req) {
   // CTA-pair tree-pass shapes: the token-tile width sets both the padding of
   // M = K+1 and how the tiles fill the 74 pairs; pick the width with the lowest
   // (rounds x width) over {auto, 176, 128} when it is >10% better (70B o-proj at
-  // M = 1025: 160 tiles of 208 = 2.2 rounds -> 288 tiles of 128 = 3.9 rounds,
-  // 118 -> 113 us, profiles/r1/plan_sweep_c2.jsonl).
-  if (p.cg == 2 && bn_req == 0 && !dual && K <= 8192) {  // long-K shapes balance with the split tail instead
+  // M = 1025: 160 tiles of 208 = 2.2 rounds -> 192 tiles of 176 = 2.6 rounds,
+  // 118 -> 113 us; 70B down-proj (K = 28672): 208-wide tiles + split tail
+  // 381-392 us -> 176-wide whole tiles 374-377 us, profiles/r1/plan_fine_down.jsonl;
+  // neutral in the power-capped loop).
+  if (p.cg == 2 && bn_req == 0 && !dual) {
     auto cost = [&](int bn) {
       const long long t = (long long)p.tiles_f * ((M + bn - 1) / bn);
       return (double)((t + P - 1) / P) * bn;

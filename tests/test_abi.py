@@ -57,12 +57,17 @@ def test_gemm_plan_tiles():
     bn, sp, ws = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong()
     assert lib.sx_gemm_plan(1025, 8192, 8192, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
     assert bn.value % 16 == 0 and bn.value * ((1025 + bn.value - 1) // bn.value) < 1025 + 5 * 16
-    # CTA-pair tiles (256 weight rows) on 74 pairs: 32 x 5 = 160 tiles leave a
-    # 2.16-wave tail, but a 6-way split of 64 k-blocks (of 128) is too short to
-    # amortise the fixup -> whole tiles; at K = 28672 -> split tail over 74 pairs
-    assert sp.value == 1
+    # CTA-pair tiles (256 weight rows) on 74 pairs: the token-tile width with the
+    # lowest (rounds x width): 6 x 176 (192 tiles, 3 rounds) beats 5 x 208 -> whole tiles
+    assert sp.value == 1 and bn.value == 176
+    # the same for the long-K down projection (K = 28672): whole 176-wide tiles
+    # measured 2-4 % faster than 208-wide tiles + a K-split tail
     assert lib.sx_gemm_plan(1025, 8192, 28672, 0, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
-    assert sp.value == 74 and ws.value == 1024 + 74 * 2 * bn.value * 128
+    assert bn.value == 176 and sp.value == 1
+    # a forced split tail (sched 3) on 208-wide tiles still plans the 74-pair tail split
+    assert lib.sx_gemm_plan(1025, 8192, 28672, 0, 3 | 2 << 4 | 13 << 8, ctypes.byref(bn), ctypes.byref(sp),
+                            ctypes.byref(ws)) == 0
+    assert bn.value == 208 and sp.value == 74 and ws.value == 1024 + 74 * 2 * bn.value * 128
     # 112 x 9 = 1008 SwiGLU pair tiles fill 14 waves at 97% -> whole tiles
     assert lib.sx_gemm_plan(1025, 28672, 8192, 1, 0, ctypes.byref(bn), ctypes.byref(sp), ctypes.byref(ws)) == 0
     assert sp.value == 1 and ws.value == 0

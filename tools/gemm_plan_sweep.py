@@ -57,6 +57,7 @@ def main():
     ap.add_argument("--set", default="c2")
     ap.add_argument("--only", default="")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fine", action="store_true", help="pair tiles over every token-tile width 64..256")
     a = ap.parse_args()
     recs = []
     for name, M, N, Kd, epi in SETS[a.set]:
@@ -76,10 +77,15 @@ def main():
             i[0] += 1
 
         cands = [0]
-        for cg in (1, 2):
-            for bn in (0, 64, 128, 208, 256):
-                for sched in (1, 3, 2):
-                    cands.append(sched | cg << 4 | (bn // 16) << 8)
+        if a.fine:  # pair tiles, whole tiles / split tail, every token-tile width
+            for bn in range(64, 257, 16):
+                for sched in (1, 3):
+                    cands.append(sched | 2 << 4 | (bn // 16) << 8)
+        else:
+            for cg in (1, 2):
+                for bn in (0, 64, 128, 208, 256):
+                    for sched in (1, 3, 2):
+                        cands.append(sched | cg << 4 | (bn // 16) << 8)
         ok = []
         for req in cands:  # drop illegal combinations
             try:
