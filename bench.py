@@ -78,9 +78,9 @@ def parse():
     ap.add_argument("--parallel", choices=["tp", "replicas"], default="tp",
                     help="N>1: tensor-parallel target (one stream) or N independent replicas")
     ap.add_argument("--reduce", choices=["bf16", "fp32"], default="bf16", help="TP all-reduce precision")
-    ap.add_argument("--tp-comm", choices=["fused", "nccl"], default="fused",
-                    help="TP reduction: GEMM epilogue reduce-scatter over peer memory (falls back to NCCL if "
-                         "symmetric memory is unavailable) or NCCL all-reduce")
+    ap.add_argument("--tp-comm", choices=["fused", "nccl"], default="nccl",
+                    help="TP reduction: NCCL all-reduce (default, north_star), or the opt-in GEMM epilogue "
+                         "reduce-scatter over peer memory (not yet run on multi-GPU hardware)")
     ap.add_argument("--attn", choices=["auto", "mma", "tc"], default="auto",
                     help="tree attention kernel: by shape (default), the mma.sync loop only, tcgen05 only (A/B)")
     return ap.parse_args()
@@ -339,7 +339,7 @@ def main():
     offload = args.workload in OFFLOAD
     target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn,
                         offload=offload, offload_buffers=args.offload_buffers, tp=comm, reduce_bf16=args.reduce == "bf16",
-                        tp_fused=None if args.tp_comm == "fused" else False)
+                        tp_fused=True if args.tp_comm == "fused" else False)
     draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
                        synthetic=syn)
     torch.cuda.synchronize()

@@ -203,7 +203,7 @@ SX_API int sx_specinfer_verify(const void* trows, int row_kind, long long ld, in
  *   sx_tree_attention  query t attends KV slots [0, dense_len[t]) (NULL: dense_const)
  *                 plus the anc_len[t] slots anc_base + anc[t*A ...] (root, ancestors, itself) -- the
  *                 flattened ancestor mask of tree.py:208-219 without a dense mask
- *   sx_kv_compact move KV rows src[i] -> dst[i] in every layer / head (accepted
+ *   sx_kv_compact move KV rows src[i] -> dst[i] (n <= 448) in every layer / head (accepted
  *                 path -> committed region after the walk)
  */
 SX_API int sx_embed(const void* E, const int* tokens, int n, int d, float* x, cudaStream_t stream);

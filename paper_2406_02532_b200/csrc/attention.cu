@@ -731,13 +731,21 @@ static int attn_splits(long long ctas) {
   return (int)(s < kMaxSplits ? s : kMaxSplits);
 }
 
+// Workspace = [fixed arrival-counter header][partials]. The header size does not
+// depend on N: callers reuse one zero-once workspace across launches of every
+// shape (draft buckets, one-token graphs, target passes), and a counter slot must
+// never alias partials a differently-sized launch wrote. Splits happen only for
+// grids of < 148 CTAs, so 148 counters always fit.
+constexpr long long kAttnCounterBytes = 1024;
+static_assert(148 * 4 <= kAttnCounterBytes, "counter header too small");
+
 extern "C" long long sx_tree_attention_ws_bytes(int N, int H, int KVH) {
   if (N <= 0 || KVH <= 0 || H % KVH || kTcRows % (H / KVH)) return 0;
   const int qb = kTcRows / (H / KVH);
   const long long ctas = (long long)((N + qb - 1) / qb) * KVH;
   const int S = attn_splits(ctas);
-  // [arrival counters, 256-B aligned][partials]; the counters must be zero on first use
-  return S > 1 ? ((ctas * 4 + 255) & ~255LL) + ctas * S * kTcRows * kPartStride * (long long)sizeof(float) : 0;
+  // the counters must be zero on first use; the kernel resets them after each launch
+  return S > 1 ? kAttnCounterBytes + ctas * S * kTcRows * kPartStride * (long long)sizeof(float) : 0;
 }
 
 extern "C" int sx_tree_attention_ws(const void* q, const void* kcache, const void* vcache, long long slots,
@@ -792,7 +800,7 @@ extern "C" int sx_tree_attention_ws(const void* q, const void* kcache, const voi
     if (split_ok) {
       a.splits = attn_splits(tc_ctas);
       a.counters = reinterpret_cast<int*>(ws);
-      a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((tc_ctas * 4 + 255) & ~255LL));
+      a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kAttnCounterBytes);
     }
     const size_t smem = 1024 + kTcAncOff + (size_t)((anc_bytes + 15) & ~15LL);
     if (int st = ensure_smem_attr((const void*)tree_attention_tc_kernel, (int)smem)) return st;

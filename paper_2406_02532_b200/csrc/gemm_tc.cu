@@ -85,7 +85,7 @@ struct GemmArgs {
   long long rope_slots;
   int* flags;      // stream-K partial-ready flags [ctas * CG]
   float* part;     // stream-K partials [ctas * CG][dual?2:1][BN][128]
-  int debug_no_tma;  // SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
+  int debug_no_tma;  // measurement builds (-DSX_GEMM_MEASURE_MMA_ONLY) + SX_GEMM_DEBUG=1: skip TMA after the first ring fill (MMA-rate measurement only)
 };
 
 constexpr int kGemmThreads = 192;
@@ -1081,8 +1081,14 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   g.rs_slice = rs_slice;
   g.flags = p.streamk ? reinterpret_cast<int*>(ws) : nullptr;
   g.part = p.streamk ? ws + kFlagFloats : nullptr;
+#ifdef SX_GEMM_MEASURE_MMA_ONLY
+  // measurement builds only (tools/gemm_probe.py: make MEASURE=1): MMA on stale
+  // tiles after the first ring fill -- wrong results by design, never in the product
   static const int debug_no_tma = env_int("SX_GEMM_DEBUG", 0);
   g.debug_no_tma = debug_no_tma;
+#else
+  g.debug_no_tma = 0;
+#endif
 
   const size_t smem = 1024 + (size_t)g.stages * g.stage_bytes + 1024 + 8192;
 #define SX_GEMM_LAUNCH(CG, DU, KP) \

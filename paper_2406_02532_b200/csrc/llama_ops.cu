@@ -259,7 +259,9 @@ extern "C" int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const i
 extern "C" int sx_kv_compact(void* kcache, void* vcache, int layers, long long layer_stride, long long slots, int KVH,
                              const int* src, const int* dst, int n, cudaStream_t stream) {
   if (n <= 0) return SX_OK;
-  if (n > 192) return arg_error("kv_compact: at most 192 rows per call (got %d)", n);
+  // all rows are staged in smem (512 B per row: K and V of one head) -- up to
+  // 448 rows, more than the deepest accepted path (max_depth <= 250 -> 251 rows)
+  if (n > 448) return arg_error("kv_compact: at most 448 rows per call (got %d)", n);
   const size_t smem = (size_t)2 * n * 16 * sizeof(uint4);
   if (smem > 48 * 1024)
     if (int st = ensure_smem_attr((const void*)kv_compact_kernel, (int)smem)) return st;

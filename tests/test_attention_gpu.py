@@ -215,3 +215,31 @@ def test_key_split_matches_unsplit(cuda, H, KVH, N, ctx, D):
     exp = reference(q, kc, vc, dense.cpu(), anc, alen, ctx)
     torch.testing.assert_close(got_split, exp, atol=2e-2, rtol=2e-2)
     torch.testing.assert_close(got_split, got_one, atol=1e-2, rtol=1e-2)
+
+
+def test_key_split_workspace_reused_across_shapes(cuda):
+    """One zero-once workspace serves split launches of different grid sizes
+    (the model's shared 'attn' scratch: draft buckets, one-token graphs, target
+    passes). A small grid's partials must never land on a larger grid's arrival
+    counters (fixed counter header, attention.cu kAttnCounterBytes)."""
+    H, KVH, ctx = 64, 8, 600
+    shapes = [1, 32, 200, 1, 100, 200]  # G = 8: 16 tokens per CTA -> 8..104 CTAs, all split
+    nmax = max(int(_lib.load().sx_tree_attention_ws_bytes(n, H, KVH)) for n in shapes)
+    ws = torch.zeros(nmax, dtype=torch.uint8, device="cuda")
+    _lib.call("sx_attention_set_impl", 2)
+    try:
+        for i, N in enumerate(shapes):
+            nws = int(_lib.load().sx_tree_attention_ws_bytes(N, H, KVH))
+            assert nws > 0
+            q, kc, vc = make(N, H, KVH, ctx + N + 8, seed=100 + i)
+            dense = torch.full((N,), ctx, dtype=torch.int32, device="cuda")
+            anc = torch.arange(N, dtype=torch.int32, device="cuda").view(N, 1)
+            alen = torch.ones(N, dtype=torch.int32, device="cuda")
+            out = torch.empty_like(q)
+            _lib.call("sx_tree_attention_ws", p(q), p(kc), p(vc), kc.shape[1], p(dense), 0, p(anc), ctx, p(alen), 1,
+                      p(out), N, H, KVH, p(ws), nmax, _lib.stream_ptr())
+            torch.cuda.synchronize()
+            exp = reference(q, kc, vc, dense.cpu(), anc.cpu().numpy(), alen.cpu().numpy(), ctx)
+            torch.testing.assert_close(out.float(), exp, atol=2e-2, rtol=2e-2)
+    finally:
+        _lib.call("sx_attention_set_impl", 0)
