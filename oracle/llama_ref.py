@@ -31,11 +31,56 @@ def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
 def forward_logits(cfg, W: dict, tokens: list[int], bias=None, layers: int | None = None) -> torch.Tensor:
     """fp32 logits [len(tokens), V] for every position of a causal prefix."""
     n = len(tokens)
+    mask = torch.full((n, n), float("-inf")).triu(1)
+    return forward_masked(cfg, W, tokens, torch.arange(n), mask, bias, layers)
+
+
+@torch.no_grad()
+def forward_tree_logits(cfg, W: dict, prompt: list[int], paths: list[tuple[int, ...]], bias=None,
+                        layers: int | None = None) -> torch.Tensor:
+    """fp32 logits [1 + len(paths), V]: row 0 = the next token after `prompt`,
+    row 1 + i = the next token after prompt + paths[i] -- what the reference's
+    `precompute` asks of the target (pkg/src/speckit/engine.py:73-89): one row
+    per tree prefix. `paths` must be prefix-closed (every non-empty path's
+    parent path is listed, or is the empty root path) and parents must come
+    first. One forward over prompt + tree tokens with the flattened ancestor
+    mask of pkg/src/speckit/tree.py:208-219 (node i sees the prompt, its
+    ancestors and itself) at position len(prompt) - 1 + depth; each row is
+    mathematically the causal forward of its full prefix (checked by
+    tests/test_llama_ref_cpu.py)."""
+    P, n = len(prompt), len(paths)
+    index = {(): P - 1}  # path -> sequence row (the root = the prompt's last token)
+    toks = list(prompt)
+    pos = list(range(P))
+    parent_row = []
+    for i, path in enumerate(paths):
+        if len(path) == 0 or path[:-1] not in index:
+            raise ValueError(f"paths must be non-empty and prefix-closed, parents first (path {i})")
+        index[tuple(path)] = P + i
+        toks.append(int(path[-1]))
+        pos.append(P - 1 + len(path))
+        parent_row.append(index[path[:-1]])
+    T = P + n
+    allow = torch.zeros((T, T), dtype=torch.bool)
+    allow[:P, :P] = torch.ones((P, P), dtype=torch.bool).tril()
+    for i in range(n):  # parents first: copy the parent's visibility, add self
+        r = P + i
+        allow[r] = allow[parent_row[i]]
+        allow[r, r] = True
+    mask = torch.zeros((T, T)).masked_fill(~allow, float("-inf"))
+    logits = forward_masked(cfg, W, toks, torch.tensor(pos), mask, bias, layers)
+    return torch.cat([logits[P - 1 : P], logits[P:]], dim=0)
+
+
+@torch.no_grad()
+def forward_masked(cfg, W: dict, tokens: list[int], pos: torch.Tensor, mask: torch.Tensor, bias=None,
+                   layers: int | None = None) -> torch.Tensor:
+    """fp32 logits of every row of `tokens` at positions `pos` under an additive
+    attention mask [n, n] (0 = visible, -inf = masked)."""
+    n = len(tokens)
     H, KVH, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
     tok = torch.tensor(tokens, dtype=torch.long)
     x = W["emb"][tok].clone()
-    pos = torch.arange(n)
-    mask = torch.full((n, n), float("-inf")).triu(1)
     for L in W["layers"][: layers if layers is not None else len(W["layers"])]:
         h = rmsnorm(x, L["n1"], cfg.eps)
         qkv = h @ L["wqkv"].t()
