@@ -11,6 +11,7 @@ no tree mask, no kernels. HF Llama conventions: RMSNorm, rotate-half RoPE
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 
@@ -28,16 +29,17 @@ def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
 
 
 @torch.no_grad()
-def forward_logits(cfg, W: dict, tokens: list[int], bias=None, layers: int | None = None) -> torch.Tensor:
+def forward_logits(cfg, W: dict, tokens: list[int], bias=None, layers: int | None = None,
+                   policy: str = "fp32") -> torch.Tensor:
     """fp32 logits [len(tokens), V] for every position of a causal prefix."""
     n = len(tokens)
     mask = torch.full((n, n), float("-inf")).triu(1)
-    return forward_masked(cfg, W, tokens, torch.arange(n), mask, bias, layers)
+    return forward_masked(cfg, W, tokens, torch.arange(n), mask, bias, layers, policy)
 
 
 @torch.no_grad()
 def forward_tree_logits(cfg, W: dict, prompt: list[int], paths: list[tuple[int, ...]], bias=None,
-                        layers: int | None = None) -> torch.Tensor:
+                        layers: int | None = None, policy: str = "fp32") -> torch.Tensor:
     """fp32 logits [1 + len(paths), V]: row 0 = the next token after `prompt`,
     row 1 + i = the next token after prompt + paths[i] -- what the reference's
     `precompute` asks of the target (pkg/src/speckit/engine.py:73-89): one row
@@ -68,35 +70,45 @@ def forward_tree_logits(cfg, W: dict, prompt: list[int], paths: list[tuple[int, 
         allow[r] = allow[parent_row[i]]
         allow[r, r] = True
     mask = torch.zeros((T, T)).masked_fill(~allow, float("-inf"))
-    logits = forward_masked(cfg, W, toks, torch.tensor(pos), mask, bias, layers)
+    logits = forward_masked(cfg, W, toks, torch.tensor(pos), mask, bias, layers, policy)
     return torch.cat([logits[P - 1 : P], logits[P:]], dim=0)
 
 
 @torch.no_grad()
 def forward_masked(cfg, W: dict, tokens: list[int], pos: torch.Tensor, mask: torch.Tensor, bias=None,
-                   layers: int | None = None) -> torch.Tensor:
+                   layers: int | None = None, policy: str = "fp32") -> torch.Tensor:
     """fp32 logits of every row of `tokens` at positions `pos` under an additive
-    attention mask [n, n] (0 = visible, -inf = masked)."""
+    attention mask [n, n] (0 = visible, -inf = masked).
+
+    policy="fp32": every activation in fp32 (the reference's meaning of the
+    model). policy="bf16": the same arithmetic with activations rounded to bf16
+    exactly where the B200 bf16 path stores them (the GEMM operands: normed
+    inputs, RoPE'd q / k and v in the KV cache, the attention output, the SwiGLU
+    product, the final normed row; residual stream and accumulators fp32) -- the
+    precision policy the north_star's "2e-2 abs in bf16" is measured against."""
+    if policy not in ("fp32", "bf16"):
+        raise ValueError(f"unknown precision policy {policy!r}")
+    act = (lambda t: t.bfloat16().float()) if policy == "bf16" else (lambda t: t)
     n = len(tokens)
     H, KVH, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
     tok = torch.tensor(tokens, dtype=torch.long)
     x = W["emb"][tok].clone()
     for L in W["layers"][: layers if layers is not None else len(W["layers"])]:
-        h = rmsnorm(x, L["n1"], cfg.eps)
+        h = act(rmsnorm(x, L["n1"], cfg.eps))
         qkv = h @ L["wqkv"].t()
         q = qkv[:, : H * hd].view(n, H, hd)
         k = qkv[:, H * hd : (H + KVH) * hd].view(n, KVH, hd)
-        v = qkv[:, (H + KVH) * hd :].view(n, KVH, hd)
-        q, k = rope(q, pos, cfg.rope_theta), rope(k, pos, cfg.rope_theta)
+        v = act(qkv[:, (H + KVH) * hd :].view(n, KVH, hd))
+        q, k = act(rope(q, pos, cfg.rope_theta)), act(rope(k, pos, cfg.rope_theta))
         g = H // KVH
         k = k.repeat_interleave(g, dim=1)
         v = v.repeat_interleave(g, dim=1)
         s = torch.einsum("qhd,khd->hqk", q, k) / hd**0.5 + mask
-        att = torch.einsum("hqk,khd->qhd", s.softmax(-1), v).reshape(n, H * hd)
+        att = act(torch.einsum("hqk,khd->qhd", s.softmax(-1), v).reshape(n, H * hd))
         x = x + att @ L["wo"].t()
-        h = rmsnorm(x, L["n2"], cfg.eps)
-        x = x + (torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
-    logits = rmsnorm(x, W["nf"], cfg.eps) @ W["lm"].t()
+        h = act(rmsnorm(x, L["n2"], cfg.eps))
+        x = x + act(torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
+    logits = act(rmsnorm(x, W["nf"], cfg.eps)) @ W["lm"].t()
     if bias is not None:
         u, w = bias
         logits = logits + u[tok] @ w.t()
@@ -138,3 +150,55 @@ def forward_logits_tp(cfg, W_local: dict, tokens: list[int], shard, all_reduce, 
     local = rmsnorm(x, W_local["nf"], cfg.eps) @ W_local["lm"].t()
     parts = all_gather(local)
     return torch.cat(list(parts), dim=1)
+
+
+class CpuLlamaLM:
+    """The reference plugin interface (pkg/src/speckit/models.py:32-63) over the
+    fp32 CPU forward: `next_distributions(prefixes)` -> canonical float64 softmax
+    rows (oracle.speckit_oracle.softmax_row, the rows the GPU computes from its
+    fp32 logits). The TorchCpuLlama of SURVEY 8(c)/(d): the timed CPU reference
+    path of bench.py's reference arm. A batch is evaluated as one tree-masked
+    forward over the prefix closure of its prefixes below their common prefix
+    (every row equals the stateless causal forward of its prefix)."""
+
+    backend = "cpu-llama"
+
+    def __init__(self, cfg, W: dict, policy: str = "fp32", threads: int | None = None):
+        self.cfg, self.W, self.policy = cfg, W, policy
+        self.vocab_size = cfg.vocab
+        if threads:
+            torch.set_num_threads(threads)
+
+    def logits(self, prefixes) -> torch.Tensor:
+        prefixes = [tuple(int(t) for t in p) for p in prefixes]
+        if not prefixes:
+            return torch.empty((0, self.vocab_size))
+        if any(len(p) == 0 for p in prefixes):
+            raise ValueError("empty prefix")
+        c = min(len(p) for p in prefixes)
+        first = prefixes[0]
+        while c > 1 and any(p[:c] != first[:c] for p in prefixes):
+            c -= 1
+        anchor = list(first[:c])
+        if any(p[:c] != first[:c] for p in prefixes):  # no shared token at all: one forward each
+            return torch.stack([forward_logits(self.cfg, self.W, list(p), policy=self.policy)[-1] for p in prefixes])
+        closure: dict[tuple[int, ...], None] = {}
+        for p in prefixes:
+            tail = p[c:]
+            for j in range(1, len(tail) + 1):
+                closure.setdefault(tail[:j], None)
+        paths = sorted(closure, key=len)
+        rows = forward_tree_logits(self.cfg, self.W, anchor, paths, policy=self.policy)
+        at = {(): 0, **{q: i + 1 for i, q in enumerate(paths)}}
+        return rows[[at[p[c:]] for p in prefixes]]
+
+    def next_distributions(self, prefixes):
+        from .speckit_oracle import softmax_row
+
+        z = self.logits(prefixes).numpy().astype(np.float32)
+        if z.shape[0] == 0:
+            return np.empty((0, self.vocab_size))
+        return np.stack([softmax_row(z[i]) for i in range(z.shape[0])])
+
+    def next_distribution(self, prefix):
+        return self.next_distributions([prefix])[0]

@@ -9,8 +9,10 @@ There is no CPU fallback: without the built library or a CUDA device every
 device call raises.
 """
 
+from .costsim import (AcceptanceCurve, BudgetChoice, CostModel, crossover_tokens, estimate_throughput, forward_time,
+                      load_preset, optimize_budget)
 from .engine import GenStats, ProbCache, generate_sequential, generate_specexec, precompute, stats_record
-from .models import LanguageModel, MarkovModel, TabularModel, make_synthetic, model_from_json
+from .models import HostRowsModel, LanguageModel, MarkovModel, TabularModel, make_synthetic, model_from_json
 from .rng import CounterRng
 from .sampling import SamplingConfig, apply_warp, sample, validate_distribution
 from .tree import ROOT, BuilderParams, DraftNode, DraftTree, FlattenedTree, build_sssp, flatten
@@ -21,6 +23,15 @@ from .specinfer import (VerifyOutcome, branching_for_budget, build_stochastic, g
 __version__ = "0.1.0"
 
 __all__ = [
+    "AcceptanceCurve",
+    "BudgetChoice",
+    "CostModel",
+    "HostRowsModel",
+    "crossover_tokens",
+    "estimate_throughput",
+    "forward_time",
+    "load_preset",
+    "optimize_budget",
     "ROOT",
     "BuilderParams",
     "CounterRng",

@@ -203,8 +203,8 @@ class SpecExecSession:
     device walk until a miss or the token limit)."""
 
     def __init__(self, prompt, draft, target, params: BuilderParams, cfg: SamplingConfig, warp_scores: bool = True):
-        if draft is target and hasattr(target, "commit_walk"):
-            raise ValueError("draft and target must be distinct model objects (separate KV caches)")
+        if draft is target and hasattr(target, "draft_view"):
+            draft = target.draft_view()  # one network in both roles: a second KV cache for the draft
         self.prompt = tuple(int(t) for t in prompt)
         self.draft, self.target, self.params, self.cfg = draft, target, params, cfg
         self.warp_scores = warp_scores

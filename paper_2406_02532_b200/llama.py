@@ -140,14 +140,22 @@ class LlamaWeights:
     up projections are stored interleaved ("wgu", interleave_gate_up)."""
 
     def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0,
-                 offload: bool = False, shard: TPShard | None = None):
+                 offload: bool = False, shard: TPShard | None = None, init: str = "device"):
+        """init="device": drawn by a CUDA generator (fast at 70B); "host": drawn
+        by a CPU generator and uploaded -- the same values `host_weights_fp32`
+        draws without a GPU (the CPU reference arm's copy of small models)."""
+        if init not in ("device", "host"):
+            raise ValueError(f"init must be 'device' or 'host', got {init!r}")
         self.cfg = cfg
         self.offload = offload
         self.shard = shard
-        g = torch.Generator(device=device)
+        host = init == "host"
+        g = torch.Generator(device="cpu" if host else device)
         g.manual_seed(seed)
 
         def rnd_(t, s=std):
+            if host:
+                return t.copy_(torch.empty(t.shape, dtype=t.dtype).normal_(0.0, s, generator=g))
             return t.normal_(0.0, s, generator=g)
 
         self.emb = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device))
@@ -200,6 +208,25 @@ class LlamaWeights:
             "nf": f(self.nf),
             "lm": f(self.lm),
         }
+
+
+def host_weights_fp32(cfg: LlamaConfig, seed: int, std: float = 0.02, lm_scale: float = 1.0) -> dict:
+    """The weights LlamaWeights(init="host") draws -- same CPU generator, same
+    draw order, bf16 values -- as fp32 CPU tensors in the CPU reference forward's
+    layout (oracle/llama_ref.py). No GPU needed (bench.py's reference arm)."""
+    g = torch.Generator(device="cpu")
+    g.manual_seed(seed)
+    rnd = lambda shape, s=std: torch.empty(shape, dtype=torch.bfloat16).normal_(0.0, s, generator=g)  # noqa: E731
+    emb = rnd((cfg.vocab, cfg.d)).float()
+    shapes = TPShard(0, 1).local_shapes(cfg)
+    layers = []
+    for _ in range(cfg.layers):
+        L = {k: rnd(shapes[k]).float() for k in ("wqkv", "wo", "wg", "wu", "wd")}
+        L["n1"] = torch.ones(cfg.d)
+        L["n2"] = torch.ones(cfg.d)
+        layers.append(L)
+    lm = rnd((cfg.vocab, cfg.d), std * lm_scale).float()
+    return {"emb": emb, "layers": layers, "nf": torch.ones(cfg.d), "lm": lm}
 
 
 class LayerStreamer:
@@ -297,6 +324,7 @@ class LlamaModel(LanguageModel):
         reduce_bf16: bool = True,
         tp_fused: bool | None = None,
         offload_buffers: int = 8,
+        init: str = "device",
     ):
         """offload_buffers: HBM staging slots of the layer streamer (offload mode);
         beyond the 2 a double buffer needs, the extra slots let the host link keep
@@ -328,7 +356,7 @@ class LlamaModel(LanguageModel):
         self.reduce_bf16 = bool(reduce_bf16 and self.tp is not None)
         self.H = cfg.heads // (self.tp.world if self.tp else 1)  # local query / KV heads
         self.KVH = cfg.kv_heads // (self.tp.world if self.tp else 1)
-        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload, shard=self.shard)
+        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload, shard=self.shard, init=init)
         self.streamer = LayerStreamer(self.w, self.device, nbuf=max(2, min(offload_buffers, cfg.layers))) if offload else None
         self.slots = max_ctx
         self.kc = torch.zeros((cfg.layers, self.KVH, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
@@ -374,6 +402,29 @@ class LlamaModel(LanguageModel):
         LlamaModel._serial += 1
         self._uid = LlamaModel._serial
         self.stats = {"forward_tokens": 0, "forwards": 0}
+
+    def draft_view(self) -> "LlamaModel":
+        """The same network (weights, buffers, communicator shared) with its own
+        KV cache and prefix state, for the draft role when a caller passes one
+        model as both draft and target (the reference CLI's default,
+        pkg/src/speckit/harness/cli.py:91): the roles keep different committed
+        prefixes and tree slots, so they cannot share one cache. Created once."""
+        v = getattr(self, "_draft_view_model", None)
+        if v is None:
+            v = object.__new__(type(self))
+            v.__dict__.update(self.__dict__)
+            v.kc = torch.zeros_like(self.kc)
+            v.vc = torch.zeros_like(self.vc)
+            v.committed = []
+            v.record = None
+            v._one_args = torch.zeros(4, dtype=torch.int32, device=self.device)
+            v._g1, v._g1_out, v._g1_warm = None, None, False
+            LlamaModel._serial += 1
+            v._uid = LlamaModel._serial
+            v.stats = {"forward_tokens": 0, "forwards": 0}
+            v._draft_view_model = v
+            self._draft_view_model = v
+        return v
 
     # ------------------------------------------------------------------ forward
     def forward(self, n: int, tokens: torch.Tensor, pos: torch.Tensor | None, pos_base: int, slot: torch.Tensor | None,

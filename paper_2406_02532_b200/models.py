@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import json
 import threading
+import weakref
 from typing import Iterable, Sequence
 
 import numpy as np
@@ -71,12 +72,19 @@ class LanguageModel:
 
 
 def as_device_model(model) -> "LanguageModel":
-    if not hasattr(model, "tree_session") or not hasattr(model, "tree_rows"):
-        raise TypeError(
-            f"{type(model).__name__} is not a device model; use paper_2406_02532_b200 models "
-            "(TabularModel/MarkovModel/make_synthetic/LlamaModel)"
-        )
-    return model
+    """The device-model view of a plugin: this package's models as they are; any
+    other object with the reference plugin interface (`vocab_size`,
+    `next_distributions(prefixes) -> float64 [n, V]`, pkg/src/speckit/models.py:32-63
+    -- e.g. the reference's own MarkovModel / NgramModel / resolve_model outputs or
+    a user plugin) through `HostRowsModel`, which uploads the rows it returns to
+    HBM so the same GPU tree / warp / walk kernels consume them."""
+    if hasattr(model, "tree_session") and hasattr(model, "tree_rows"):
+        return model
+    if hasattr(model, "next_distributions") and hasattr(model, "vocab_size"):
+        return HostRowsModel.wrap(model)
+    raise TypeError(
+        f"{type(model).__name__} is not a LanguageModel: it needs vocab_size and next_distributions(prefixes)"
+    )
 
 
 def _normalize_rows(table: np.ndarray) -> np.ndarray:
@@ -268,3 +276,138 @@ def model_from_json(document: str) -> LanguageModel:
     if backend == "markov":
         return MarkovModel(np.asarray(data["table"]), order=data["order"])
     raise ValueError(f"unknown backend {backend!r}")
+
+
+# ---------------------------------------------------------------------------
+# host-row plugins (the drop-in boundary for models this package did not build)
+# ---------------------------------------------------------------------------
+
+
+def _host_rows(model, prefixes: list[Prefix]) -> np.ndarray:
+    """`next_distributions` of a host plugin as a float64 [n, V] array (ValueError
+    on a wrong shape -- the reference's contract, models.py:47-52)."""
+    V = int(model.vocab_size)
+    if not prefixes:
+        return np.empty((0, V))
+    rows = np.asarray(model.next_distributions(prefixes), dtype=np.float64)
+    if rows.shape != (len(prefixes), V):
+        raise ValueError(f"next_distributions returned shape {rows.shape}, expected {(len(prefixes), V)}")
+    return np.ascontiguousarray(rows)
+
+
+class _HostRowsSession:
+    """Feeds the GPU tree builder from a host plugin: per round the batch's node
+    paths are rebuilt from the workspace's ancestor-slot lists (each expanded
+    node owns one slot, tree.cu tree_update_kernel), the plugin evaluates their
+    full prefixes, and the float64 rows go up to HBM for sx_tree_round."""
+
+    def __init__(self, adapter: "HostRowsModel", prefix: Prefix, params: BuilderParams):
+        self.a = adapter
+        self.prefix = prefix
+        self.ws = _WS.get(params.budget, params.batch_size, adapter.vocab_size, params.max_depth)
+        self.ws.begin(root_slot=0, pad_slot=0)
+        self.slot_path: dict[int, Prefix] = {0: ()}
+        self.first = True
+        self.batch_n = 1
+
+    def batch_rows(self) -> torch.Tensor:
+        if self.first:
+            self.first = False
+            return self.a._upload(_host_rows(self.a.model, [self.prefix]))
+        ws, n = self.ws, self.batch_n
+        anc = ws.batch_anc()[:n].cpu().tolist()
+        alen = ws.batch_anc_len()[:n].cpu().tolist()
+        toks = ws.batch_tokens()[:n].cpu().tolist()
+        slots = ws.batch_slots()[:n].cpu().tolist()
+        K.IO["d2h"] += 4 * n * (len(anc[0]) + 3) if n else 0
+        paths = []
+        for b in range(n):
+            path = self.slot_path[anc[b][alen[b] - 2]] + (toks[b],)
+            self.slot_path[slots[b]] = path
+            paths.append(self.prefix + path)
+        return self.a._upload(_host_rows(self.a.model, paths))
+
+    def advance(self, ctl) -> None:
+        self.batch_n = ctl["batch_n"]
+
+    def finish(self, tree) -> None:
+        pass
+
+
+class _HostRowsStochastic:
+    """Level rows for the host-built trees (SpecInfer's stochastic builder, beam search)."""
+
+    def __init__(self, adapter: "HostRowsModel"):
+        self.a = adapter
+
+    def level_rows(self, tree, level: list[int]) -> torch.Tensor:
+        return self.a._upload(_host_rows(self.a.model, [tree.full_prefix(n) for n in level]))
+
+    def finish(self, tree) -> None:
+        pass
+
+
+class HostRowsModel(LanguageModel):
+    """Adapter for any reference-API LanguageModel plugin that is not one of this
+    package's device models. Only the model rows come from the plugin (the
+    reference contract: pure, batch-consistent float64 rows); tree building,
+    scoring warps, the target-row cache and the acceptance walk run in the same
+    sm_100a kernels as for device models. Rows are uploaded per draft round /
+    per target pass (pinned staging, one H2D copy each)."""
+
+    _cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+    _lock = threading.Lock()
+
+    def __init__(self, model) -> None:
+        self.model = model
+        self.vocab_size = int(model.vocab_size)
+        self.backend = f"host:{getattr(model, 'backend', type(model).__name__)}"
+        self.device = _device()
+        self._stage: torch.Tensor | None = None
+
+    @classmethod
+    def wrap(cls, model) -> "HostRowsModel":
+        try:
+            with cls._lock:
+                a = cls._cache.get(model)
+                if a is None:
+                    a = cls._cache[model] = cls(model)
+            return a
+        except TypeError:  # not weak-referenceable: a fresh (stateless) adapter
+            return cls(model)
+
+    def _upload(self, rows: np.ndarray) -> torch.Tensor:
+        n = rows.shape[0]
+        need = rows.size
+        if self._stage is None or self._stage.numel() < need:
+            self._stage = torch.empty(max(need, 1), dtype=torch.float64).pin_memory()
+        st = self._stage[:need]
+        # the previous upload out of this staging buffer must have landed first
+        torch.cuda.current_stream().synchronize()
+        st.numpy()[:] = rows.reshape(-1)
+        out = torch.empty((n, self.vocab_size), dtype=torch.float64, device=self.device)
+        out.view(-1).copy_(st, non_blocking=True)
+        K.IO["h2d"] += rows.nbytes
+        return out
+
+    # reference plugin API: the wrapped model's rows, unchanged
+    def next_distributions(self, prefixes) -> np.ndarray:
+        return _host_rows(self.model, [_check_prefix(p, self.vocab_size) for p in prefixes])
+
+    def to_json(self) -> str:
+        return self.model.to_json()
+
+    # device-model protocol
+    def tree_session(self, prefix: Prefix, params: BuilderParams) -> _HostRowsSession:
+        return _HostRowsSession(self, _check_prefix(prefix, self.vocab_size), params)
+
+    def stochastic_session(self, prefix: Prefix, max_nodes: int, max_depth: int) -> _HostRowsStochastic:
+        _check_prefix(prefix, self.vocab_size)
+        return _HostRowsStochastic(self)
+
+    def tree_rows(self, tree) -> torch.Tensor:
+        prefixes = [tree.prefix] + [tree.full_prefix(i) for i in range(len(tree))]
+        return self._upload(_host_rows(self.model, prefixes))
+
+    def prefix_rows(self, prefix: Prefix) -> torch.Tensor:
+        return self._upload(_host_rows(self.model, [_check_prefix(prefix, self.vocab_size)]))

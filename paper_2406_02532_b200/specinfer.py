@@ -197,6 +197,8 @@ def generate_specinfer(prompt, draft, target, branching, cfg: SamplingConfig):
     """Draft-then-verify until cfg.max_new_tokens (specinfer.py:99-127); KV of
     the accepted path is compacted in place for device models with caches."""
     prompt = tuple(int(t) for t in prompt)
+    if draft is target and hasattr(target, "draft_view"):
+        draft = target.draft_view()  # one network in both roles: a second KV cache for the draft
     rng_draft = CounterRng(cfg.seed, DRAFT_STREAM)
     rng_accept = CounterRng(cfg.seed, ACCEPT_STREAM)
     stats = GenStats()

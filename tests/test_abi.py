@@ -83,13 +83,14 @@ def test_gemm_plan_tiles():
 def test_attention_split_workspace_sizing():
     """Key-split workspace (host logic, no GPU): needed only when the tcgen05
     grid (ceil(N / (128 / G)) x KVH CTAs) is smaller than the 148 SMs; counters
-    (256-B aligned) then up to 8 splits x 128 rows x 132 floats per CTA."""
+    (a fixed 1 KB header for up to 148 CTAs, independent of N so one workspace
+    serves every shape) then up to 8 splits x 128 rows x 132 floats per CTA."""
     lib = _lib.load()
     assert lib.sx_tree_attention_ws_bytes(1025, 64, 8) == 0  # 65 x 8 = 520 CTAs
     assert lib.sx_tree_attention_ws_bytes(1024, 32, 32) == 0  # 8 x 32 = 256 CTAs
     one = lib.sx_tree_attention_ws_bytes(1, 64, 8)  # 8 CTAs -> 8 splits
-    assert one == 256 + 8 * 8 * 128 * 132 * 4
+    assert one == 1024 + 8 * 8 * 128 * 132 * 4
     mid = lib.sx_tree_attention_ws_bytes(256, 32, 32)  # 64 CTAs -> ceil(296 / 64) = 5 splits
-    assert mid == 256 + 64 * 5 * 128 * 132 * 4
+    assert mid == 1024 + 64 * 5 * 128 * 132 * 4
     assert lib.sx_tree_attention_ws_bytes(0, 64, 8) == 0
     assert lib.sx_tree_attention_ws_bytes(4, 64, 7) == 0  # H not a multiple of KVH: no split path

@@ -1,8 +1,15 @@
 """Logit parity at the named architectures (SURVEY 8(d) shapes at real width):
 2-layer truncations of Llama-2-7B / Llama-2-70B / Llama-3-8B / Llama-3-70B
 (the first two decoder layers of the seeded full models -- same draw order),
-bf16 weights, against the fp32 CPU oracle (oracle/llama_ref.py) on the same
-weights, within the north_star bf16 tolerance 2e-2 abs:
+bf16 weights, against the CPU oracle (oracle/llama_ref.py) on the same weights.
+
+At these widths the bf16 activation policy itself moves logits by 0.03-0.09
+abs away from an all-fp32 forward (N(0, 0.02) init: logit std ~1.3 at d=4096,
+measured by the oracle's two policies), so the north_star's "2e-2 abs in bf16"
+is checked against the oracle run under the same bf16 policy (activations
+rounded to bf16 where the GPU stores them), and the GPU's distance to the fp32
+forward must not exceed the policy's own (plus 5e-3). The all-fp32 tolerance
+(1e-4) is the fp32 target mode's (tests/test_fp32_mode_gpu.py). Rows checked:
 
 * prefill rows (causal chain through the prefix cache) of draft and target;
 * every draft row of a K=1024, B=1024 GPU tree build (the batched tree rounds
@@ -56,15 +63,23 @@ def _max_err(got: torch.Tensor, exp: torch.Tensor) -> float:
     return float((got.float().cpu() - exp).abs().max())
 
 
+def check(got, cpu_fn, what):
+    """got vs the bf16-policy oracle (< TOL) and vs fp32 (no worse than the policy)."""
+    ref16, ref32 = cpu_fn("bf16"), cpu_fn("fp32")
+    e16, e32, pol = _max_err(got, ref16), _max_err(got, ref32), _max_err(ref16, ref32)
+    print(f"{what}: |gpu - bf16 policy| {e16:.4g}  |gpu - fp32| {e32:.4g}  |bf16 policy - fp32| {pol:.4g}")
+    assert e16 < TOL, (what, e16)
+    assert e32 <= pol + 5e-3, (what, e32, pol)
+
+
 def test_prefill_rows(named_pair):
     for m in named_pair:
         prompt = _prompt(m.cfg.vocab, 11)
         W = m.w.to_cpu_fp32()
-        exp = llama_ref.forward_logits(m.cfg, W, prompt)
+        exp = {pol: llama_ref.forward_logits(m.cfg, W, prompt, policy=pol) for pol in ("bf16", "fp32")}
         for n in (1, 37, P):
             got = m.prefix_rows(prompt[:n])[0]
-            err = _max_err(got, exp[n - 1])
-            assert err < TOL, (m.cfg.name, n, err)
+            check(got, lambda pol: exp[pol][n - 1], f"{m.cfg.name} prefill n={n}")
 
 
 def test_tree_build_and_target_pass_rows(named_pair):
@@ -79,14 +94,14 @@ def test_tree_build_and_target_pass_rows(named_pair):
     assert len(tree.nodes) == K
     # every draft row the builder consumed (root + each expanded node)
     paths = sorted((k[P:] for k in rec if len(k) > P), key=len)
-    exp_d = llama_ref.forward_tree_logits(draft.cfg, draft.w.to_cpu_fp32(), prompt, paths)
+    Wd = draft.w.to_cpu_fp32()
     got_d = torch.stack([torch.from_numpy(rec[tuple(prompt)])] + [torch.from_numpy(rec[tuple(prompt) + p]) for p in paths])
-    err_d = _max_err(got_d, exp_d)
-    assert err_d < TOL, ("draft rows", len(paths), err_d)
+    check(got_d, lambda pol: llama_ref.forward_tree_logits(draft.cfg, Wd, prompt, paths, policy=pol),
+          f"{draft.cfg.name} draft rows ({len(paths) + 1})")
     # the target's one pass over anchor + every node
     rows = target.tree_rows(tree)
     assert rows.shape == (K + 1, target.cfg.vocab)
     tpaths = [tree.path_tokens(i) for i in range(K)]
-    exp_t = llama_ref.forward_tree_logits(target.cfg, target.w.to_cpu_fp32(), prompt, tpaths)
-    err_t = _max_err(rows, exp_t)
-    assert err_t < TOL, ("target rows", err_t)
+    Wt = target.w.to_cpu_fp32()
+    check(rows, lambda pol: llama_ref.forward_tree_logits(target.cfg, Wt, prompt, tpaths, policy=pol),
+          f"{target.cfg.name} tree pass rows ({K + 1})")
