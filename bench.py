@@ -71,6 +71,7 @@ def parse():
                     help="scale of the shared synthetic prev-token logit bias (0 = pure random init)")
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 legs (demo pair + tiny Llama end to end)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sequential", action="store_true", help="skip the sequential-decoding speed-up denominator")
     ap.add_argument("--offload-buffers", type=int, default=8,
@@ -218,86 +219,289 @@ def ncu_traffic(prefix: str = "gemm_tc_kernel<2") -> tuple[float | None, str]:
     return best if best else (None, "no ncu capture committed")
 
 
-# ----------------------------------------------------------------------------- CPU baseline
-def cpu_baseline(args, w, accepted_per_iter: float, rounds_per_iter: float, tree_nodes: int, ctx: int) -> dict:
-    """The oracle port timed on this host: one fp32 decoder layer of the target
-    at N = K+1 tree tokens and one of the draft at B tokens (oracle/llama_ref.py
-    arithmetic, all host threads), extrapolated to the full depth, plus the
-    oracle's tree bookkeeping (oracle build_sssp over synthetic rows of the same
-    V/K/B). tokens/s = accepted tokens per iteration / CPU seconds per iteration."""
-    import torch
+# ----------------------------------------------------------------------------- CPU reference path
+ACCEPT_FILE = ROOT / "profiles" / "accept_by_workload.json"
 
-    from oracle import llama_ref
-    from oracle import speckit_oracle as ox
+
+def bench_config(args, K: int, B: int, scoring: str) -> dict:
+    """`config` of the JSON line -- identical in both arms (the same workload)."""
+    dname, tname = WORKLOADS[args.workload][:2]
     from paper_2406_02532_b200.llama import PRESETS
 
-    threads = os.cpu_count() or 1
-    torch.set_num_threads(threads)
-    dname, tname, K, D, B = w[0], w[1], w[2], w[3], w[4]
+    tb = PRESETS[tname].weight_bytes() + PRESETS[dname].weight_bytes()
+    cfg = {"workload": workload_desc(args.workload, K, B), "scoring": scoring, "prompt_len": args.prompt_len,
+           "l2": (f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)" if tb > 1e9
+                  else f"weights {tb / 1e6:.0f} MB: L2-resident across steps (demo size, not a bench line)")}
+    if args.workload in OFFLOAD:
+        cfg["offload_buffers"] = args.offload_buffers
+    return cfg
 
-    def layer_seconds(cfg, n_tok, n_ctx):
+
+def recorded_acceptance(workload: str) -> tuple[float, float, str]:
+    """(accepted tokens / iteration, draft calls / iteration, source) of the GPU
+    arm on the same workload and seeds, from the committed record (the driver
+    runs the reference arm first, so it cannot read the GPU arm's live value)."""
+    try:
+        rec = json.loads(ACCEPT_FILE.read_text())[workload]
+        return rec["accepted_tokens_per_iter"], rec["draft_calls_per_iter"], f"{ACCEPT_FILE.name}: {rec['source']}"
+    except (OSError, KeyError, ValueError):
+        return 1.0, 2.0, "no recorded GPU acceptance for this workload: 1.0 assumed"
+
+
+class CpuIterationSampler:
+    """The reference's CPU path for one target iteration, timed on this host
+    (SURVEY 8(d)): every piece that runs is measured, none is assumed.
+
+    Per sample: one fp32 decoder layer of the target over the K+1 tree tokens
+    (queries) against prompt + tree keys under the tree's ancestor mask, the
+    target LM head over those K+1 rows, one draft decoder layer over a batch of
+    B rows and the draft LM head (the batched round), the draft's one-token root
+    round (layer + head), the reference tree bookkeeping -- oracle build_sssp
+    (the restatement of pkg/src/speckit/tree.py:240-327, pinned to the
+    reference's fixtures) at the workload's K, D, B, V on logits rows -- and the
+    walk (apply_warp + sample + advance, engine.py:118-128) for the accepted
+    tokens. The iteration time is L_target x layer + head + draft (root +
+    (rounds - 1) x (L_draft x layer + head)) + tree + walk; only the layer count
+    is extrapolated (every layer has the same shapes). Weights are fp32 N(0,
+    0.02), allocated once outside the timed sample."""
+
+    def __init__(self, workload: str, K: int, B: int, prompt_len: int, threads: int):
+        import numpy as np
+        import torch
+
+        from oracle import llama_ref
+        from paper_2406_02532_b200.llama import PRESETS
+
+        self.torch, self.np, self.ref = torch, np, llama_ref
+        torch.set_num_threads(threads)
+        self.threads = threads
+        w = WORKLOADS[workload]
+        self.dcfg, self.tcfg = PRESETS[w[0]], PRESETS[w[1]]
+        self.K, self.D, self.B, self.temp, self.top_p = K, w[3], B, w[5], w[6]
+        self.ctx = prompt_len
         g = torch.Generator().manual_seed(0)
-        d, H, KVH, hd = cfg.d, cfg.heads, cfg.kv_heads, cfg.head_dim
-        L = {"wqkv": torch.randn(cfg.qkv_out, d, generator=g) * 0.02, "wo": torch.randn(d, H * hd, generator=g) * 0.02,
-             "wg": torch.randn(cfg.ff, d, generator=g) * 0.02, "wu": torch.randn(cfg.ff, d, generator=g) * 0.02,
-             "wd": torch.randn(d, cfg.ff, generator=g) * 0.02, "n1": torch.ones(d), "n2": torch.ones(d)}
-        x = torch.randn(n_tok, d, generator=g)
-        kctx = torch.randn(n_ctx, KVH, hd, generator=g)
+        self.Wt = self._layer(self.tcfg, g)
+        self.Wd = self._layer(self.dcfg, g)
+        self.lm_t = torch.randn(self.tcfg.vocab, self.tcfg.d, generator=g) * 0.02
+        self.lm_d = torch.randn(self.dcfg.vocab, self.dcfg.d, generator=g) * 0.02
+        # a random tree of K nodes (depth <= D) for the target pass mask
+        rng = np.random.default_rng(0)
+        depth, parent = [0], [-1]
+        for i in range(1, K + 1):
+            cand = int(rng.integers(max(0, i - 64), i))
+            while depth[cand] >= self.D:
+                cand = parent[cand]
+            parent.append(cand)
+            depth.append(depth[cand] + 1)
+        self.t_mask, self.t_pos = self._tree_mask(parent, depth)
+        self.d_mask, self.d_pos = self._tree_mask(parent[: B], depth[: B])
+
+    @staticmethod
+    def _layer(cfg, g):
+        import torch
+
+        r = lambda *s: torch.randn(*s, generator=g) * 0.02  # noqa: E731
+        return {"wqkv": r(cfg.qkv_out, cfg.d), "wo": r(cfg.d, cfg.heads * cfg.head_dim), "wg": r(cfg.ff, cfg.d),
+                "wu": r(cfg.ff, cfg.d), "wd": r(cfg.d, cfg.ff), "n1": torch.ones(cfg.d), "n2": torch.ones(cfg.d)}
+
+    def _tree_mask(self, parent, depth):
+        torch = self.torch
+        n = len(parent)
+        allow = torch.zeros((n, self.ctx + n), dtype=torch.bool)
+        allow[:, : self.ctx] = True
+        for i in range(n):
+            if parent[i] >= 0:
+                allow[i, self.ctx : self.ctx + n] = allow[parent[i], self.ctx : self.ctx + n]
+            allow[i, self.ctx + i] = True
+        mask = torch.zeros(allow.shape).masked_fill(~allow, float("-inf"))
+        return mask, torch.tensor([self.ctx - 1 + d for d in depth])
+
+    def _layer_time(self, cfg, L, n, mask, pos) -> float:
+        torch, ref = self.torch, self.ref
+        H, KVH, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
+        g = torch.Generator().manual_seed(1)
+        x = torch.randn(n, cfg.d, generator=g)
+        kv_ctx = torch.randn(self.ctx, KVH, hd, generator=g)
         t0 = time.perf_counter()
         with torch.no_grad():
-            h = llama_ref.rmsnorm(x, L["n1"], cfg.eps)
+            h = ref.rmsnorm(x, L["n1"], cfg.eps)
             qkv = h @ L["wqkv"].t()
-            q = qkv[:, : H * hd].view(n_tok, H, hd)
-            k = kctx.repeat_interleave(H // KVH, dim=1)
-            s = torch.einsum("qhd,khd->hqk", q, k) / hd**0.5
-            att = torch.einsum("hqk,khd->qhd", s.softmax(-1), k).reshape(n_tok, H * hd)
+            q = ref.rope(qkv[:, : H * hd].view(n, H, hd), pos, cfg.rope_theta)
+            k = ref.rope(qkv[:, H * hd : (H + KVH) * hd].view(n, KVH, hd), pos, cfg.rope_theta)
+            v = qkv[:, (H + KVH) * hd :].view(n, KVH, hd)
+            k = torch.cat([kv_ctx, k]).repeat_interleave(H // KVH, dim=1)
+            v = torch.cat([kv_ctx, v]).repeat_interleave(H // KVH, dim=1)
+            s = torch.einsum("qhd,khd->hqk", q, k) / hd**0.5 + mask
+            att = torch.einsum("hqk,khd->qhd", s.softmax(-1), v).reshape(n, H * hd)
             x = x + att @ L["wo"].t()
-            h = llama_ref.rmsnorm(x, L["n2"], cfg.eps)
+            h = ref.rmsnorm(x, L["n2"], cfg.eps)
             x = x + (torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
         return time.perf_counter() - t0
 
-    tcfg, dcfg = PRESETS[tname], PRESETS[dname]
-    t_layer = layer_seconds(tcfg, tree_nodes + 1, ctx + tree_nodes + 1)
-    d_layer = layer_seconds(dcfg, B, ctx + 64)
-    # LM heads: one GEMM each
-    t_head = 2.0 * (tree_nodes + 1) * tcfg.d * tcfg.vocab / 0.7e12
-    t0 = time.perf_counter()
-    lm = ox.LogitsLM(tcfg.vocab, ox.hashed_logits_fn(tcfg.vocab, 11, 1.3))
-    ox.build_sssp(tuple(range(8)), lm, ox.BuilderParams(K, D, B))
-    t_tree = time.perf_counter() - t0
-    per_iter = t_layer * tcfg.layers + t_head + rounds_per_iter * d_layer * dcfg.layers + t_tree
-    value = accepted_per_iter / per_iter
-    return {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": (f"one fp32 {tname} layer at N={tree_nodes + 1} ({t_layer:.2f}s) x {tcfg.layers} + LM head, "
-                       f"one fp32 {dname} layer at B={B} ({d_layer:.2f}s) x {dcfg.layers} x {rounds_per_iter:.1f} rounds, "
-                       f"oracle build_sssp K={K} V={tcfg.vocab} ({t_tree:.2f}s); extrapolated "
-                       f"{per_iter:.1f} s/iteration at {accepted_per_iter:.2f} accepted tokens/iteration"),
-            "seconds_per_iteration": per_iter}
+    def _head_time(self, lm, n, d) -> float:
+        torch = self.torch
+        h = torch.randn(n, d)
+        t0 = time.perf_counter()
+        with torch.no_grad():
+            z = h @ lm.t()
+            z.max(dim=1)
+        return time.perf_counter() - t0
+
+    def sample(self, accepted: float, rounds: float) -> dict:
+        from oracle import speckit_oracle as ox
+
+        torch = self.torch
+        tc, dc, K, B = self.tcfg, self.dcfg, self.K, self.B
+        t_wall = time.perf_counter()
+        t_layer = self._layer_time(tc, self.Wt, K + 1, self.t_mask, self.t_pos)
+        t_head = self._head_time(self.lm_t, K + 1, tc.d)
+        d_layer = self._layer_time(dc, self.Wd, B, self.d_mask, self.d_pos)
+        d_head = self._head_time(self.lm_d, B, dc.d)
+        root_mask = torch.zeros((1, self.ctx + 1))
+        d_root = self._layer_time(dc, self.Wd, 1, root_mask, torch.tensor([self.ctx - 1])) * dc.layers \
+            + self._head_time(self.lm_d, 1, dc.d)
+        t0 = time.perf_counter()
+        lm = ox.LogitsLM(tc.vocab, ox.hashed_logits_fn(tc.vocab, 11, 1.3))
+        warp = ox.SamplingConfig(self.temp, self.top_p) if self.temp > 0 else None
+        tree = ox.build_sssp(tuple(range(8)), lm, ox.BuilderParams(K, self.D, B), warp, warp_scores=warp is not None)
+        t_tree = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rng = ox.CounterRng(0, "generation")
+        row = lm.next_distributions([tuple(range(9))])[0]
+        cfg = ox.SamplingConfig(self.temp, self.top_p, seed=0)
+        for _ in range(max(1, int(round(accepted)))):
+            ox.sample(ox.apply_warp(row, cfg), rng)
+            tree.child_with_token(-1, 0)
+        t_walk = time.perf_counter() - t0
+        per_iter = (t_layer * tc.layers + t_head + d_root + max(0.0, rounds - 1) * (d_layer * dc.layers + d_head)
+                    + t_tree + t_walk)
+        return {"seconds_per_iteration": per_iter, "sample_seconds": time.perf_counter() - t_wall,
+                "parts_s": {"target_layer": t_layer, "target_lm_head": t_head, "draft_layer_batch": d_layer,
+                            "draft_lm_head_batch": d_head, "draft_root_round": d_root, "tree_bookkeeping": t_tree,
+                            "walk": t_walk}}
+
+    def describe(self, accepted: float, rounds: float, src: str) -> str:
+        tc, dc = self.tcfg, self.dcfg
+        return (f"measured per sample: one fp32 {tc.name} layer over K+1={self.K + 1} tree queries (ctx "
+                f"{self.ctx}, tree mask) + its LM head, one {dc.name} layer at B={self.B} + LM head, the draft root "
+                f"round, oracle build_sssp K={self.K} D={self.D} B={self.B} V={tc.vocab}, the walk; layers x "
+                f"{tc.layers} / {dc.layers}, {rounds:.1f} draft calls and {accepted:.2f} accepted tokens per iteration "
+                f"({src}); {self.threads} threads")
+
+
+def c1_legs(gpu: bool, threads: int) -> dict:
+    """BASELINE configs[0] (C1) end to end: the reference demo pair
+    (pkg/demos/03_cached_generation.py:19-20: make_synthetic(3, 16, 0.05), draft =
+    power_smoothed(0.7)) and a tiny Llama pair (tiny-draft -> tiny, weights drawn
+    on the host so both arms use the same values), one 128-token prompt, K=128,
+    D=16, B=8, t=0 (the Llama pair with raw draft scoring). gpu=False:
+    through the CPU reference path (oracle engine; CpuLlamaLM = fp32 TorchCpuLlama
+    plugin); gpu=True: through this package's public API on cuda:0."""
+    import hashlib
+
+    import numpy as np
+
+    def leg(fn, n_tok):
+        t0 = time.perf_counter()
+        toks, stats = fn()
+        if gpu:
+            import torch
+
+            torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        return {"tokens_per_s": len(toks) / el, "tokens": len(toks), "seconds": el,
+                "accepted_per_iter": stats.generation_rate,
+                "tokens_sha1": hashlib.sha1(json.dumps(list(toks)).encode()).hexdigest()[:12]}
+
+    out = {}
+    rng = np.random.default_rng(1000)
+    demo_prompt = tuple(int(t) for t in rng.integers(0, 16, size=128))
+    llama_prompt = tuple(int(t) for t in rng.integers(0, 32000, size=128))
+    if gpu:
+        import paper_2406_02532_b200 as sx
+        from paper_2406_02532_b200.llama import LlamaModel
+
+        tgt = sx.make_synthetic(3, 16, 0.05)
+        drf = tgt.power_smoothed(0.7)
+        cfg = sx.SamplingConfig(0.0, 1.0, seed=0, max_new_tokens=256)
+        sx.generate_specexec(demo_prompt, drf, tgt, sx.BuilderParams(128, 16, 8), cfg)  # warm
+        out["demo03"] = leg(lambda: sx.generate_specexec(demo_prompt, drf, tgt, sx.BuilderParams(128, 16, 8), cfg), 256)
+        lt = LlamaModel("tiny", seed=1, max_ctx=2048, max_tokens=256, init="host")
+        ld = LlamaModel("tiny-draft", seed=2, max_ctx=4096, max_tokens=256, init="host")
+        cfg = sx.SamplingConfig(0.0, 1.0, seed=0, max_new_tokens=8)
+        sx.generate_specexec(llama_prompt, ld, lt, sx.BuilderParams(128, 16, 8), cfg, warp_scores=False)  # warm
+        cfg = sx.SamplingConfig(0.0, 1.0, seed=0, max_new_tokens=16)
+        out["tiny_llama"] = leg(lambda: sx.generate_specexec(llama_prompt, ld, lt, sx.BuilderParams(128, 16, 8), cfg,
+                                                             warp_scores=False), 16)
+        del lt, ld
+    else:
+        import torch
+
+        from oracle import llama_ref
+        from oracle import speckit_oracle as ox
+        from paper_2406_02532_b200.llama import PRESETS, host_weights_fp32
+
+        torch.set_num_threads(threads)
+        tgt = ox.make_synthetic(3, 16, 0.05)
+        drf = tgt.power_smoothed(0.7)
+        cfg = ox.SamplingConfig(0.0, 1.0, seed=0, max_new_tokens=256)
+        out["demo03"] = leg(lambda: ox.generate_specexec(demo_prompt, drf, tgt, ox.BuilderParams(128, 16, 8), cfg), 256)
+        lt = llama_ref.CpuLlamaLM(PRESETS["tiny"], host_weights_fp32(PRESETS["tiny"], 1))
+        ld = llama_ref.CpuLlamaLM(PRESETS["tiny-draft"], host_weights_fp32(PRESETS["tiny-draft"], 2))
+        cfg = ox.SamplingConfig(0.0, 1.0, seed=0, max_new_tokens=16)
+        out["tiny_llama"] = leg(lambda: ox.generate_specexec(llama_prompt, ld, lt, ox.BuilderParams(128, 16, 8), cfg,
+                                                             warp_scores=False), 16)
+    out["config"] = "C1: demo03 pair V=16 and tiny Llama pair (d=256, V=32000), 128-token prompt, K=128 D=16 B=8 t=0"
+    return out
+
+
+def cpu_baseline(args, K: int, B: int, accepted: float, rounds: float, src: str) -> dict:
+    """The CPU reference path beside the GPU run (rank 0, N=1): one bounded sample."""
+    threads = os.cpu_count() or 1
+    sampler = CpuIterationSampler(args.workload, K, B, args.prompt_len, threads)
+    smp = sampler.sample(accepted, rounds)
+    return {"value": accepted / smp["seconds_per_iteration"], "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": sampler.describe(accepted, rounds, src), "seconds_per_iteration": smp["seconds_per_iteration"],
+            "parts_s": smp["parts_s"], "sample_seconds": smp["sample_seconds"], "extrapolated": "layer count only"}
 
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """`--impl reference`: the reference's CPU implementation of the path timed on
+    this box's host cores (the oracle port: the reference is pure Python and
+    cannot travel; its restatement is pinned to its fixtures). Rank 0 only."""
     world, rank, local = dist_env()
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
     K = args.budget or w[2]
     B = args.batch or w[4]
-    steps = []
-    cb = None
+    scoring = args.scoring or ("raw" if w[5] == 0.0 else "warped")
+    threads = os.cpu_count() or 1
+    accepted, rounds, src = recorded_acceptance(args.workload)
+    sampler = CpuIterationSampler(args.workload, K, B, args.prompt_len, threads)
+    per_iter, walls, parts = [], [], None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(args, (w[0], w[1], K, w[3], B), 1.0, max(1.0, K / B + 1), K, args.prompt_len)
+        smp = sampler.sample(accepted, rounds)
         if i >= args.warmup:
-            steps.append(cb["seconds_per_iteration"])
-    sec = statistics.mean(steps)
-    value = 1.0 / sec
-    cb["value"] = value
+            per_iter.append(smp["seconds_per_iteration"])
+            walls.append(smp["sample_seconds"])
+            parts = smp["parts_s"]
+    sec = statistics.mean(per_iter)
+    value = accepted / sec
+    c1 = c1_legs(gpu=False, threads=threads) if not args.no_c1 else None
+    cb = {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+          "sample": sampler.describe(accepted, rounds, src), "seconds_per_iteration": sec, "parts_s": parts,
+          "extrapolated": "layer count only"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_desc(args.workload, K, B),
-                       "note": "CPU oracle port (extrapolated per-layer timing; 1 accepted token/iteration assumed)"},
-            "cpu_baseline": cb, "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": bench_config(args, K, B, scoring),
+            "step": "one measured CPU sample of a target iteration (ms_per_step = its wall time); value = "
+                    "accepted tokens / the iteration time assembled from the sample",
+            "accepted_tokens_per_iter": accepted, "draft_calls_per_iter": rounds,
+            "cpu_baseline": cb, "c1": c1,
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
@@ -488,10 +692,12 @@ def main():
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(args, (dname, tname, K, D, B), accepted_per_iter, draft_calls / max(1, iters), K,
-                          args.prompt_len)
+        cb = cpu_baseline(args, K, B, accepted_per_iter, draft_calls / max(1, iters),
+                          f"live: this run's {args.steps} timed iterations")
+    c1 = None
+    if rank == 0 and world == 1 and not args.no_c1:
+        c1 = c1_legs(gpu=True, threads=os.cpu_count() or 1)
     if rank == 0:
-        tb = PRESETS[tname].weight_bytes() + PRESETS[dname].weight_bytes()
         line = {
             "metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -500,12 +706,9 @@ def main():
             "dtype": "bf16",
             "data": "synthetic: random-init weights (N(0,0.02)), random 128-token prompt" +
                     (f", shared synthetic prev-token bias scale {args.synthetic}" if syn else ""),
-            "config": {"workload": workload_desc(args.workload, K, B), "scoring": scoring,
-                       "parallelism": (f"tp{world} target ({'fused GEMM reduce-scatter over peer memory' if target.tp_fused else 'NCCL all-reduce'}, {args.reduce}), draft replicated"
-                                       if tp else f"replicas x{world}") if world > 1 else "1 GPU",
-                       "l2": f"weights {tb / 1e9:.0f} GB >> 126 MB L2, streamed every step (no flush needed)",
-                       "prompt_len": args.prompt_len,
-                       **({"offload_buffers": target.streamer.nbuf} if offload else {})},
+            "config": bench_config(args, K, B, scoring),
+            "parallelism": (f"tp{world} target ({'fused GEMM reduce-scatter over peer memory' if target.tp_fused else 'NCCL all-reduce'}, {args.reduce}), draft replicated"
+                            if tp else f"replicas x{world}") if world > 1 else "1 GPU",
             "accepted_tokens_per_iter": accepted_per_iter,
             "draft_calls_per_iter": draft_calls / max(1, iters),
             "stage_ms_per_step": stages,
@@ -513,6 +716,7 @@ def main():
             "gemm_shapes": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in gemm_shapes],
             "roofline": roof,
             "cpu_baseline": cb,
+            "c1": c1,
             "e2e": e2e,
             "sequential": seq,
             "gpu_launches": launches,
