@@ -241,6 +241,30 @@ SX_API int sx_stream_copy(void* dst, const void* src, long long bytes, int to_de
 SX_API int sx_kv_compact(void* kcache, void* vcache, int layers, long long layer_stride, long long slots, int KVH,
                          const int* src, const int* dst, int n, cudaStream_t stream);
 
+/* ------------------------------------------------ fp32 target mode (csrc/fp32_path.cu)
+ * The same forward with fp32 weights, activations, KV cache and CUDA-core FFMA
+ * accumulation (north_star: target logits within 1e-4 of the fp32 reference).
+ * Semantics as the bf16 entry points above; all pointers fp32.
+ *   sx_gemm_f32        out[t, f] (op)= sum_k x[t, k] w[f, k]; epi SX_EPI_F32 / SX_EPI_ADD_F32 /
+ *                      SX_EPI_SWIGLU_IL (out [M, N/2]); K a multiple of 4, 16-byte aligned operands
+ *   sx_tree_attention_f32  key set as sx_tree_attention (H / KVH <= 32)
+ *   sx_add_rmsnorm_f32 x += y (y NULL: none), out = x * rsqrt(mean(x^2) + eps) * w (w NULL: add only)
+ *   sx_kv_compact_f32  as sx_kv_compact on an fp32 cache (n <= 224)
+ */
+SX_API int sx_gemm_f32(const float* w, const float* x, float* out, int M, int N, int K, long long ldo, int epi,
+                       cudaStream_t stream);
+SX_API int sx_tree_attention_f32(const float* q, const float* kcache, const float* vcache, long long slots,
+                                 const int* dense_len, int dense_const, const int* anc, int anc_base,
+                                 const int* anc_len, int A, float* out, int N, int H, int KVH, cudaStream_t stream);
+SX_API int sx_embed_f32(const float* E, const int* tokens, int n, int d, float* x, cudaStream_t stream);
+SX_API int sx_add_rmsnorm_f32(float* x, const float* y, const float* w, int n, int d, float eps, float* out,
+                              cudaStream_t stream);
+SX_API int sx_rope_kv_f32(const float* qkv, const int* pos, int pos_base, const int* slot, int slot_base, int n,
+                          int H, int KVH, const float* cos_t, const float* sin_t, float* q, float* kcache,
+                          float* vcache, long long slots, cudaStream_t stream);
+SX_API int sx_kv_compact_f32(void* kcache, void* vcache, int layers, long long layer_stride, long long slots,
+                             int KVH, const int* src, const int* dst, int n, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,19 @@ SIGNATURES: dict[str, tuple] = {
     "sx_attention_set_impl": (_c_int, [_c_int]),
     "sx_stream_copy": (_c_int, [_vp, _vp, _c_ll, _c_int, _vp, _vp, _vp]),
     "sx_kv_compact": (_c_int, [_vp, _vp, _c_int, _c_ll, _c_ll, _c_int, _vp, _vp, _c_int, _vp]),
+    # fp32 target mode
+    "sx_gemm_f32": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_ll, _c_int, _vp]),
+    "sx_tree_attention_f32": (
+        _c_int,
+        [_vp, _vp, _vp, _c_ll, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp],
+    ),
+    "sx_embed_f32": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
+    "sx_add_rmsnorm_f32": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, ctypes.c_float, _vp, _vp]),
+    "sx_rope_kv_f32": (
+        _c_int,
+        [_vp, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_ll, _vp],
+    ),
+    "sx_kv_compact_f32": (_c_int, [_vp, _vp, _c_int, _c_ll, _c_ll, _c_int, _vp, _vp, _c_int, _vp]),
 }
 
 ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1

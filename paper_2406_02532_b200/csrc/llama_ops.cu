@@ -146,24 +146,47 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, const int*
 }
 
 // Move KV rows src_slot[i] -> dst_slot[i] for all layers / kv heads. Rows are
-// staged in shared memory first, so overlapping source/destination ranges are safe.
-__global__ void kv_compact_kernel(__nv_bfloat16* kc, __nv_bfloat16* vc, long long layer_stride, long long slots,
-                                  int KVH, const int* __restrict__ src, const int* __restrict__ dst, int n) {
-  extern __shared__ __align__(16) uint4 stage[];  // [2][n][16] uint4 (128 bf16 = 16 x uint4)
+// staged in shared memory first, so overlapping source/destination ranges are
+// safe. A row is 128 elements: row_u4 = 16 uint4 (bf16) or 32 (fp32 mode).
+__global__ void kv_compact_kernel(uint8_t* kc, uint8_t* vc, long long layer_stride_bytes, long long slots, int KVH,
+                                  int row_u4, const int* __restrict__ src, const int* __restrict__ dst, int n) {
+  extern __shared__ __align__(16) uint4 stage[];  // [2][n][row_u4]
   const int layer = blockIdx.y, h = blockIdx.x;
-  __nv_bfloat16* kb = kc + layer * layer_stride + (long long)h * slots * 128;
-  __nv_bfloat16* vb = vc + layer * layer_stride + (long long)h * slots * 128;
-  for (int i = threadIdx.x; i < n * 16; i += blockDim.x) {
-    const int r = i >> 4, c = i & 15;
-    stage[i] = reinterpret_cast<const uint4*>(kb + (long long)src[r] * 128)[c];
-    stage[n * 16 + i] = reinterpret_cast<const uint4*>(vb + (long long)src[r] * 128)[c];
+  const long long row_bytes = (long long)row_u4 * 16;
+  uint8_t* kb = kc + layer * layer_stride_bytes + (long long)h * slots * row_bytes;
+  uint8_t* vb = vc + layer * layer_stride_bytes + (long long)h * slots * row_bytes;
+  const int total = n * row_u4;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int r = i / row_u4, c = i - r * row_u4;
+    stage[i] = reinterpret_cast<const uint4*>(kb + src[r] * row_bytes)[c];
+    stage[total + i] = reinterpret_cast<const uint4*>(vb + src[r] * row_bytes)[c];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n * 16; i += blockDim.x) {
-    const int r = i >> 4, c = i & 15;
-    reinterpret_cast<uint4*>(kb + (long long)dst[r] * 128)[c] = stage[i];
-    reinterpret_cast<uint4*>(vb + (long long)dst[r] * 128)[c] = stage[n * 16 + i];
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int r = i / row_u4, c = i - r * row_u4;
+    reinterpret_cast<uint4*>(kb + dst[r] * row_bytes)[c] = stage[i];
+    reinterpret_cast<uint4*>(vb + dst[r] * row_bytes)[c] = stage[total + i];
   }
+}
+
+static int kv_compact_launch(void* kcache, void* vcache, int layers, long long layer_stride_elems, long long slots,
+                             int KVH, int elem_bytes, const int* src, const int* dst, int n, cudaStream_t stream) {
+  if (n <= 0) return SX_OK;
+  const int row_u4 = 128 * elem_bytes / 16;
+  // all rows are staged in smem (K and V of one head): up to 448 bf16 rows / 224
+  // fp32 rows -- more than the deepest accepted path (max_depth <= 250 -> 251
+  // rows) in bf16; fp32 mode validates its depth up front
+  const int max_rows = (int)((227LL * 1024) / (2LL * row_u4 * 16));
+  if (n > max_rows) return arg_error("kv_compact: at most %d rows per call (got %d)", max_rows, n);
+  const size_t smem = (size_t)2 * n * row_u4 * sizeof(uint4);
+  if (smem > 48 * 1024)
+    if (int st = ensure_smem_attr((const void*)kv_compact_kernel, (int)smem)) return st;
+  kv_compact_kernel<<<dim3(KVH, layers), 256, smem, stream>>>(reinterpret_cast<uint8_t*>(kcache),
+                                                               reinterpret_cast<uint8_t*>(vcache),
+                                                               layer_stride_elems * elem_bytes, slots, KVH, row_u4,
+                                                               src, dst, n);
+  SX_CHECK_LAUNCH("kv_compact_kernel");
+  return SX_OK;
 }
 
 }  // namespace sx
@@ -258,16 +281,10 @@ extern "C" int sx_rope_kv(const void* qkv, const int* pos, int pos_base, const i
 
 extern "C" int sx_kv_compact(void* kcache, void* vcache, int layers, long long layer_stride, long long slots, int KVH,
                              const int* src, const int* dst, int n, cudaStream_t stream) {
-  if (n <= 0) return SX_OK;
-  // all rows are staged in smem (512 B per row: K and V of one head) -- up to
-  // 448 rows, more than the deepest accepted path (max_depth <= 250 -> 251 rows)
-  if (n > 448) return arg_error("kv_compact: at most 448 rows per call (got %d)", n);
-  const size_t smem = (size_t)2 * n * 16 * sizeof(uint4);
-  if (smem > 48 * 1024)
-    if (int st = ensure_smem_attr((const void*)kv_compact_kernel, (int)smem)) return st;
-  kv_compact_kernel<<<dim3(KVH, layers), 256, smem, stream>>>(reinterpret_cast<__nv_bfloat16*>(kcache),
-                                                               reinterpret_cast<__nv_bfloat16*>(vcache), layer_stride,
-                                                               slots, KVH, src, dst, n);
-  SX_CHECK_LAUNCH("kv_compact_kernel");
-  return SX_OK;
+  return kv_compact_launch(kcache, vcache, layers, layer_stride, slots, KVH, 2, src, dst, n, stream);
+}
+
+extern "C" int sx_kv_compact_f32(void* kcache, void* vcache, int layers, long long layer_stride, long long slots,
+                                 int KVH, const int* src, const int* dst, int n, cudaStream_t stream) {
+  return kv_compact_launch(kcache, vcache, layers, layer_stride, slots, KVH, 4, src, dst, n, stream);
 }

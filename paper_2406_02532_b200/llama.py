@@ -111,11 +111,12 @@ def split_gate_up(wgu: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 def layer_layout(cfg: LlamaConfig, shard: TPShard | None = None,
-                 stored: bool = True) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
+                 stored: bool = True, elem: int = 2) -> tuple[dict[str, tuple[int, tuple[int, ...]]], int]:
     """Byte offsets of one decoder layer's tensors in a contiguous buffer
     (256-B aligned, the unit streamed in offload mode); `shard`: this rank's
     tensor-parallel slice of the layer (tp.py). stored=True: the HBM layout
-    (gate/up interleaved as "wgu"); False: the draw layout (wg, wu apart)."""
+    (gate/up interleaved as "wgu"); False: the draw layout (wg, wu apart).
+    elem: bytes per element (2 = bf16, 4 = the fp32 target mode)."""
     shapes = dict((TPShard(0, 1) if shard is None else shard).local_shapes(cfg))
     if stored:
         f, d = shapes.pop("wg")
@@ -126,12 +127,13 @@ def layer_layout(cfg: LlamaConfig, shard: TPShard | None = None,
     out, off = {}, 0
     for k, shp in shapes.items():
         out[k] = (off, shp)
-        off += (math.prod(shp) * 2 + 255) // 256 * 256
+        off += (math.prod(shp) * elem + 255) // 256 * 256
     return out, off
 
 
-def layer_views(buf: torch.Tensor, layout) -> dict[str, torch.Tensor]:
-    return {k: buf[o : o + math.prod(s) * 2].view(torch.bfloat16).view(s) for k, (o, s) in layout.items()}
+def layer_views(buf: torch.Tensor, layout, dtype: torch.dtype = torch.bfloat16) -> dict[str, torch.Tensor]:
+    e = torch.empty((), dtype=dtype).element_size()
+    return {k: buf[o : o + math.prod(s) * e].view(dtype).view(s) for k, (o, s) in layout.items()}
 
 
 class LlamaWeights:
@@ -140,7 +142,8 @@ class LlamaWeights:
     up projections are stored interleaved ("wgu", interleave_gate_up)."""
 
     def __init__(self, cfg: LlamaConfig, seed: int, device, std: float = 0.02, lm_scale: float = 1.0,
-                 offload: bool = False, shard: TPShard | None = None, init: str = "device"):
+                 offload: bool = False, shard: TPShard | None = None, init: str = "device",
+                 dtype: torch.dtype = torch.bfloat16):
         """init="device": drawn by a CUDA generator (fast at 70B); "host": drawn
         by a CPU generator and uploaded -- the same values `host_weights_fp32`
         draws without a GPU (the CPU reference arm's copy of small models)."""
@@ -149,6 +152,8 @@ class LlamaWeights:
         self.cfg = cfg
         self.offload = offload
         self.shard = shard
+        self.dtype = dtype
+        elem = torch.empty((), dtype=dtype).element_size()
         host = init == "host"
         g = torch.Generator(device="cpu" if host else device)
         g.manual_seed(seed)
@@ -158,20 +163,20 @@ class LlamaWeights:
                 return t.copy_(torch.empty(t.shape, dtype=t.dtype).normal_(0.0, s, generator=g))
             return t.normal_(0.0, s, generator=g)
 
-        self.emb = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device))
-        self.layout, self.layer_bytes = layer_layout(cfg, shard)
+        self.emb = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=dtype, device=device))
+        self.layout, self.layer_bytes = layer_layout(cfg, shard, elem=elem)
         self.layer_bufs: list[torch.Tensor] = []
         self.layers = []
         tmp = torch.empty(self.layer_bytes, dtype=torch.uint8, device=device) if offload else None
         # every layer is drawn in the full, unsharded draw layout (same draw order
         # for every TP degree / storage layout), then sliced (TP) and stored
-        gen_layout, gen_bytes = layer_layout(cfg, stored=False)
+        gen_layout, gen_bytes = layer_layout(cfg, stored=False, elem=elem)
         gen_tmp = torch.empty(gen_bytes, dtype=torch.uint8, device=device)
         sh = shard if shard is not None else TPShard(0, 1)
         for _ in range(cfg.layers):
             buf = tmp if offload else torch.empty(self.layer_bytes, dtype=torch.uint8, device=device)
-            v = layer_views(buf, self.layout)
-            src = layer_views(gen_tmp, gen_layout)
+            v = layer_views(buf, self.layout, dtype)
+            src = layer_views(gen_tmp, gen_layout, dtype)
             for k in ("wqkv", "wo", "wg", "wu", "wd"):  # draw order
                 rnd_(src[k])
             for k in ("wqkv", "wo", "wd"):
@@ -183,13 +188,13 @@ class LlamaWeights:
                 host = torch.empty(self.layer_bytes, dtype=torch.uint8, pin_memory=True)
                 host.copy_(buf)
                 self.layer_bufs.append(host)
-                self.layers.append(layer_views(host, self.layout))
+                self.layers.append(layer_views(host, self.layout, dtype))
             else:
                 self.layer_bufs.append(buf)
                 self.layers.append(v)
         del tmp, gen_tmp
-        self.nf = torch.ones(cfg.d, dtype=torch.bfloat16, device=device)
-        self.lm = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=torch.bfloat16, device=device), std * lm_scale)
+        self.nf = torch.ones(cfg.d, dtype=dtype, device=device)
+        self.lm = rnd_(torch.empty((cfg.vocab, cfg.d), dtype=dtype, device=device), std * lm_scale)
         if shard is not None:
             self.lm = shard.shard(cfg, "lm", self.lm)
 
@@ -282,7 +287,8 @@ class LayerStreamer:
 
 
 class _Buffers:
-    def __init__(self, cfg: LlamaConfig, n: int, device, shard: TPShard | None = None, reduce_bf16: bool = False):
+    def __init__(self, cfg: LlamaConfig, n: int, device, shard: TPShard | None = None, reduce_bf16: bool = False,
+                 act_dtype: torch.dtype = torch.bfloat16):
         self.n = n
         sh = TPShard(0, 1) if shard is None else shard
         H = cfg.heads // sh.world
@@ -290,11 +296,11 @@ class _Buffers:
         self.x = torch.empty((n, cfg.d), dtype=torch.float32, device=device)
         # o / down projection output (TP: the partial sums that are all-reduced)
         self.y = torch.empty((n, cfg.d), dtype=torch.bfloat16 if reduce_bf16 else torch.float32, device=device)
-        self.h = torch.empty((n, cfg.d), dtype=torch.bfloat16, device=device)
-        self.qkv = torch.empty((n, (H + 2 * KVH) * cfg.head_dim), dtype=torch.bfloat16, device=device)
-        self.q = torch.empty((n, H * cfg.head_dim), dtype=torch.bfloat16, device=device)
-        self.att = torch.empty((n, H * cfg.head_dim), dtype=torch.bfloat16, device=device)
-        self.act = torch.empty((n, cfg.ff // sh.world), dtype=torch.bfloat16, device=device)
+        self.h = torch.empty((n, cfg.d), dtype=act_dtype, device=device)
+        self.qkv = torch.empty((n, (H + 2 * KVH) * cfg.head_dim), dtype=act_dtype, device=device)
+        self.q = torch.empty((n, H * cfg.head_dim), dtype=act_dtype, device=device)
+        self.att = torch.empty((n, H * cfg.head_dim), dtype=act_dtype, device=device)
+        self.act = torch.empty((n, cfg.ff // sh.world), dtype=act_dtype, device=device)
         self.logits = torch.empty((n, cfg.vocab), dtype=torch.float32, device=device)
         if sh.world > 1:  # vocab-parallel LM head: local slice + all-gather staging
             self.logits_l = torch.empty((n, cfg.vocab // sh.world), dtype=torch.float32, device=device)
@@ -325,6 +331,7 @@ class LlamaModel(LanguageModel):
         tp_fused: bool | None = None,
         offload_buffers: int = 8,
         init: str = "device",
+        dtype: str = "bf16",
     ):
         """offload_buffers: HBM staging slots of the layer streamer (offload mode);
         beyond the 2 a double buffer needs, the extra slots let the host link keep
@@ -342,6 +349,12 @@ class LlamaModel(LanguageModel):
             cfg = PRESETS[cfg]
         if cfg.head_dim != 128:
             raise ValueError("head_dim must be 128")
+        if dtype not in ("bf16", "fp32"):
+            raise ValueError(f"dtype must be 'bf16' or 'fp32', got {dtype!r}")
+        # fp32 target mode (csrc/fp32_path.cu): fp32 weights / activations / KV, FFMA GEMMs
+        self.fp32 = dtype == "fp32"
+        if self.fp32 and (offload or (tp is not None and tp.world > 1)):
+            raise ValueError("the fp32 target mode runs resident on one GPU (no offload / tensor parallelism)")
         if not torch.cuda.is_available():
             raise RuntimeError("LlamaModel needs a CUDA device; there is no CPU fallback")
         _lib.load()
@@ -356,15 +369,18 @@ class LlamaModel(LanguageModel):
         self.reduce_bf16 = bool(reduce_bf16 and self.tp is not None)
         self.H = cfg.heads // (self.tp.world if self.tp else 1)  # local query / KV heads
         self.KVH = cfg.kv_heads // (self.tp.world if self.tp else 1)
-        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload, shard=self.shard, init=init)
+        wdt = torch.float32 if self.fp32 else torch.bfloat16
+        self.dtype = dtype
+        self.w = LlamaWeights(cfg, seed, self.device, std, lm_scale, offload=offload, shard=self.shard, init=init,
+                              dtype=wdt)
         self.streamer = LayerStreamer(self.w, self.device, nbuf=max(2, min(offload_buffers, cfg.layers))) if offload else None
         self.slots = max_ctx
-        self.kc = torch.zeros((cfg.layers, self.KVH, max_ctx, cfg.head_dim), dtype=torch.bfloat16, device=self.device)
+        self.kc = torch.zeros((cfg.layers, self.KVH, max_ctx, cfg.head_dim), dtype=wdt, device=self.device)
         self.vc = torch.zeros_like(self.kc)
         self.layer_stride = self.KVH * max_ctx * cfg.head_dim
         self.cos, self.sin = _rope_tables(cfg, max_ctx + 64, self.device)
         self.max_tokens = max_tokens
-        self.buf = _Buffers(cfg, max_tokens, self.device, self.shard, self.reduce_bf16)
+        self.buf = _Buffers(cfg, max_tokens, self.device, self.shard, self.reduce_bf16, act_dtype=wdt)
         self.tp_fused = False
         if self.tp is not None and tp_fused is not False:
             W = self.tp.world
@@ -390,7 +406,9 @@ class LlamaModel(LanguageModel):
                 0.0, 1.0, generator=g)
             self.bias_w = (torch.empty((cfg.vocab, synthetic.rank), dtype=torch.bfloat16, device=self.device)
                            .normal_(0.0, 1.0, generator=g) * (synthetic.scale / math.sqrt(synthetic.rank))).bfloat16()
-            self.bias_in = torch.empty((max_tokens, synthetic.rank), dtype=torch.bfloat16, device=self.device)
+            if self.fp32:  # the same (bf16-valued) table, held in fp32 for the FFMA GEMM
+                self.bias_u, self.bias_w = self.bias_u.float(), self.bias_w.float()
+            self.bias_in = torch.empty((max_tokens, synthetic.rank), dtype=wdt, device=self.device)
         self.committed: list[int] = []  # tokens whose KV is in slots [0, len)
         self.record: list[dict] | None = None  # test hook: per build, prefix -> fp32 logits row
         self.use_graphs = True  # draft rounds and one-token chains as CUDA graphs
@@ -438,6 +456,9 @@ class LlamaModel(LanguageModel):
         cfg, b, w = self.cfg, self.buf, self.w
         if n > b.n:
             raise ValueError(f"forward of {n} tokens exceeds max_tokens={b.n}")
+        if self.fp32:
+            return self._forward_f32(n, tokens, pos, pos_base, slot, slot_base, dense_len, dense_const, anc, anc_base,
+                                     anc_len, A, logits_from)
         st = _lib.stream_ptr()
         x, h = b.x[:n], b.h[:n]
         _lib.call("sx_embed", _lib.ptr(w.emb), _lib.ptr(tokens), n, cfg.d, _lib.ptr(x), st)
@@ -498,6 +519,48 @@ class LlamaModel(LanguageModel):
             bi = self.bias_in[:m]
             torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)
             K.gemm(bi, self.bias_w, out=logits, epi=K.EPI_ADD_F32)
+        return logits
+
+    def _forward_f32(self, n, tokens, pos, pos_base, slot, slot_base, dense_len, dense_const, anc, anc_base, anc_len, A,
+                     logits_from):
+        """The fp32 target mode: the same sequence of operations as `forward`,
+        every tensor fp32, FFMA GEMMs and the fp32 attention (csrc/fp32_path.cu)."""
+        cfg, b, w = self.cfg, self.buf, self.w
+        st, p = _lib.stream_ptr(), _lib.ptr
+        x, h, y = b.x[:n], b.h[:n], b.y[:n]
+        H, KVH = self.H, self.KVH
+        _lib.call("sx_embed_f32", p(w.emb), p(tokens), n, cfg.d, p(x), st)
+
+        def gemm(xin, wt, out, epi):
+            _lib.call("sx_gemm_f32", p(wt), p(xin), p(out), xin.shape[0], wt.shape[0], wt.shape[1], out.stride(0), epi,
+                      st)
+
+        for li in range(cfg.layers):
+            L = w.layers[li]
+            kc, vc = self.kc[li], self.vc[li]
+            _lib.call("sx_add_rmsnorm_f32", p(x), p(y) if li > 0 else None, p(L["n1"]), n, cfg.d, cfg.eps, p(h), st)
+            gemm(h, L["wqkv"], b.qkv[:n], K.EPI_F32)
+            _lib.call("sx_rope_kv_f32", p(b.qkv), p(pos), pos_base, p(slot), slot_base, n, H, KVH, p(self.cos),
+                      p(self.sin), p(b.q), p(kc), p(vc), self.slots, st)
+            _lib.call("sx_tree_attention_f32", p(b.q), p(kc), p(vc), self.slots, p(dense_len), dense_const, p(anc),
+                      anc_base, p(anc_len), A, p(b.att), n, H, KVH, st)
+            gemm(b.att[:n], L["wo"], y, K.EPI_F32)
+            _lib.call("sx_add_rmsnorm_f32", p(x), p(y), p(L["n2"]), n, cfg.d, cfg.eps, p(h), st)
+            gemm(h, L["wgu"], b.act[:n], K.EPI_SWIGLU_IL)
+            gemm(b.act[:n], L["wd"], y, K.EPI_F32)
+        self.stats["forward_tokens"] += n
+        self.stats["forwards"] += 1
+        if logits_from is None:
+            return None
+        m = n - logits_from
+        hh = b.h[logits_from:n]
+        _lib.call("sx_add_rmsnorm_f32", p(x[logits_from:]), p(y[logits_from:]), p(w.nf), m, cfg.d, cfg.eps, p(hh), st)
+        logits = b.logits[:m]
+        gemm(hh, w.lm, logits, K.EPI_F32)
+        if self.synthetic is not None:
+            bi = self.bias_in[:m]
+            torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)
+            gemm(bi, self.bias_w, logits, K.EPI_ADD_F32)
         return logits
 
     def _fused_reduce(self, xin: torch.Tensor, w: torch.Tensor, n: int) -> None:
@@ -641,8 +704,9 @@ class LlamaModel(LanguageModel):
                 src = torch.tensor([c + r for r in rows], dtype=torch.int32).to(self.device, non_blocking=True)
                 dst = torch.tensor([c + 1 + i for i in range(len(rows))], dtype=torch.int32).to(self.device,
                                                                                                  non_blocking=True)
-                _lib.call("sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc), self.cfg.layers, self.layer_stride,
-                          self.slots, self.KVH, _lib.ptr(src), _lib.ptr(dst), len(rows), _lib.stream_ptr())
+                _lib.call("sx_kv_compact_f32" if self.fp32 else "sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc),
+                          self.cfg.layers, self.layer_stride, self.slots, self.KVH, _lib.ptr(src), _lib.ptr(dst),
+                          len(rows), _lib.stream_ptr())
                 K.IO["h2d"] += 8 * len(rows)
             self.committed.extend(tree.nodes[r - 1].token for r in rows)
         elif getattr(tree, "draft_model", None) is self:
@@ -663,8 +727,9 @@ class LlamaModel(LanguageModel):
                 s_t = torch.tensor(src, dtype=torch.int32).to(self.device, non_blocking=True)
                 d_t = torch.tensor([c + 1 + i for i in range(len(src))], dtype=torch.int32).to(self.device,
                                                                                                 non_blocking=True)
-                _lib.call("sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc), self.cfg.layers, self.layer_stride,
-                          self.slots, self.KVH, _lib.ptr(s_t), _lib.ptr(d_t), len(src), _lib.stream_ptr())
+                _lib.call("sx_kv_compact_f32" if self.fp32 else "sx_kv_compact", _lib.ptr(self.kc), _lib.ptr(self.vc),
+                          self.cfg.layers, self.layer_stride, self.slots, self.KVH, _lib.ptr(s_t), _lib.ptr(d_t),
+                          len(src), _lib.stream_ptr())
                 K.IO["h2d"] += 8 * len(src)
             self.committed.extend(toks)
 
