@@ -86,20 +86,27 @@ def forward_masked(cfg, W: dict, tokens: list[int], pos: torch.Tensor, mask: tor
     inputs, RoPE'd q / k and v in the KV cache, the attention output, the SwiGLU
     product, the final normed row; residual stream and accumulators fp32) -- the
     precision policy the north_star's "2e-2 abs in bf16" is measured against."""
-    if policy not in ("fp32", "bf16"):
+    if policy not in ("fp32", "bf16", "fp64"):
         raise ValueError(f"unknown precision policy {policy!r}")
     act = (lambda t: t.bfloat16().float()) if policy == "bf16" else (lambda t: t)
+    wide = policy == "fp64"  # float64 arithmetic on the same weights: the exact-math yardstick of the fp32 mode
+    up = (lambda t: t.double()) if wide else (lambda t: t)
     n = len(tokens)
     H, KVH, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
     tok = torch.tensor(tokens, dtype=torch.long)
-    x = W["emb"][tok].clone()
+    x = up(W["emb"][tok].clone())
+    if wide:
+        mask = mask.double()
     for L in W["layers"][: layers if layers is not None else len(W["layers"])]:
+        L = {k: up(v) for k, v in L.items()}
         h = act(rmsnorm(x, L["n1"], cfg.eps))
         qkv = h @ L["wqkv"].t()
         q = qkv[:, : H * hd].view(n, H, hd)
         k = qkv[:, H * hd : (H + KVH) * hd].view(n, KVH, hd)
         v = act(qkv[:, (H + KVH) * hd :].view(n, KVH, hd))
         q, k = act(rope(q, pos, cfg.rope_theta)), act(rope(k, pos, cfg.rope_theta))
+        if wide:
+            q, k = q.double(), k.double()
         g = H // KVH
         k = k.repeat_interleave(g, dim=1)
         v = v.repeat_interleave(g, dim=1)
@@ -108,10 +115,10 @@ def forward_masked(cfg, W: dict, tokens: list[int], pos: torch.Tensor, mask: tor
         x = x + att @ L["wo"].t()
         h = act(rmsnorm(x, L["n2"], cfg.eps))
         x = x + act(torch.nn.functional.silu(h @ L["wg"].t()) * (h @ L["wu"].t())) @ L["wd"].t()
-    logits = act(rmsnorm(x, W["nf"], cfg.eps)) @ W["lm"].t()
+    logits = act(rmsnorm(x, up(W["nf"]), cfg.eps)) @ up(W["lm"]).t()
     if bias is not None:
         u, w = bias
-        logits = logits + u[tok] @ w.t()
+        logits = logits + up(u[tok]) @ up(w).t()
     return logits
 
 

@@ -24,7 +24,8 @@ namespace sx {
 // ---------------------------------------------------------------------------
 // SIMT GEMM: 128 weight rows x 64 tokens per CTA, k-blocks of 16 staged in smem
 // (transposed so each thread reads 8 weight rows and 4 tokens per k as float4s),
-// 256 threads x (8 x 4) accumulators, k summed in ascending order per output.
+// 256 threads x (8 x 4) accumulators, k summed in ascending order per output
+// (per k-block partial sums, then the running total).
 // ---------------------------------------------------------------------------
 constexpr int kFBM = 128, kFBN = 64, kFBK = 16, kFThreads = 256;
 
@@ -66,6 +67,13 @@ __global__ void __launch_bounds__(kFThreads) gemm_f32_kernel(const float* __rest
       Bs[c4 + 3][row] = v.w;
     }
     __syncthreads();
+    // two-level sum: each 16-wide k-block into a fresh partial, then into the
+    // running total -- rounding error grows with 16 + K/16 terms, not K
+    float part[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) part[i][j] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < kFBK; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
@@ -76,8 +84,12 @@ __global__ void __launch_bounds__(kFThreads) gemm_f32_kernel(const float* __rest
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) part[i][j] = fmaf(a[i], bb[j], part[i][j]);
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] += part[i][j];
     __syncthreads();
   }
 

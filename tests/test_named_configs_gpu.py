@@ -11,8 +11,8 @@ each rounding flip re-randomises the downstream rounding noise
 q / k / v / attention agree to 0.15 % one-ulp flips, yet after one SwiGLU 22 %
 of activations differ by an ulp). So the bf16 path is held to what bf16 can
 deliver: no further from the fp32 forward than the bf16 policy itself (max and
-rms, the oracle run with activations rounded where the GPU stores them), and
-rms error < 2e-2. The 2e-2 max bound holds at d=256 (tests/test_llama_gpu.py);
+rms, the oracle run with activations rounded where the GPU stores them; rms
+0.006-0.026 at these widths). The 2e-2 max bound holds at d=256 (tests/test_llama_gpu.py);
 the all-fp32 tolerance 1e-4 is the fp32 target mode's
 (tests/test_fp32_mode_gpu.py, same widths). Rows checked:
 
@@ -70,7 +70,7 @@ def _max_err(got: torch.Tensor, exp: torch.Tensor) -> float:
 
 def check(got, cpu_fn, what):
     """bf16 GPU rows vs the fp32 oracle: no further from it than the bf16
-    precision policy itself (max and rms, restated by the oracle), rms < TOL."""
+    precision policy itself (max and rms, restated by the oracle)."""
     ref16, ref32 = cpu_fn("bf16"), cpu_fn("fp32")
     g = got.float().cpu()
     d32, pol, d16 = g - ref32, ref16 - ref32, g - ref16
@@ -80,7 +80,6 @@ def check(got, cpu_fn, what):
           f"rms {rms(pol):.3g}; |gpu - bf16 policy| max {e16:.4g} rms {rms(d16):.3g}")
     assert e32 <= p32 + 5e-3, (what, e32, p32)
     assert rms(d32) <= 1.1 * rms(pol) + 1e-4, (what, rms(d32), rms(pol))
-    assert rms(d32) < TOL, (what, rms(d32))
 
 
 def test_prefill_rows(named_pair):
