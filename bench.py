@@ -72,6 +72,9 @@ def parse():
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 legs (demo pair + tiny Llama end to end)")
+    ap.add_argument("--c3-steps", type=int, default=3,
+                    help="C2 runs only: timed iterations of the stage-3 block (70B target offloaded to pinned host "
+                         "RAM, per-layer streaming, K=2048, t=0.6/top-p 0.9) after the C2 line's own timing; 0 = skip")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sequential", action="store_true", help="skip the sequential-decoding speed-up denominator")
     ap.add_argument("--offload-buffers", type=int, default=8,
@@ -505,6 +508,90 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# ----------------------------------------------------------------------------- stage 3 block
+def measure_c3(args, draft, prompt, resident_pass_ms: float, resident_pass_tokens: int) -> dict:
+    """BASELINE configs[2] (C3) on the same box after the C2 timing: the 70B
+    target re-created offloaded (weights in pinned host RAM, streamed per layer
+    through the HBM ring, LayerStreamer), the resident 7B draft, K=2048,
+    t=0.6 / top-p 0.9 (warped scoring). Reports tokens/s and accepted tokens per
+    iteration, the achieved H2D rate against the pinned rate measured here
+    (north_star: >= 80 % of host-link bandwidth), sequential decoding on the
+    same offloaded target (the speed-up denominator), and the cost model
+    (costsim.forward_time) fitted from this run's own measurements."""
+    import torch
+
+    import paper_2406_02532_b200 as sx
+    from paper_2406_02532_b200.costsim import CostModel, forward_time
+    from paper_2406_02532_b200.engine import SpecExecSession
+    from paper_2406_02532_b200.llama import PRESETS, LlamaModel
+
+    dname, tname, K, D, B, temp, top_p = WORKLOADS["c3"]
+    h2d_peak = measure_h2d(torch)
+    t0 = time.time()
+    ctx_cap = args.prompt_len + (1 + args.c3_steps + 4) * (D + 1) + 64
+    target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=K + 1, offload=True,
+                        offload_buffers=args.offload_buffers)
+    torch.cuda.synchronize()
+    init_s = time.time() - t0
+    cfg = sx.SamplingConfig(temp, top_p, seed=0, max_new_tokens=100000)
+    sess = SpecExecSession(prompt, draft, target, sx.BuilderParams(K, D, B), cfg, warp_scores=True)
+    sess.step(100000)  # warm-up iteration (graph buckets at K=2048, ring fill)
+    from paper_2406_02532_b200 import engine as Eng
+
+    Eng.STAGES = Eng.StageTimer()
+    bytes0, tok0, it0, dc0 = target.streamer.bytes, len(sess.tokens), sess.stats.target_calls, sess.stats.draft_calls
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    n_iter = 0
+    while n_iter < args.c3_steps:
+        sess.step(100000)
+        if sess.cache is None:
+            n_iter += 1
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    stages = {k: v / args.c3_steps for k, v in Eng.STAGES.totals().items()}
+    Eng.STAGES = None
+    tokens = len(sess.tokens) - tok0
+    streamed = target.streamer.bytes - bytes0
+    h2d = streamed / (ms / 1e3) / 1e9
+    draft_calls = (sess.stats.draft_calls - dc0) / args.c3_steps
+    # sequential decoding on the same offloaded target: one streamed pass per token
+    cfg1 = sx.SamplingConfig(temp, top_p, seed=11, max_new_tokens=1)
+    cfg2 = sx.SamplingConfig(temp, top_p, seed=11, max_new_tokens=2)
+    sx.generate_sequential(prompt, target, cfg1)  # prompt KV already committed; warm
+    tt = []
+    for c in (cfg1, cfg2):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        sx.generate_sequential(prompt, target, c)
+        torch.cuda.synchronize()
+        tt.append(time.perf_counter() - t1)
+    seq_rate = 1.0 / max(1e-9, tt[1] - tt[0])
+    value = tokens / (ms / 1e3)
+    tb = PRESETS[tname].weight_bytes()
+    cm = CostModel.from_b200_measurements(target_bytes=target.w.layer_bytes * target.cfg.layers,
+                                          h2d_bytes_per_s=h2d_peak * 1e9, resident_pass_s=resident_pass_ms / 1e3,
+                                          pass_tokens=resident_pass_tokens, draft_bytes=PRESETS[dname].weight_bytes(),
+                                          draft_step_s=stages.get("draft", 0.0) / 1e3 / max(1.0, draft_calls),
+                                          ring_layers=target.streamer.nbuf, layers=target.cfg.layers,
+                                          draft_phase_s=stages.get("draft", 0.0) / 1e3)
+    out = {"workload": workload_desc("c3", K, B), "scoring": "warped", "steps": args.c3_steps,
+           "tokens_per_s": value, "ms_per_iteration": ms / args.c3_steps, "accepted_tokens_per_iter": tokens / args.c3_steps,
+           "draft_calls_per_iter": draft_calls, "stage_ms_per_step": stages,
+           "h2d": {"achieved_GBps": h2d, "pinned_peak_GBps": h2d_peak, "frac": h2d / h2d_peak if h2d_peak else None,
+                   "bytes_per_iteration": streamed / args.c3_steps,
+                   "note": "bytes the layer ring streamed during the timed iterations / their device time; peak = "
+                           "pinned 1 GiB H2D copies measured in this run"},
+           "sequential": {"tokens_per_s": seq_rate, "speedup_of_specexec": value / seq_rate},
+           "costsim": {"preset": json.loads(cm.to_json()), "forward_time_model_s": forward_time(cm, K + 1),
+                       "target_stage_measured_s": stages.get("target", 0.0) / 1e3},
+           "init_seconds": init_s, "weights_streamed_GB_per_pass": tb / 1e9}
+    del sess, target
+    return out
+
+
 # ----------------------------------------------------------------------------- B200 arm
 def main():
     args = parse()
@@ -690,6 +777,18 @@ def main():
                "note": "target-only decoding, one token per target pass (CUDA graph), prompt KV cached; "
                        "difference of a (2 + n)- and a 2-token run, min of 3 each"}
 
+    c3 = None
+    if world == 1 and args.workload == "c2" and args.c3_steps > 0:
+        import gc
+
+        resident_pass_ms = stages.get("target", 0.0)
+        del sess
+        target = None
+        gc.collect()
+        torch.cuda.empty_cache()
+        c3 = measure_c3(args, draft, prompt, resident_pass_ms, K + 1)
+        gc.collect()
+        torch.cuda.empty_cache()
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args, K, B, accepted_per_iter, draft_calls / max(1, iters),
@@ -717,6 +816,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cb,
             "c1": c1,
+            "c3": c3,
             "e2e": e2e,
             "sequential": seq,
             "gpu_launches": launches,
