@@ -154,12 +154,12 @@ class LlamaWeights:
         self.shard = shard
         self.dtype = dtype
         elem = torch.empty((), dtype=dtype).element_size()
-        host = init == "host"
-        g = torch.Generator(device="cpu" if host else device)
+        host_draw = init == "host"
+        g = torch.Generator(device="cpu" if host_draw else device)
         g.manual_seed(seed)
 
         def rnd_(t, s=std):
-            if host:
+            if host_draw:
                 return t.copy_(torch.empty(t.shape, dtype=t.dtype).normal_(0.0, s, generator=g))
             return t.normal_(0.0, s, generator=g)
 
