@@ -281,6 +281,50 @@ def gen_beam_instances(n=80):
     return out
 
 
+def gen_harness():
+    """The reference harness (pkg/src/speckit/harness/experiments.py) on a small
+    grid: run_acceptance (rows with bootstrap CIs and mean_rounds, curves,
+    run records, the versioned CSV / JSONL text), run_throughput over a bundled
+    preset (rows + CSV) and run_equivalence (cells + JSONL)."""
+    import tempfile
+
+    from speckit import load_preset
+    from speckit.harness.config import ExperimentConfig
+    from speckit.harness.experiments import run_acceptance, run_equivalence, run_throughput
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        spec = dict(kind="acceptance", target={"kind": "synthetic", "seed": 11, "vocab_size": 16, "sharpness": 0.3},
+                    draft={"kind": "power", "base": {"kind": "synthetic", "seed": 11, "vocab_size": 16,
+                                                     "sharpness": 0.3}, "power": 0.6},
+                    prompt_source={"kind": "inline", "token_lists": [[1, 2, 3], [4, 5]]}, budgets=[4, 16, 32],
+                    seeds=[0, 1, 2], sampling=[{"temperature": 0.6, "top_p": 0.9}, {"temperature": 0.0}],
+                    max_new_tokens=16, max_depth=5, batch_size=4, si_depth=4, output_path=f"{td}/acc.csv")
+        cfg = ExperimentConfig(**spec)
+        res = run_acceptance(cfg)
+        out["acceptance"] = {"config": {k: v for k, v in spec.items() if k != "output_path"},
+                             "rows": [r.__dict__ for r in res.rows],
+                             "curves": {m: {"budgets": c.budgets, "gen_rates": c.gen_rates, "rounds": c.rounds}
+                                        for m, c in res.curves.items()},
+                             "run_records": res.run_records,
+                             "csv": (pathlib.Path(td) / "acc.csv").read_text(),
+                             "jsonl": (pathlib.Path(td) / "acc.runs.jsonl").read_text()}
+        cfg_t = ExperimentConfig(**{**spec, "kind": "throughput", "output_path": f"{td}/thr.csv"})
+        thr = run_throughput(cfg_t, load_preset("pcie4-16bit-70b"), res.curves)
+        out["throughput"] = {"preset": "pcie4-16bit-70b", "rows": [r.__dict__ for r in thr.rows],
+                             "choices": {m: c.__dict__ for m, c in thr.choices.items()},
+                             "csv": (pathlib.Path(td) / "thr.csv").read_text()}
+        spec_e = dict(kind="equivalence", target={"kind": "synthetic", "seed": 1, "vocab_size": 10, "sharpness": 0.3},
+                      budgets=[8], seeds=[0, 1, 2], sampling=[{"temperature": 0.6, "top_p": 0.9}, {"temperature": 0.0},
+                                                              {"temperature": 1.0}],
+                      max_new_tokens=12, max_depth=4, batch_size=4, equivalence_cells=12, vocab_size=10,
+                      sharpness=0.3, output_path=f"{td}/eq.jsonl")
+        rep = run_equivalence(ExperimentConfig(**spec_e))
+        out["equivalence"] = {"config": {k: v for k, v in spec_e.items() if k != "output_path"},
+                              "passed": rep.passed, "jsonl": (pathlib.Path(td) / "eq.jsonl").read_text()}
+    return out
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     jobs = {
@@ -291,6 +335,7 @@ def main():
         "logit_engine.json": gen_logit_engine,
         "specinfer_grid.json": gen_specinfer_grid,
         "beam_instances.json": gen_beam_instances,
+        "harness_grid.json": gen_harness,
     }
     only = set(sys.argv[1:])
     for name, fn in jobs.items():
