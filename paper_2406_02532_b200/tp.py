@@ -117,7 +117,10 @@ def gather_vocab(comm, local: torch.Tensor, out: torch.Tensor, staging: torch.Te
 
 
 class NcclComm:
-    """torch.distributed communicator (NCCL over NVLink on the B200 box)."""
+    """torch.distributed communicator: NCCL over NVLink on the B200 box (one
+    process per GPU). Under a gloo group (the 2-process test on one GPU,
+    tests/test_tp_procs_gpu.py) the same calls stage device tensors through
+    host memory -- gloo's collectives are host-side."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -126,17 +129,28 @@ class NcclComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.host_staging = dist.get_backend(group) == "gloo"
 
     def all_reduce_(self, t: torch.Tensor) -> None:
+        if self.host_staging:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+            return
         self.dist.all_reduce(t, group=self.group)
 
     def all_gather_(self, local: torch.Tensor, out: torch.Tensor) -> None:
         """local [world-slices of out]: out [world, *local.shape] contiguous."""
         # concatenated layout [world * rows, ...] (accepted by every backend)
+        if self.host_staging:
+            h = torch.empty((out.numel(),), dtype=out.dtype)
+            self.dist.all_gather_into_tensor(h.view(-1, *local.shape[1:]), local.contiguous().cpu(), group=self.group)
+            out.view(-1).copy_(h)
+            return
         self.dist.all_gather_into_tensor(out.view(-1, *local.shape[1:]), local, group=self.group)
 
     def broadcast_ints(self, vals: list[int], src: int = 0) -> list[int]:
-        t = torch.tensor(vals, dtype=torch.int64, device="cuda")
+        t = torch.tensor(vals, dtype=torch.int64, device="cpu" if self.host_staging else "cuda")
         self.dist.broadcast(t, src, group=self.group)
         return [int(v) for v in t.tolist()]
 
