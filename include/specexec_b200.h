@@ -118,6 +118,10 @@ SX_API int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows,
                          int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream);
 SX_API int sx_tree_finalize(void* ws, int K, int B, int V, int D, int root_token, int* out_parent, int* out_token,
                             double* out_edge, int* out_depth, int* out_slot, cudaStream_t stream);
+/* Raw scoring of fp32 logits rows: 0 (default) = one fused persistent kernel
+ * (row statistics + exact scoring, one HBM read per row), 1 = the two-kernel
+ * tree_row_stats + tree_score path (A/B measurement; identical results). */
+SX_API int sx_tree_set_impl(int unfused);
 
 /* ------------------------------------------------ exact table models on GPU
  * MarkovModel / TabularModel (pkg/src/speckit/models.py:77-151) rows for tree

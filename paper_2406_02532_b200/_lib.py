@@ -39,6 +39,7 @@ SIGNATURES: dict[str, tuple] = {
         _c_int,
         [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl, _vp, _vp],
     ),
+    "sx_tree_set_impl": (_c_int, [_c_int]),
     "sx_tree_finalize": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sx_markov_rows": (
         _c_int,

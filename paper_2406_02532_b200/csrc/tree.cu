@@ -250,6 +250,128 @@ __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout
 }
 
 // --------------------------------------------------------------------------
+// Fused row statistics + scoring for fp32 logits rows (raw scoring): a
+// persistent grid walks the batch rows, one 256-thread CTA per row at a time.
+//   pass 1  one HBM read of the row (16-byte loads): exact max and an online
+//           fp32 sum of exp(z - max) -- the prefilter estimate; rows whose best
+//           child cannot beat the threshold stop here (the common case once the
+//           tree holds K nodes);
+//   pass 2  canonical fp64 sum (lane t sums v = t, t + 256, ... then the
+//           halving tree -- the same order as tree_row_stats_kernel), from L2;
+//   pass 3  exact edges / keys of the prefiltered candidates, survivors appended.
+// Bit-identical to tree_row_stats + tree_score (the prefilter only decides
+// which candidates take the exact path, with 1e-3 of slack against an
+// estimate good to ~1e-5), with one read of the row instead of two plus a
+// 64 x B grid of mostly-empty score CTAs.
+__global__ void __launch_bounds__(kRowThreads) tree_logits_rows_kernel(uint8_t* ws, TreeLayout L,
+                                                                         const float* __restrict__ rows, long long ld,
+                                                                         int vec4) {
+  __shared__ RowSmemLite sm;
+  __shared__ float red_m[kRowThreads / 32], red_s[kRowThreads / 32];
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int batch_n = c->batch_n, V = L.V, tid = threadIdx.x, lane = tid & 31;
+  const bool has_thr = c->has_thr;
+  const double thr_nll = c->thr_nll;
+  const unsigned long long th = (unsigned long long)__double_as_longlong(thr_nll);
+  const unsigned long long tl = c->thr_lo;
+  for (int b = blockIdx.x; b < batch_n; b += gridDim.x) {
+    const float* z = rows + b * ld;
+    // ---- pass 1: max and online fp32 sum of exp(z - max)
+    float m = -CUDART_INF_F, sacc = 0.f;
+    auto acc1 = [&](float x) {
+      if (x > m) {
+        sacc = sacc * __expf(m - x) + 1.f;
+        m = x;
+      } else {
+        sacc += __expf(x - m);
+      }
+    };
+    if (vec4) {
+      const float4* z4 = reinterpret_cast<const float4*>(z);
+      const int V4 = V >> 2;
+      int v = tid;
+      for (; v + 3 * kRowThreads < V4; v += 4 * kRowThreads) {  // 4 loads in flight per thread
+        const float4 a0 = __ldcs(z4 + v), a1 = __ldcs(z4 + v + kRowThreads), a2 = __ldcs(z4 + v + 2 * kRowThreads),
+                     a3 = __ldcs(z4 + v + 3 * kRowThreads);
+        acc1(a0.x), acc1(a0.y), acc1(a0.z), acc1(a0.w);
+        acc1(a1.x), acc1(a1.y), acc1(a1.z), acc1(a1.w);
+        acc1(a2.x), acc1(a2.y), acc1(a2.z), acc1(a2.w);
+        acc1(a3.x), acc1(a3.y), acc1(a3.z), acc1(a3.w);
+      }
+      for (; v < V4; v += kRowThreads) {
+        const float4 a0 = z4[v];
+        acc1(a0.x), acc1(a0.y), acc1(a0.z), acc1(a0.w);
+      }
+    } else {
+      for (int v = tid; v < V; v += kRowThreads) acc1(z[v]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sacc, o);
+      const float mm = fmaxf(m, m2);
+      sacc = (m == -CUDART_INF_F ? 0.f : sacc * __expf(m - mm)) + (m2 == -CUDART_INF_F ? 0.f : s2 * __expf(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) {
+      red_m[tid >> 5] = m;
+      red_s[tid >> 5] = sacc;
+    }
+    __syncthreads();
+    float M = red_m[0];
+    for (int w = 1; w < kRowThreads / 32; ++w) M = fmaxf(M, red_m[w]);
+    float S_est = 0.f;
+    for (int w = 0; w < kRowThreads / 32; ++w)
+      if (red_m[w] != -CUDART_INF_F) S_est += red_s[w] * __expf(red_m[w] - M);
+    __syncthreads();  // red_* reused by the next row
+    const float lsa = logf(S_est);
+    const double parent_nll = at<double>(ws, L.b_nll)[b];
+    if (has_thr && dsub(dadd(parent_nll, (double)lsa), kPrefilterSlack) > thr_nll) continue;  // no child survives
+    // ---- pass 2: canonical fp64 sum
+    double acc = 0.0;
+    for (int v = tid; v < V; v += kRowThreads) acc = dadd(acc, sx_exp(dsub((double)z[v], (double)M)));
+    const double S = block_canon_sum(sm, acc);
+    // ---- pass 3: exact keys of the candidates the fp32 estimate cannot rule out
+    const int depth = at<int>(ws, L.b_depth)[b] + 1;
+    const int plex = at<int>(ws, L.b_lex)[b];
+    for (int v0 = 0; v0 < V; v0 += kRowThreads) {
+      const int v = v0 + tid;
+      bool keep = false;
+      double nll = 0.0, edge = 0.0;
+      unsigned long long lo = 0;
+      if (v < V) {
+        const float zv = z[v];
+        if (!has_thr || !(dsub(dsub(parent_nll, (double)((zv - M) - lsa)), kPrefilterSlack) > thr_nll)) {
+          const double pv = ddiv(sx_exp(dsub((double)zv, (double)M)), S);
+          if (pv > 0.0) {
+            edge = sx_log(pv);
+            nll = dsub(parent_nll, edge);
+            lo = make_lo(depth, plex, v);
+            keep = !has_thr || key_less((unsigned long long)__double_as_longlong(nll), lo, th, tl);
+          }
+        }
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (mask) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&c->n_surv, __popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const long long k = base + __popc(mask & ((1u << lane) - 1));
+          if (k < L.cap) {
+            at<double>(ws, L.s_nll)[k] = nll;
+            at<unsigned long long>(ws, L.s_lo)[k] = lo;
+            at<double>(ws, L.s_edge)[k] = edge;
+            at<int>(ws, L.s_row)[k] = b;
+          } else {
+            c->err = 1;
+          }
+        }
+      }
+    }
+    __syncthreads();  // sm reused by the next row's canonical sum
+  }
+}
+
+// --------------------------------------------------------------------------
 // The single-CTA update: select, sort, relabel, threshold, next batch.
 constexpr int kUpdThreads = 1024;
 
@@ -371,6 +493,27 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   const int n_old = c->count;
   const int n_new = min((long long)c->n_surv, L.cap);
   const int n = n_old + n_new;
+  int* lex;
+  const int* par;
+  unsigned long long* lo_arr;
+  int sel, dst;
+  bool has_thr;
+  unsigned long long th, tl;
+  if (n_new == 0) {
+    // no candidate beat the threshold (every row prefiltered away, or only
+    // zero-probability tokens): the materialized list, its lex ranks and the
+    // threshold are unchanged -- only the next batch is picked (steps 1-5 would
+    // reproduce the same sorted list bit for bit)
+    dst = cur;
+    sel = n_old;
+    lex = at<int>(ws, L.m_lex[cur]);
+    par = at<int>(ws, L.m_parent[cur]);
+    lo_arr = at<unsigned long long>(ws, L.m_lo[cur]);
+    has_thr = c->has_thr;
+    th = (unsigned long long)__double_as_longlong(c->thr_nll);
+    tl = c->thr_lo;
+  } else {
+    dst = nxt;
 
   // ---- 1. select the K smallest keys (radix select over 16 8-bit digits) ----
   unsigned long long ph = 0, pl = 0;
@@ -428,7 +571,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     }
   }
   __syncthreads();
-  const int sel = sm.sel_n;  // == min(n, K)
+  sel = sm.sel_n;  // == min(n, K)
   int np2 = 1;
   while (np2 < sel) np2 <<= 1;
   for (int i = sel + tid; i < np2; i += kUpdThreads) {
@@ -482,11 +625,11 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     if (r == 0 || lo_depth(sk_l[r - 1]) != d) sm.depth_start[d] = r;
   }
   __syncthreads();
-  int* lex = at<int>(ws, L.m_lex[nxt]);
+  lex = at<int>(ws, L.m_lex[nxt]);
   for (int r = tid; r < sel; r += kUpdThreads) lex[sk_v[r]] = r - sm.depth_start[lo_depth(sk_l[r])];
   __syncthreads();
-  const int* par = at<int>(ws, L.m_parent[nxt]);
-  unsigned long long* lo_arr = at<unsigned long long>(ws, L.m_lo[nxt]);
+  par = at<int>(ws, L.m_parent[nxt]);
+  lo_arr = at<unsigned long long>(ws, L.m_lo[nxt]);
   for (int pos = tid; pos < sel; pos += kUpdThreads) {
     const unsigned long long lo = lo_arr[pos];
     const int p = par[pos];
@@ -495,15 +638,16 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   __syncthreads();
 
   // ---- 5. threshold ----
-  const bool has_thr = sel >= K;
-  const unsigned long long th = has_thr ? (unsigned long long)__double_as_longlong(at<double>(ws, L.m_nll[nxt])[K - 1]) : 0;
-  const unsigned long long tl = has_thr ? lo_arr[K - 1] : 0;
+  has_thr = sel >= K;
+  th = has_thr ? (unsigned long long)__double_as_longlong(at<double>(ws, L.m_nll[nxt])[K - 1]) : 0;
+  tl = has_thr ? lo_arr[K - 1] : 0;
+  }  // n_new > 0
 
   // ---- 6. next batch: first B unexpanded nodes with depth < D and key < threshold ----
   const int per = (sel + kUpdThreads - 1) / kUpdThreads;
   const int p0 = min(sel, tid * per), p1 = min(sel, p0 + per);
-  const double* nll_arr = at<double>(ws, L.m_nll[nxt]);
-  int* slot_arr = at<int>(ws, L.m_slot[nxt]);
+  const double* nll_arr = at<double>(ws, L.m_nll[dst]);
+  int* slot_arr = at<int>(ws, L.m_slot[dst]);
   auto eligible = [&](int pos) -> bool {
     if (slot_arr[pos] >= 0) return false;
     const unsigned long long lo = lo_arr[pos];
@@ -561,7 +705,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   }
   __syncthreads();
   if (tid == 0) {
-    c->cur = nxt;
+    c->cur = dst;
     c->count = sel;
     c->has_thr = has_thr;
     c->thr_nll = __longlong_as_double((long long)th);
@@ -826,6 +970,14 @@ extern "C" int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot
   return SX_OK;
 }
 
+static int g_tree_unfused = 0;  // sx_tree_set_impl: 1 = the two-kernel row_stats + score path (A/B)
+
+extern "C" int sx_tree_set_impl(int unfused) {
+  if (unfused < 0 || unfused > 1) return arg_error("tree impl %d (0 fused rows kernel, 1 row_stats + score)", unfused);
+  g_tree_unfused = unfused;
+  return SX_OK;
+}
+
 extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
                              int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream) {
   int st = check_tree_args(K, B, V, D);
@@ -846,6 +998,12 @@ extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* r
     dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, B);
     tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, nullptr, -1, V);
     SX_CHECK_LAUNCH("tree_score_kernel");
+  } else if (score_mode == SX_SCORE_RAW && row_kind == SX_ROWS_LOGITS_F32 && !g_tree_unfused) {
+    // persistent: up to 8 resident 256-thread CTAs per SM walk the batch rows
+    const int grid = B < 8 * kNumSMs ? B : 8 * kNumSMs;
+    const int vec4 = (V % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0);
+    tree_logits_rows_kernel<<<grid, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld, vec4);
+    SX_CHECK_LAUNCH("tree_logits_rows_kernel");
   } else if (score_mode == SX_SCORE_RAW) {
     if (row_kind == SX_ROWS_LOGITS_F32) {
       tree_row_stats_kernel<<<B, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld);

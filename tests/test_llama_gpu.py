@@ -202,3 +202,27 @@ def test_fused_qkv_rope_matches_separate_kernels(pair):
     assert (ra - rb).abs().max().item() < TOL
     assert (ka - kb).abs().max().item() <= 2e-2 * max(1.0, ka.abs().max().item())
     assert (va - vb).abs().max().item() <= 2e-2 * max(1.0, va.abs().max().item())
+
+
+@pytest.mark.parametrize("V,K_,B_", [(32000, 1024, 256), (128256, 512, 128)])
+def test_fused_round_kernel_matches_two_kernel_path(cuda, V, K_, B_):
+    """sx_tree_set_impl A/B: the fused persistent row kernel (one HBM read per
+    row) and the tree_row_stats + tree_score pair build the same tree, node for
+    node, on the same draft rows."""
+    from paper_2406_02532_b200 import _lib
+    from paper_2406_02532_b200.llama import LlamaConfig
+
+    cfg = LlamaConfig(V, 256, 2, 2, 1, 512, 1e4, 1e-5, name=f"fused-v{V}")
+    draft = LlamaModel(cfg, seed=9, max_ctx=4 * K_ + 2 * B_ * 13 + 256, max_tokens=max(B_, 64),
+                       synthetic=SyntheticBias(seed=4, rank=64, scale=3.0))
+    prompt = tuple(int(t) for t in np.random.default_rng(V).integers(0, V, size=12))
+    trees = []
+    for impl in (1, 0):
+        _lib.call("sx_tree_set_impl", impl)
+        try:
+            draft.committed.clear()
+            g = sx.build_sssp(prompt, draft, sx.BuilderParams(K_, 12, B_), None, warp_scores=False)
+            trees.append(([(n.parent, n.token, n.edge_logprob) for n in g.nodes], g.rounds))
+        finally:
+            _lib.call("sx_tree_set_impl", 0)
+    assert trees[0] == trees[1]

@@ -1,0 +1,70 @@
+"""Stage-1 selection kernels (sx_tree_round: row statistics + scoring + the
+update) on synthetic fp32 logits rows, per round, against the HBM roofline of
+B x V x 4 bytes read per round. A build = root round + rounds of
+B rows until the batch empties (rows N(0, scale) per round, like random-init
+drafts: scale ~1.3). Prints one JSON line per configuration; `--impl` 1 = the
+two-kernel path (A/B). GPU tool (ncu: one round per launch list).
+
+  python tools/tree_round_bench.py --V 32000 --K 1024 --B 1024
+"""
+import argparse
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2406_02532_b200 import _lib  # noqa: E402
+from paper_2406_02532_b200 import kernels as K  # noqa: E402
+from paper_2406_02532_b200._lib import SCORE_RAW  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--V", type=int, default=32000)
+    ap.add_argument("--K", type=int, default=1024)
+    ap.add_argument("--B", type=int, default=1024)
+    ap.add_argument("--D", type=int, default=16)
+    ap.add_argument("--scale", type=float, default=1.3)
+    ap.add_argument("--builds", type=int, default=5)
+    ap.add_argument("--impl", type=int, default=0)
+    a = ap.parse_args()
+    _lib.call("sx_tree_set_impl", a.impl)
+    peak = 6549.4
+    try:
+        peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+    except OSError:
+        pass
+    ws = K.TreeWorkspace(a.K, a.B, a.V, a.D)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    rows = torch.empty((a.B, a.V), device="cuda")
+    per_round = []  # (batch_n, ms)
+    for bi in range(a.builds + 1):
+        ws.begin()
+        n = 1
+        while True:
+            rows[:n].normal_(0.0, a.scale, generator=g)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ws.launch_round(rows, SCORE_RAW)
+            e1.record()
+            ctl = ws.read_ctl()
+            if bi > 0:
+                per_round.append((n, e0.elapsed_time(e1)))
+            n = ctl["batch_n"]
+            if n == 0:
+                break
+    full = [(n, ms) for n, ms in per_round if n == a.B]
+    out = {"V": a.V, "K": a.K, "B": a.B, "scale": a.scale, "impl": "fused" if a.impl == 0 else "row_stats+score",
+           "rounds_per_build": len(per_round) / a.builds}
+    if full:
+        ms = sum(x for _, x in full) / len(full)
+        gbs = a.B * a.V * 4 / (ms / 1e3) / 1e9
+        out.update({"full_rounds": len(full), "us_per_full_round": ms * 1e3, "bytes_per_round": a.B * a.V * 4,
+                    "achieved_GBps": gbs, "hbm_peak_GBps": peak, "frac": gbs / peak})
+    out["us_per_round_all"] = [round(x * 1e3, 1) for _, x in per_round[: 12]]
+    out["batch_sizes"] = [n for n, _ in per_round[: 12]]
+    print(json.dumps(out))
+
+
+main()
