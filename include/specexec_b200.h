@@ -69,6 +69,9 @@ enum {
 };
 /* 0 = auto (default: CTA-pair cta_group::2 tiles for M >= 256 tokens), 1 = single-CTA only, 2 = pair when legal */
 SX_API int sx_gemm_set_pair_mode(int mode);
+/* 1 (default) = M <= 4 tokens run the weight-streaming matrix-vector kernel (same
+ * epilogues except SWIGLU_BF16 / RS_BF16); 0 = always the tcgen05 tile kernel (A/B) */
+SX_API int sx_gemm_set_gemv(int enabled);
 SX_API int sx_gemm_plan(int M, int N, int K, int dual, int splits_req, int* bn_out, int* splits_out,
                  long long* ws_floats_out);
 SX_API int sx_gemm_bf16(const void* W, const void* W2, const void* X, void* out, float* ws, long long ws_floats,
@@ -118,10 +121,26 @@ SX_API int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows,
                          int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream);
 SX_API int sx_tree_finalize(void* ws, int K, int B, int V, int D, int root_token, int* out_parent, int* out_token,
                             double* out_edge, int* out_depth, int* out_slot, cudaStream_t stream);
-/* Raw scoring of fp32 logits rows: 0 (default) = one fused persistent kernel
- * (row statistics + exact scoring, one HBM read per row), 1 = the two-kernel
- * tree_row_stats + tree_score path (A/B measurement; identical results). */
+/* Raw scoring of fp32 logits rows: 0 (default) = the chunked path (max / sum /
+ * score kernels over (row, chunk) units, one HBM read per prefiltered row), 1 =
+ * the two-kernel tree_row_stats + tree_score path (A/B; identical results). */
 SX_API int sx_tree_set_impl(int unfused);
+/* Survivor buffer (candidates of one round that beat the threshold): capacity
+ * min(B*V, max(V + K, 2^24)) entries (sx_tree_survivor_cap). A round whose
+ * survivors overflow it leaves the tree untouched and reports ctl->err (int 8
+ * of host_ctl); the caller then clears the flag (sx_tree_clear_overflow) and
+ * re-runs the SAME rows in slices [r0, r1) of at most cap / V rows with
+ * sx_tree_round_rows: final = 0 merges a slice's survivors (keeping the K best,
+ * remapping the batch), final = 1 on the last slice also picks the next batch --
+ * the same tree as one unbounded round. sx_tree_round == rows [0, batch_n),
+ * final = 1. sx_tree_set_survivor_cap overrides the capacity of workspaces
+ * laid out afterwards (0 = default; tests). */
+SX_API long long sx_tree_survivor_cap(int K, int B, int V, int D);
+SX_API int sx_tree_set_survivor_cap(long long cap);
+SX_API int sx_tree_clear_overflow(void* ws, int K, int B, int V, int D, cudaStream_t stream);
+SX_API int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
+                              int score_mode, double temperature, double top_p, int r0, int r1, int final,
+                              int* host_ctl, cudaStream_t stream);
 
 /* ------------------------------------------------ exact table models on GPU
  * MarkovModel / TabularModel (pkg/src/speckit/models.py:77-151) rows for tree

@@ -27,6 +27,7 @@ SIGNATURES: dict[str, tuple] = {
     "sx_last_error": (ctypes.c_char_p, []),
     "sx_launch_count": (_c_ll, []),
     "sx_gemm_set_pair_mode": (_c_int, [_c_int]),
+    "sx_gemm_set_gemv": (_c_int, [_c_int]),
     "sx_gemm_plan": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _ip, _ip, _llp]),
     "sx_gemm_bf16": (
         _c_int,
@@ -40,6 +41,14 @@ SIGNATURES: dict[str, tuple] = {
         [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl, _vp, _vp],
     ),
     "sx_tree_set_impl": (_c_int, [_c_int]),
+    "sx_tree_survivor_cap": (_c_ll, [_c_int, _c_int, _c_int, _c_int]),
+    "sx_tree_set_survivor_cap": (_c_int, [_c_ll]),
+    "sx_tree_clear_overflow": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "sx_tree_round_rows": (
+        _c_int,
+        [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl, _c_int, _c_int, _c_int,
+         _vp, _vp],
+    ),
     "sx_tree_finalize": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sx_markov_rows": (
         _c_int,

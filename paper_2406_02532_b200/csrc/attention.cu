@@ -99,6 +99,7 @@ struct AttnSmem {
 };
 
 __global__ void __launch_bounds__(kAttWarps * 32) tree_attention_kernel(const AttnArgs a) {
+  griddep_launch_dependents();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   AttnSmem& sm = *reinterpret_cast<AttnSmem*>(smem_raw);
 
@@ -467,6 +468,7 @@ SX_DEV void merge_splits(const AttnArgs& a, TcSmemHdr& hd, int kvh, int zsplit, 
 }
 
 __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const AttnArgs a) {
+  griddep_launch_dependents();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   TcSmemHdr& hd = *reinterpret_cast<TcSmemHdr*>(base);

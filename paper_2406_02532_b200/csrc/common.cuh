@@ -106,6 +106,23 @@ SX_DEV void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
 }
 // Programmatic dependent launch: wait for the preceding grid (and its memory)
 SX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ... and let the next grid (if launched with programmatic stream serialization)
+// become resident now: it prefetches what does not depend on this grid, then
+// waits in griddepcontrol.wait for this grid's completion. A no-op otherwise.
+SX_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// 1-D bulk copy global -> shared (16-B aligned, bytes a multiple of 16), completing
+// `bytes` of transaction on the mbarrier; L2 policy hint
+SX_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// L2 prefetch of `bytes` (multiple of 16, 16-B aligned) contiguous global bytes
+SX_DEV void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 // TMA load multicast to the CTAs of `mask` in the cluster (same smem offset;
 // complete_tx lands on each destination CTA's barrier at the same offset)
 SX_DEV void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask,

@@ -43,6 +43,7 @@
 // so each thread writes 16-byte runs along the feature dimension.
 #include "capi_util.h"
 #include "common.cuh"
+#include "gemv.h"
 #include "specexec_b200.h"
 
 namespace sx {
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t mrank = MC > 1 ? cluster_ctarank() : 0u;  // position in the multicast cluster
   const int unit = blockIdx.x / (CG * MC);
 
+  griddep_launch_dependents();  // a PDL-launched successor may set up while this grid runs
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapA);
     if (DUAL) tma_prefetch_desc(&mapA2);
@@ -1021,6 +1023,32 @@ static int gemm_launch(const void* W, const void* W2, const void* X, void* out, 
   if (M <= 0 || Nf <= 0 || K <= 0 || (K % 64) != 0)
     return arg_error("sx_gemm: need M,N > 0 and K a positive multiple of 64 (M=%d N=%d K=%d)", M, Nf, K);
   int st;
+  if (gemv_applies(M, epi, dual)) {  // 1..4 tokens: weight-streaming matrix-vector path (gemv.cu)
+    GemvArgs v{};
+    v.W = reinterpret_cast<const __nv_bfloat16*>(W);
+    v.X = reinterpret_cast<const __nv_bfloat16*>(X);
+    v.out = out;
+    v.ldo = ldo;
+    v.M = M;
+    v.Nf = Nf;
+    v.K = K;
+    v.epi = epi;
+    if (rope) {
+      v.rope_pos = rope->rope_pos;
+      v.rope_slot = rope->rope_slot;
+      v.rope_pos_base = rope->rope_pos_base;
+      v.rope_slot_base = rope->rope_slot_base;
+      v.rope_H = rope->rope_H;
+      v.rope_KVH = rope->rope_KVH;
+      v.rope_cos = rope->rope_cos;
+      v.rope_sin = rope->rope_sin;
+      v.rope_q = rope->rope_q;
+      v.rope_kc = rope->rope_kc;
+      v.rope_vc = rope->rope_vc;
+      v.rope_slots = rope->rope_slots;
+    }
+    return launch_gemv(v, stream);
+  }
   Plan p = make_plan(M, Nf, K, dual, splits_req);
   if (p.ws_floats > 0 && (ws == nullptr || ws_floats < p.ws_floats))
     return arg_error("sx_gemm: stream-K workspace needs %lld floats, got %lld", p.ws_floats, ws_floats);

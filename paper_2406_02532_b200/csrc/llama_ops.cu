@@ -16,6 +16,7 @@ namespace sx {
 
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int* __restrict__ tokens, int n, int d,
                              float* __restrict__ x) {
+  griddep_launch_dependents();
   const int t = blockIdx.x;
   if (t >= n) return;
   const long long tok = tokens[t];
@@ -26,6 +27,7 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int* __r
 
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w, int d, float eps,
                                __nv_bfloat16* __restrict__ y) {
+  griddep_launch_dependents();
   const int t = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + (long long)t * d);
   float ss = 0.f;
@@ -75,6 +77,7 @@ SX_DEV float4 ld4<__nv_bfloat16>(const __nv_bfloat16* p, int i) {
 template <typename T>
 __global__ void add_rmsnorm_kernel(float* __restrict__ x, const T* __restrict__ yin, const __nv_bfloat16* __restrict__ w,
                                    int d, float eps, __nv_bfloat16* __restrict__ out) {
+  griddep_launch_dependents();
   const int t = blockIdx.x;
   float4* xr = reinterpret_cast<float4*>(x + (long long)t * d);
   const T* yr = yin + (long long)t * d;

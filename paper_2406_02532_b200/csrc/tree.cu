@@ -19,18 +19,25 @@
 //   sx_tree_score  : canonical float64 probabilities of every batch row (from
 //                    fp32 logits, fp64 probabilities, or a warped row), edge =
 //                    sx_log(p), nll = parent_nll - edge, keep key < threshold.
-//   sx_tree_update : ONE CTA. Radix-select (8-bit digits over the 128-bit key)
-//                    of the K best of materialized U survivors, bitonic sort in
-//                    shared memory, parent remap, lex-rank recompute (sort by lo),
-//                    new threshold = K-th key, next batch = first B unexpanded
-//                    nodes with depth < D and key < threshold, their draft-KV
-//                    slots and ancestor-slot lists.
+//   sx_tree_update : a cluster of kUpdCluster CTAs. Radix select (8-bit digits
+//                    over the 128-bit key) of the K best of materialized U
+//                    survivors: every CTA histograms its slice of the keys, the
+//                    histograms are summed over distributed shared memory and
+//                    the bin is found by a parallel scan in every CTA (identical
+//                    result, no broadcast); the selected keys are gathered into
+//                    CTA 0's shared memory. CTA 0 then bitonic-sorts them, remaps
+//                    parents, recomputes lex ranks (sort by lo), sets the new
+//                    threshold = K-th key and picks the next batch = first B
+//                    unexpanded nodes with depth < D and key < threshold, their
+//                    draft-KV slots and ancestor-slot lists.
 #include "capi_util.h"
 #include "common.cuh"
 #include "specexec_b200.h"
 #include "sxmath.cuh"
 #include "tree_layout.h"
 #include "warp_rows.cuh"
+
+#include <cooperative_groups.h>
 
 namespace sx {
 
@@ -44,6 +51,11 @@ SX_DEV unsigned long long make_lo(int depth, int plex, int token) {
 }
 SX_DEV int lo_depth(unsigned long long lo) { return (int)(lo >> 56); }
 SX_DEV int lo_token(unsigned long long lo) { return (int)(lo & 0xffffffffu); }
+
+// Scoring kernels take the batch-row range [r0, r1) of this launch (r1 < 0: up to
+// batch_n) -- the whole batch normally; slices of it when a round overflowed the
+// survivor buffer and is re-run in parts (sx_tree_round_rows).
+SX_DEV int rows_end(const TreeCtl* c, int r1) { return r1 < 0 ? c->batch_n : min(r1, c->batch_n); }
 
 SX_DEV bool key_less(unsigned long long ah, unsigned long long al, unsigned long long bh, unsigned long long bl) {
   return ah < bh || (ah == bh && al < bl);
@@ -65,6 +77,7 @@ __global__ void tree_begin_kernel(uint8_t* ws, TreeLayout L, int root_slot, int 
   c->err = 0;
   c->thr_nll = 0.0;
   c->thr_lo = 0ull;
+  at<int>(ws, L.r_aux)[0] = 0;
   at<int>(ws, L.b_node)[0] = -1;
   at<double>(ws, L.b_nll)[0] = 0.0;
   at<int>(ws, L.b_depth)[0] = 0;
@@ -79,21 +92,26 @@ __global__ void tree_begin_kernel(uint8_t* ws, TreeLayout L, int root_slot, int 
 // Canonical warp of each batch row (t > 0 scoring): w_rows[b] = apply_warp(row b).
 __global__ void __launch_bounds__(kRowThreads) tree_warp_rows_kernel(uint8_t* ws, TreeLayout L, const void* rows,
                                                                        int row_kind, long long ld, double temperature,
-                                                                       double top_p) {
+                                                                       double top_p, int r0, int r1) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
-  const int b = blockIdx.x;
-  if (b >= c->batch_n) return;
   const int V = L.V;
-  const float* z = row_kind == SX_ROWS_LOGITS_F32 ? reinterpret_cast<const float*>(rows) + b * ld : nullptr;
-  const double* p = row_kind == SX_ROWS_PROBS_F64 ? reinterpret_cast<const double*>(rows) + b * ld : nullptr;
-  double* out = at<double>(ws, L.w_rows) + (long long)b * V;
-  unsigned long long* k1 = at<unsigned long long>(ws, L.w_keys) + (long long)b * V;
-  unsigned long long* k2 = at<unsigned long long>(ws, L.w_keys2) + (long long)b * V;
-  int* i1 = at<int>(ws, L.w_idx) + (long long)b * V;
-  int* i2 = at<int>(ws, L.w_idx2) + (long long)b * V;
-  warp_row(sm, z, p, V, temperature, top_p, out, k1, i1, k2, i2);
+  // persistent over the batch rows; the radix-sort scratch belongs to the CTA
+  // (kWarpScratchRows rows of V), not to the row -- 148 x V instead of B x V
+  const long long sc = (long long)blockIdx.x * V;
+  unsigned long long* k1 = at<unsigned long long>(ws, L.w_keys) + sc;
+  unsigned long long* k2 = at<unsigned long long>(ws, L.w_keys2) + sc;
+  int* i1 = at<int>(ws, L.w_idx) + sc;
+  int* i2 = at<int>(ws, L.w_idx2) + sc;
+  const int re = rows_end(c, r1);
+  for (int b = r0 + blockIdx.x; b < re; b += gridDim.x) {
+    const float* z = row_kind == SX_ROWS_LOGITS_F32 ? reinterpret_cast<const float*>(rows) + b * ld : nullptr;
+    const double* p = row_kind == SX_ROWS_PROBS_F64 ? reinterpret_cast<const double*>(rows) + b * ld : nullptr;
+    double* out = at<double>(ws, L.w_rows) + (long long)b * V;
+    warp_row(sm, z, p, V, temperature, top_p, out, k1, i1, k2, i2);
+    __syncthreads();  // sm and the scratch are reused by the next row
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -112,11 +130,11 @@ __global__ void __launch_bounds__(kRowThreads) tree_warp_rows_kernel(uint8_t* ws
 constexpr double kPrefilterSlack = 1e-3;
 
 __global__ void __launch_bounds__(kRowThreads) tree_row_stats_kernel(uint8_t* ws, TreeLayout L, const float* rows,
-                                                                       long long ld) {
+                                                                       long long ld, int r0, int r1) {
   __shared__ RowSmemLite sm;
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
-  const int b = blockIdx.x;
-  if (b >= c->batch_n) return;
+  const int b = r0 + blockIdx.x;
+  if (b >= rows_end(c, r1)) return;
   const float* z = rows + b * ld;
   const int V = L.V;
   float mx = -CUDART_INF_F;
@@ -149,12 +167,12 @@ __global__ void __launch_bounds__(kRowThreads) tree_row_stats_kernel(uint8_t* ws
 
 // Argmax rows (t = 0 warped scoring): one child per row with p = 1, edge = log(1) = 0.
 __global__ void __launch_bounds__(kRowThreads) tree_argmax_score_kernel(uint8_t* ws, TreeLayout L, const void* rows,
-                                                                          int row_kind, long long ld) {
+                                                                          int row_kind, long long ld, int r0, int r1) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
-  const int b = blockIdx.x;
-  if (b >= c->batch_n) return;
+  const int b = r0 + blockIdx.x;
+  if (b >= rows_end(c, r1)) return;
   double bv = -CUDART_INF;
   int bi = 0x7fffffff;
   for (int v = threadIdx.x; v < L.V; v += kRowThreads) {
@@ -173,10 +191,14 @@ __global__ void __launch_bounds__(kRowThreads) tree_argmax_score_kernel(uint8_t*
     const unsigned long long lo = make_lo(at<int>(ws, L.b_depth)[b] + 1, at<int>(ws, L.b_lex)[b], best);
     if (!c->has_thr || key_less(hi, lo, (unsigned long long)__double_as_longlong(c->thr_nll), c->thr_lo)) {
       const int k = atomicAdd(&c->n_surv, 1);
-      at<double>(ws, L.s_nll)[k] = nll;
-      at<unsigned long long>(ws, L.s_lo)[k] = lo;
-      at<double>(ws, L.s_edge)[k] = 0.0;
-      at<int>(ws, L.s_row)[k] = b;
+      if (k < L.cap) {
+        at<double>(ws, L.s_nll)[k] = nll;
+        at<unsigned long long>(ws, L.s_lo)[k] = lo;
+        at<double>(ws, L.s_edge)[k] = 0.0;
+        at<int>(ws, L.s_row)[k] = b;
+      } else {
+        c->err = 1;
+      }
     }
   }
 }
@@ -184,10 +206,10 @@ __global__ void __launch_bounds__(kRowThreads) tree_argmax_score_kernel(uint8_t*
 // Score every (row, token): grid (chunks, B). mode: probabilities (fp64 rows or the
 // warped rows) or logits (fp32 + row stats).
 __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout L, const void* rows, int row_kind,
-                                                           long long ld) {
+                                                           long long ld, int r0, int r1) {
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
-  const int b = blockIdx.y;
-  if (b >= c->batch_n) return;
+  const int b = r0 + blockIdx.y;
+  if (b >= rows_end(c, r1)) return;
   const int V = L.V;
   const double parent_nll = at<double>(ws, L.b_nll)[b];
   const int depth = at<int>(ws, L.b_depth)[b] + 1;
@@ -250,33 +272,50 @@ __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout
 }
 
 // --------------------------------------------------------------------------
-// Fused row statistics + scoring for fp32 logits rows (raw scoring): a
-// persistent grid walks the batch rows, one 256-thread CTA per row at a time.
-//   pass 1  one HBM read of the row (16-byte loads): exact max and an online
-//           fp32 sum of exp(z - max) -- the prefilter estimate; rows whose best
-//           child cannot beat the threshold stop here (the common case once the
-//           tree holds K nodes);
-//   pass 2  canonical fp64 sum (lane t sums v = t, t + 256, ... then the
-//           halving tree -- the same order as tree_row_stats_kernel), from L2;
-//   pass 3  exact edges / keys of the prefiltered candidates, survivors appended.
-// Bit-identical to tree_row_stats + tree_score (the prefilter only decides
-// which candidates take the exact path, with 1e-3 of slack against an
-// estimate good to ~1e-5), with one read of the row instead of two plus a
-// 64 x B grid of mostly-empty score CTAs.
-__global__ void __launch_bounds__(kRowThreads) tree_logits_rows_kernel(uint8_t* ws, TreeLayout L,
-                                                                         const float* __restrict__ rows, long long ld,
-                                                                         int vec4) {
-  __shared__ RowSmemLite sm;
-  __shared__ float red_m[kRowThreads / 32], red_s[kRowThreads / 32];
+// Chunked logits-row path (raw scoring of fp32 logits rows), three persistent
+// kernels over (row, chunk) work units so that a round of any batch size
+// spreads over the whole GPU -- a one-row root round included:
+//   max    units of kRowChunkA elements: one HBM read (16-byte streaming loads),
+//          chunk max + online fp32 sum of exp(z - max). The last chunk of a row
+//          to arrive combines the partials in chunk order: exact row max M and
+//          the fp32 estimate S~ (prefilter only). Rows whose best child cannot
+//          beat the threshold stop here -- the common case once the tree holds
+//          K nodes; the others are appended to the work list.
+//   sum    units of kRowChunkB elements of the listed rows: e_v =
+//          sx_exp(z_v - M) into the fp64 row scratch; the last chunk to arrive
+//          forms the canonical sum (lane t adds e_t, e_t+256, ... then the
+//          halving tree -- the order of tree_row_stats_kernel / oxmath.c).
+//   score  units of kRowChunkB elements of the listed rows: exact edges
+//          sx_log(e_v / S) and keys of the candidates the fp32 estimate cannot
+//          rule out; survivors appended.
+// Bit-identical to tree_row_stats + tree_score: the prefilter only decides
+// which candidates take the exact path (1e-3 of slack against an estimate
+// good to ~1e-5), and e_v / S are the same canonical values.
+constexpr int kMaxThreads = 128;  // max-pass CTA: small, so >= 1024 of them are resident (one row each at B = 1024)
+
+__global__ void __launch_bounds__(kMaxThreads) tree_rows_max_kernel(uint8_t* ws, TreeLayout L,
+                                                                     const float* __restrict__ rows, long long ld,
+                                                                     int vec4, int r0, int r1) {
+  __shared__ float red_m[kMaxThreads / 32], red_s[kMaxThreads / 32];
+  __shared__ int last_s;
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
-  const int batch_n = c->batch_n, V = L.V, tid = threadIdx.x, lane = tid & 31;
-  const bool has_thr = c->has_thr;
-  const double thr_nll = c->thr_nll;
-  const unsigned long long th = (unsigned long long)__double_as_longlong(thr_nll);
-  const unsigned long long tl = c->thr_lo;
-  for (int b = blockIdx.x; b < batch_n; b += gridDim.x) {
+  const int batch_n = rows_end(c, r1) - r0, V = L.V, tid = threadIdx.x, lane = tid & 31;
+  // Work units: whole rows when the batch fills the grid (no cross-CTA combine),
+  // else each row cut into enough chunks (multiples of kRowChunkA elements) to
+  // give every CTA work -- the one-row root round spreads over up to 64 CTAs.
+  int clen = V;
+  if (2 * batch_n <= (int)gridDim.x) {  // whole units per CTA: floor, so no CTA gets one unit more than the rest
+    const int per = min(kRowChunksMax, (int)gridDim.x / batch_n);
+    clen = ((V + per - 1) / per + kRowChunkA - 1) / kRowChunkA * kRowChunkA;
+  }
+  const int nch = (V + clen - 1) / clen;
+  float* pm = at<float>(ws, L.r_pm);
+  float* ps = at<float>(ws, L.r_ps);
+  int* cnt = at<int>(ws, L.r_cnt);
+  for (int u = blockIdx.x; u < batch_n * nch; u += gridDim.x) {
+    const int b = r0 + u / nch, j = u % nch;
+    const int v0 = j * clen, v1 = min(V, v0 + clen);
     const float* z = rows + b * ld;
-    // ---- pass 1: max and online fp32 sum of exp(z - max)
     float m = -CUDART_INF_F, sacc = 0.f;
     auto acc1 = [&](float x) {
       if (x > m) {
@@ -286,24 +325,20 @@ __global__ void __launch_bounds__(kRowThreads) tree_logits_rows_kernel(uint8_t* 
         sacc += __expf(x - m);
       }
     };
-    if (vec4) {
-      const float4* z4 = reinterpret_cast<const float4*>(z);
-      const int V4 = V >> 2;
-      int v = tid;
-      for (; v + 3 * kRowThreads < V4; v += 4 * kRowThreads) {  // 4 loads in flight per thread
-        const float4 a0 = __ldcs(z4 + v), a1 = __ldcs(z4 + v + kRowThreads), a2 = __ldcs(z4 + v + 2 * kRowThreads),
-                     a3 = __ldcs(z4 + v + 3 * kRowThreads);
-        acc1(a0.x), acc1(a0.y), acc1(a0.z), acc1(a0.w);
-        acc1(a1.x), acc1(a1.y), acc1(a1.z), acc1(a1.w);
-        acc1(a2.x), acc1(a2.y), acc1(a2.z), acc1(a2.w);
-        acc1(a3.x), acc1(a3.y), acc1(a3.z), acc1(a3.w);
-      }
-      for (; v < V4; v += kRowThreads) {
-        const float4 a0 = z4[v];
-        acc1(a0.x), acc1(a0.y), acc1(a0.z), acc1(a0.w);
+    if (vec4) {  // chunk bounds are multiples of 4; 4 loads per thread in flight
+      const float4* z4 = reinterpret_cast<const float4*>(z + v0);
+      const int n4 = (v1 - v0) >> 2;
+      for (int i = tid; i < n4; i += 8 * kMaxThreads) {  // 8 x 16 B per thread in flight, tail included
+        float4 a[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (i + k * kMaxThreads < n4) a[k] = __ldcs(z4 + i + k * kMaxThreads);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (i + k * kMaxThreads < n4) acc1(a[k].x), acc1(a[k].y), acc1(a[k].z), acc1(a[k].w);
       }
     } else {
-      for (int v = tid; v < V; v += kRowThreads) acc1(z[v]);
+      for (int v = v0 + tid; v < v1; v += kMaxThreads) acc1(z[v]);
     }
     for (int o = 16; o > 0; o >>= 1) {
       const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sacc, o);
@@ -316,31 +351,122 @@ __global__ void __launch_bounds__(kRowThreads) tree_logits_rows_kernel(uint8_t* 
       red_s[tid >> 5] = sacc;
     }
     __syncthreads();
-    float M = red_m[0];
-    for (int w = 1; w < kRowThreads / 32; ++w) M = fmaxf(M, red_m[w]);
-    float S_est = 0.f;
-    for (int w = 0; w < kRowThreads / 32; ++w)
-      if (red_m[w] != -CUDART_INF_F) S_est += red_s[w] * __expf(red_m[w] - M);
-    __syncthreads();  // red_* reused by the next row
-    const float lsa = logf(S_est);
+    if (tid == 0) {
+      float M = red_m[0];
+      for (int w = 1; w < kMaxThreads / 32; ++w) M = fmaxf(M, red_m[w]);
+      float S = 0.f;
+      for (int w = 0; w < kMaxThreads / 32; ++w)
+        if (red_m[w] != -CUDART_INF_F) S += red_s[w] * __expf(red_m[w] - M);
+      if (nch > 1) {
+        pm[b * kRowChunksMax + j] = M;
+        ps[b * kRowChunksMax + j] = S;
+        __threadfence();
+        last_s = atomicAdd(&cnt[b], 1) == nch - 1;
+      } else {
+        last_s = 1;
+        red_m[0] = M;
+        red_s[0] = S;
+      }
+    }
+    __syncthreads();
+    if (last_s && tid < 32) {  // warp 0 finishes the row (the last of its chunks to arrive)
+      float RM = red_m[0], RS = red_s[0];
+      if (nch > 1) {  // combine the partials (nch <= 64: two per lane, fixed shuffle order)
+        __threadfence();
+        const float m0 = lane < nch ? __ldcg(pm + b * kRowChunksMax + lane) : -CUDART_INF_F;
+        const float m1 = lane + 32 < nch ? __ldcg(pm + b * kRowChunksMax + lane + 32) : -CUDART_INF_F;
+        const float s0 = lane < nch ? __ldcg(ps + b * kRowChunksMax + lane) : 0.f;
+        const float s1 = lane + 32 < nch ? __ldcg(ps + b * kRowChunksMax + lane + 32) : 0.f;
+        RM = fmaxf(m0, m1);
+        for (int o = 16; o > 0; o >>= 1) RM = fmaxf(RM, __shfl_xor_sync(0xffffffffu, RM, o));
+        RS = (m0 == -CUDART_INF_F ? 0.f : s0 * __expf(m0 - RM)) + (m1 == -CUDART_INF_F ? 0.f : s1 * __expf(m1 - RM));
+        for (int o = 16; o > 0; o >>= 1) RS += __shfl_xor_sync(0xffffffffu, RS, o);
+      }
+      if (lane == 0) {
+        const float lsa = logf(RS);
+        const double parent_nll = at<double>(ws, L.b_nll)[b];
+        const bool skip = c->has_thr && dsub(dadd(parent_nll, (double)lsa), kPrefilterSlack) > c->thr_nll;
+        at<float>(ws, L.r_max)[b] = RM;
+        at<float>(ws, L.r_lsa)[b] = skip ? -CUDART_INF_F : lsa;
+        if (nch > 1) cnt[b] = 0;
+        if (!skip) at<int>(ws, L.r_list)[atomicAdd(at<int>(ws, L.r_aux), 1)] = b;
+      }
+    }
+    __syncthreads();  // red_* reused by the next unit
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) tree_rows_sum_kernel(uint8_t* ws, TreeLayout L,
+                                                                     const float* __restrict__ rows, long long ld) {
+  __shared__ RowSmemLite sm;
+  __shared__ int last;
+  const int V = L.V, tid = threadIdx.x;
+  const int nwork = *(volatile int*)at<int>(ws, L.r_aux);
+  const int nch = (V + kRowChunkB - 1) / kRowChunkB;
+  int* cnt = at<int>(ws, L.r_cnt) + L.B;
+  for (int u = blockIdx.x; u < nwork * nch; u += gridDim.x) {
+    const int w = u / nch, j = u - w * nch;
+    const int b = at<int>(ws, L.r_list)[w];
+    const float* z = rows + b * ld;
+    const double M = (double)at<float>(ws, L.r_max)[b];
+    double* e = at<double>(ws, L.w_rows) + (long long)b * V;
+    const int v1 = min(V, (j + 1) * kRowChunkB);
+    for (int v = j * kRowChunkB + tid; v < v1; v += kRowThreads) e[v] = sx_exp(dsub((double)z[v], M));
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&cnt[b], 1) == nch - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      double acc = 0.0;  // canonical sum: lane t adds e_t, e_t+256, ... in order
+      int v = tid;
+      for (; v + 7 * kRowThreads < V; v += 8 * kRowThreads) {  // 8 independent loads, then the ordered adds
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __ldcg(e + v + k * kRowThreads);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = dadd(acc, x[k]);
+      }
+      for (; v < V; v += kRowThreads) acc = dadd(acc, __ldcg(e + v));
+      const double S = block_canon_sum(sm, acc);
+      if (tid == 0) {
+        at<double>(ws, L.r_sum)[b] = S;
+        cnt[b] = 0;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) tree_rows_score_kernel(uint8_t* ws, TreeLayout L,
+                                                                       const float* __restrict__ rows, long long ld) {
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int V = L.V, tid = threadIdx.x, lane = tid & 31;
+  const int nwork = at<int>(ws, L.r_aux)[0];
+  const int nch = (V + kRowChunkB - 1) / kRowChunkB;
+  const bool has_thr = c->has_thr;
+  const double thr_nll = c->thr_nll;
+  const unsigned long long th = (unsigned long long)__double_as_longlong(thr_nll);
+  const unsigned long long tl = c->thr_lo;
+  for (int u = blockIdx.x; u < nwork * nch; u += gridDim.x) {
+    const int w = u / nch, j = u - w * nch;
+    const int b = at<int>(ws, L.r_list)[w];
+    const float* z = rows + b * ld;
+    const float M = at<float>(ws, L.r_max)[b], lsa = at<float>(ws, L.r_lsa)[b];
+    const double S = at<double>(ws, L.r_sum)[b];
     const double parent_nll = at<double>(ws, L.b_nll)[b];
-    if (has_thr && dsub(dadd(parent_nll, (double)lsa), kPrefilterSlack) > thr_nll) continue;  // no child survives
-    // ---- pass 2: canonical fp64 sum
-    double acc = 0.0;
-    for (int v = tid; v < V; v += kRowThreads) acc = dadd(acc, sx_exp(dsub((double)z[v], (double)M)));
-    const double S = block_canon_sum(sm, acc);
-    // ---- pass 3: exact keys of the candidates the fp32 estimate cannot rule out
     const int depth = at<int>(ws, L.b_depth)[b] + 1;
     const int plex = at<int>(ws, L.b_lex)[b];
-    for (int v0 = 0; v0 < V; v0 += kRowThreads) {
-      const int v = v0 + tid;
+    const double* e = at<double>(ws, L.w_rows) + (long long)b * V;
+    const int v0 = j * kRowChunkB;
+    for (int vb = v0; vb < v0 + kRowChunkB; vb += kRowThreads) {  // whole warps iterate (ballot)
+      const int v = vb + tid;
       bool keep = false;
       double nll = 0.0, edge = 0.0;
       unsigned long long lo = 0;
       if (v < V) {
         const float zv = z[v];
         if (!has_thr || !(dsub(dsub(parent_nll, (double)((zv - M) - lsa)), kPrefilterSlack) > thr_nll)) {
-          const double pv = ddiv(sx_exp(dsub((double)zv, (double)M)), S);
+          const double pv = ddiv(e[v], S);
           if (pv > 0.0) {
             edge = sx_log(pv);
             nll = dsub(parent_nll, edge);
@@ -367,16 +493,18 @@ __global__ void __launch_bounds__(kRowThreads) tree_logits_rows_kernel(uint8_t* 
         }
       }
     }
-    __syncthreads();  // sm reused by the next row's canonical sum
   }
 }
 
 // --------------------------------------------------------------------------
 // The single-CTA update: select, sort, relabel, threshold, next batch.
 constexpr int kUpdThreads = 1024;
+constexpr int kUpdCluster = 8;  // CTAs sharing the radix-select histograms (portable cluster size)
+constexpr int kUpdBatch = 8;    // independent key loads per thread before the histogram votes
 
 struct UpdSmem {
-  int hist[256];
+  int hist[2][256];  // this CTA's histogram of the current digit (double-buffered across digits)
+  int wsum[8];
   int bin;
   int rank;
   int done;
@@ -479,26 +607,52 @@ SX_DEV int block_excl_scan(UpdSmem& sm, int v, int& excl) {
   return total;
 }
 
-__global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws, TreeLayout L) {
+// final = 0: merge only (a slice of an overflowed round, sx_tree_round_rows): the
+// materialized list, lex ranks and threshold take in this slice's survivors and
+// the current batch is remapped to the new positions; the next batch is picked
+// by the last slice (final = 1), as in an ordinary round.
+__global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws, TreeLayout L, int final) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
   unsigned long long* sk_h = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(UpdSmem) + 15) & ~size_t(15)));
   unsigned long long* sk_l = sk_h + L.kpad;
   int* sk_v = reinterpret_cast<int*>(sk_l + L.kpad);
 
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned crank = cluster.block_rank();
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int tid = threadIdx.x;
   const int K = L.K;
+  if (c->err) {
+    // survivor buffer overflow: some candidates of this round were dropped, so
+    // leave the tree untouched; the host re-runs the round in row slices whose
+    // survivors fit (sx_tree_round_rows). err stays set for the host to see.
+    if (crank == 0 && tid == 0) {
+      c->n_surv = 0;
+      at<int>(ws, L.r_aux)[0] = 0;
+    }
+    return;
+  }
   const int cur = c->cur, nxt = cur ^ 1;
   const int n_old = c->count;
   const int n_new = min((long long)c->n_surv, L.cap);
   const int n = n_old + n_new;
+  // every CTA has read the control block before CTA 0 can rewrite it: CTA 0 only
+  // writes after the cluster barriers of steps 1-2 (n_new > 0), and with
+  // n_new == 0 the other CTAs have nothing to do
+  if (n_new == 0 && crank != 0) return;
+  const int i0 = (int)((long long)n * crank / kUpdCluster), i1 = (int)((long long)n * (crank + 1) / kUpdCluster);
   int* lex;
   const int* par;
   unsigned long long* lo_arr;
   int sel, dst;
   bool has_thr;
   unsigned long long th, tl;
+  if (n_new == 0 && !final) {  // merge-only slice with nothing to merge
+    if (tid == 0) at<int>(ws, L.r_aux)[0] = 0;
+    return;
+  }
   if (n_new == 0) {
     // no candidate beat the threshold (every row prefiltered away, or only
     // zero-probability tokens): the materialized list, its lex ranks and the
@@ -516,33 +670,64 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     dst = nxt;
 
   // ---- 1. select the K smallest keys (radix select over 16 8-bit digits) ----
+  // Every CTA of the cluster histograms its slice [i0, i1) of the n keys; the
+  // 256-bin totals are summed over DSMEM and scanned in parallel by every CTA.
   unsigned long long ph = 0, pl = 0;
   int ndig = 0;  // digits fixed in the prefix
-  bool select_all = n <= K;
+  const bool select_all = n <= K;
   if (!select_all) {
-    if (tid == 0) {
-      sm.rank = K;
-      sm.done = 0;
-    }
-    __syncthreads();
+    int rank = K;
     for (int d = 0; d < 16; ++d) {
-      for (int i = tid; i < 256; i += kUpdThreads) sm.hist[i] = 0;
+      int* h = sm.hist[d & 1];
+      if (tid < 256) h[tid] = 0;
       __syncthreads();
-      for (int i = tid; i < n; i += kUpdThreads) {
-        unsigned long long h, l;
-        get_key(ws, L, cur, n_old, i, h, l);
-        if (cmp_prefix(h, l, ph, pl, d) == 0) atomicAdd(&sm.hist[digit_of(h, l, d)], 1);
+      // kUpdBatch independent key loads per thread, then the votes (uniform trip count)
+      for (int base = i0; base < i1; base += kUpdThreads * kUpdBatch) {
+        unsigned long long kh[kUpdBatch], kl[kUpdBatch];
+#pragma unroll
+        for (int r = 0; r < kUpdBatch; ++r) {
+          const int i = base + r * kUpdThreads + tid;
+          kh[r] = kl[r] = 0;
+          if (i < i1) {
+            if (d < 8)  // digits 0..7 and their prefix need only the nll bits
+              kh[r] = (unsigned long long)__double_as_longlong(i < n_old ? at<double>(ws, L.m_nll[cur])[i]
+                                                                        : at<double>(ws, L.s_nll)[i - n_old]);
+            else
+              get_key(ws, L, cur, n_old, i, kh[r], kl[r]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kUpdBatch; ++r) {
+          const int i = base + r * kUpdThreads + tid;
+          const int dig = (i < i1 && cmp_prefix(kh[r], kl[r], ph, pl, d) == 0) ? digit_of(kh[r], kl[r], d) : -1;
+          // warp-aggregated increments: the leading digits are shared by most keys,
+          // so per-key shared atomics would serialise on one bin
+          const unsigned same = __match_any_sync(0xffffffffu, dig);
+          if (dig >= 0 && (tid & 31) == __ffs(same) - 1) atomicAdd(&h[dig], __popc(same));
+        }
+      }
+      // the peers' histograms of digit d are complete (and every peer has finished
+      // reading digit d-1's buffer, which digit d+1 zeroes)
+      cluster.sync();
+      int v = 0, x = 0;
+      if (tid < 256) {
+        for (int r = 0; r < kUpdCluster; ++r) v += cluster.map_shared_rank(h, r)[tid];
+        x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if ((tid & 31) >= o) x += y;
+        }
+        if ((tid & 31) == 31) sm.wsum[tid >> 5] = x;
       }
       __syncthreads();
-      if (tid == 0) {
-        int r = sm.rank, acc = 0, b = 0;
-        for (; b < 256; ++b) {
-          if (acc + sm.hist[b] >= r) break;
-          acc += sm.hist[b];
+      if (tid < 256) {
+        for (int w = 0; w < (tid >> 5); ++w) x += sm.wsum[w];
+        const int excl = x - v;
+        if (excl < rank && rank <= x) {  // the bin holding the rank-th smallest key
+          sm.bin = tid;
+          sm.rank = rank - excl;
+          sm.done = (v == rank - excl);
         }
-        sm.bin = b;
-        sm.rank = r - acc;
-        sm.done = (sm.hist[b] == r - acc);
       }
       __syncthreads();
       const unsigned long long bd = (unsigned long long)sm.bin;
@@ -551,27 +736,54 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
       else
         pl |= bd << (56 - 8 * (d - 8));
       ndig = d + 1;
+      rank = sm.rank;
       const int done = sm.done;
       __syncthreads();
       if (done) break;
     }
   }
 
-  // ---- 2. gather the selected keys into shared memory ----
+  // ---- 2. gather the selected keys into CTA 0's shared memory ----
   if (tid == 0) sm.sel_n = 0;
   __syncthreads();
-  for (int i = tid; i < n; i += kUpdThreads) {
-    unsigned long long h, l;
-    get_key(ws, L, cur, n_old, i, h, l);
-    if (select_all || cmp_prefix(h, l, ph, pl, ndig) <= 0) {
-      const int k = atomicAdd(&sm.sel_n, 1);
-      sk_h[k] = h;
-      sk_l[k] = l;
-      sk_v[k] = i;
+  for (int base = i0; base < i1; base += kUpdThreads * kUpdBatch) {
+    unsigned long long h[kUpdBatch], l[kUpdBatch];
+#pragma unroll
+    for (int r = 0; r < kUpdBatch; ++r) {
+      const int i = base + r * kUpdThreads + tid;
+      if (i < i1) get_key(ws, L, cur, n_old, i, h[r], l[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kUpdBatch; ++r) {
+      const int i = base + r * kUpdThreads + tid;
+      if (i < i1 && (select_all || cmp_prefix(h[r], l[r], ph, pl, ndig) <= 0)) {
+        const int k = atomicAdd(&sm.sel_n, 1);
+        sk_h[k] = h[r];
+        sk_l[k] = l[r];
+        sk_v[k] = i;
+      }
     }
   }
-  __syncthreads();
-  sel = sm.sel_n;  // == min(n, K)
+  cluster.sync();  // every CTA's local count is final
+  if (crank != 0) {  // append this CTA's keys after those of lower ranks, in CTA 0
+    int base = 0;
+    for (unsigned r = 0; r < crank; ++r) base += *cluster.map_shared_rank(&sm.sel_n, r);
+    unsigned long long* dh = cluster.map_shared_rank(sk_h, 0u);
+    unsigned long long* dl = cluster.map_shared_rank(sk_l, 0u);
+    int* dv = cluster.map_shared_rank(sk_v, 0u);
+    for (int k = tid; k < sm.sel_n; k += kUpdThreads) {
+      dh[base + k] = sk_h[k];
+      dl[base + k] = sk_l[k];
+      dv[base + k] = sk_v[k];
+    }
+  } else if (tid == 0) {
+    int tot = 0;
+    for (int r = 0; r < kUpdCluster; ++r) tot += *cluster.map_shared_rank(&sm.sel_n, r);
+    sm.elig_total = tot;
+  }
+  cluster.sync();  // CTA 0 holds every selected key; nobody touches a peer's smem after this
+  if (crank != 0) return;
+  sel = sm.elig_total;  // == min(n, K)
   int np2 = 1;
   while (np2 < sel) np2 <<= 1;
   for (int i = sel + tid; i < np2; i += kUpdThreads) {
@@ -584,7 +796,9 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
 
   // ---- 3. write the new materialized list (sorted), remap old -> new ----
   int* remap = at<int>(ws, L.remap);
-  const int* b_node = at<int>(ws, L.b_node);
+  int* b_node = at<int>(ws, L.b_node);
+  for (int i = tid; i < n_old; i += kUpdThreads) remap[i] = -1;  // pruned unless selected
+  __syncthreads();
   for (int pos = tid; pos < sel; pos += kUpdThreads) {
     const int src = sk_v[pos];
     if (src < n_old) remap[src] = pos;
@@ -641,6 +855,33 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   has_thr = sel >= K;
   th = has_thr ? (unsigned long long)__double_as_longlong(at<double>(ws, L.m_nll[nxt])[K - 1]) : 0;
   tl = has_thr ? lo_arr[K - 1] : 0;
+  if (!final) {
+    // merge-only slice: the batch nodes move to their new positions and lex
+    // ranks (the next slice's children are keyed by them). A batch node pruned by
+    // this merge (-2) gets nll = +inf: its children are worse than it, hence past
+    // the new threshold, so none can survive in a later slice.
+    for (int b = tid; b < c->batch_n; b += kUpdThreads) {
+      const int pos = b_node[b];
+      if (pos < 0) continue;  // the root
+      const int np = remap[pos];
+      b_node[b] = np < 0 ? -2 : np;
+      if (np < 0)
+        at<double>(ws, L.b_nll)[b] = CUDART_INF;
+      else
+        at<int>(ws, L.b_lex)[b] = lex[np];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      c->cur = dst;
+      c->count = sel;
+      c->has_thr = has_thr;
+      c->thr_nll = __longlong_as_double((long long)th);
+      c->thr_lo = tl;
+      c->n_surv = 0;
+      at<int>(ws, L.r_aux)[0] = 0;
+    }
+    return;
+  }
   }  // n_new > 0
 
   // ---- 6. next batch: first B unexpanded nodes with depth < D and key < threshold ----
@@ -713,6 +954,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     c->batch_n = batch_n;
     c->slot_next = slot_base + batch_n;
     c->n_surv = 0;
+    at<int>(ws, L.r_aux)[0] = 0;  // chunked row path: empty work list for the next round
   }
 }
 
@@ -935,17 +1177,36 @@ extern "C" int sx_beam_step(const double* q, long long ldq, int V, int nb, const
   return SX_OK;
 }
 
+static long long g_survivor_cap = 0;  // sx_tree_set_survivor_cap: 0 = default_survivor_cap (tests force overflows)
+
+static TreeLayout host_layout(int K, int B, int V, int D) {
+  long long cap = g_survivor_cap > 0 ? g_survivor_cap : default_survivor_cap(K, B, V);
+  if (cap < V) cap = V;  // a single row's candidates always fit: the sliced retry makes progress
+  return tree_layout(K, B, V, D, cap);
+}
+
+extern "C" int sx_tree_set_survivor_cap(long long cap) {
+  if (cap < 0) return arg_error("survivor cap must be >= 0 (0 = default)");
+  g_survivor_cap = cap;
+  return SX_OK;
+}
+
+extern "C" long long sx_tree_survivor_cap(int K, int B, int V, int D) {
+  if (K < 1 || B < 1 || V < 2 || D < 1 || D > 250) return -1;
+  return host_layout(K, B, V, D).cap;
+}
+
 static size_t upd_smem_bytes(const TreeLayout& L) {
   return ((sizeof(UpdSmem) + 15) & ~size_t(15)) + (size_t)L.kpad * (8 + 8 + 4) + 64;
 }
 
 extern "C" long long sx_tree_workspace_bytes(int K, int B, int V, int D) {
   if (K < 1 || B < 1 || V < 2 || D < 1 || D > 250) return -1;
-  return tree_layout(K, B, V, D).total;
+  return host_layout(K, B, V, D).total;
 }
 
 extern "C" int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n) {
-  TreeLayout L = tree_layout(K, B, V, D);
+  TreeLayout L = host_layout(K, B, V, D);
   const long long vals[] = {L.ctl,   L.b_node,    L.b_nll, L.b_depth,   L.b_lex,   L.b_slot,  L.b_token, L.b_anc,
                             L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows, L.b_pos, L.b_dense, L.total};
   const int m = (int)(sizeof(vals) / sizeof(vals[0]));
@@ -964,7 +1225,7 @@ static int check_tree_args(int K, int B, int V, int D) {
 extern "C" int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, int pad_slot, cudaStream_t stream) {
   int st = check_tree_args(K, B, V, D);
   if (st) return st;
-  TreeLayout L = tree_layout(K, B, V, D);
+  TreeLayout L = host_layout(K, B, V, D);
   tree_begin_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, root_slot, pad_slot);
   SX_CHECK_LAUNCH("tree_begin_kernel");
   return SX_OK;
@@ -980,44 +1241,82 @@ extern "C" int sx_tree_set_impl(int unfused) {
 
 extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
                              int score_mode, double temperature, double top_p, int* host_ctl, cudaStream_t stream) {
+  return sx_tree_round_rows(ws, K, B, V, D, rows, row_kind, ld, score_mode, temperature, top_p, 0, -1, 1, host_ctl,
+                            stream);
+}
+
+extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const void* rows, int row_kind, long long ld,
+                                  int score_mode, double temperature, double top_p, int r0, int r1, int final,
+                                  int* host_ctl, cudaStream_t stream) {
   int st = check_tree_args(K, B, V, D);
   if (st) return st;
   if (row_kind != SX_ROWS_LOGITS_F32 && row_kind != SX_ROWS_PROBS_F64) return arg_error("tree: bad row kind");
   if (ld < V) return arg_error("tree: row stride %lld < V %d", ld, V);
-  TreeLayout L = tree_layout(K, B, V, D);
+  if (r0 < 0 || r0 >= B || (r1 >= 0 && r1 <= r0) || r1 > B) return arg_error("tree: bad row range [%d, %d)", r0, r1);
+  TreeLayout L = host_layout(K, B, V, D);
+  const int nrows = (r1 < 0 ? B : r1) - r0;  // grid bound; the kernels clip to batch_n
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
   if (int st = ensure_smem_attr((const void*)tree_update_kernel, 227 * 1024)) return st;
   if (int st = ensure_smem_attr((const void*)tree_warp_rows_kernel, (int)sizeof(RowSmem))) return st;
   if (int st = ensure_smem_attr((const void*)tree_argmax_score_kernel, (int)sizeof(RowSmem))) return st;
   if (score_mode == SX_SCORE_ARGMAX) {
-    tree_argmax_score_kernel<<<B, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld);
+    tree_argmax_score_kernel<<<nrows, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld, r0, r1);
     SX_CHECK_LAUNCH("tree_argmax_score_kernel");
   } else if (score_mode == SX_SCORE_WARP) {
-    tree_warp_rows_kernel<<<B, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld, temperature, top_p);
+    tree_warp_rows_kernel<<<L.wsc, kRowThreads, sizeof(RowSmem), stream>>>(w, L, rows, row_kind, ld, temperature,
+                                                                         top_p, r0, r1);
     SX_CHECK_LAUNCH("tree_warp_rows_kernel");
-    dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, B);
-    tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, nullptr, -1, V);
+    dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, nrows);
+    tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, nullptr, -1, V, r0, r1);
     SX_CHECK_LAUNCH("tree_score_kernel");
   } else if (score_mode == SX_SCORE_RAW && row_kind == SX_ROWS_LOGITS_F32 && !g_tree_unfused) {
-    // persistent: up to 8 resident 256-thread CTAs per SM walk the batch rows
-    const int grid = B < 8 * kNumSMs ? B : 8 * kNumSMs;
+    // persistent grids of (row, chunk) units, sized to the resident CTAs
+    static int occ[3] = {0, 0, 0};
+    if (!occ[0]) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], tree_rows_max_kernel, kMaxThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], tree_rows_sum_kernel, kRowThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], tree_rows_score_kernel, kRowThreads, 0);
+      for (int& o : occ) o = o < 1 ? 1 : o;
+    }
+    const long long ua = (long long)nrows * ((V + kRowChunkA - 1) / kRowChunkA);
+    const long long ub = (long long)nrows * ((V + kRowChunkB - 1) / kRowChunkB);
+    auto grid_of = [&](long long units, int o) { return (int)(units < (long long)o * kNumSMs ? units : (long long)o * kNumSMs); };
+    const float* z = reinterpret_cast<const float*>(rows);
     const int vec4 = (V % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0);
-    tree_logits_rows_kernel<<<grid, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld, vec4);
-    SX_CHECK_LAUNCH("tree_logits_rows_kernel");
+    tree_rows_max_kernel<<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, vec4, r0, r1);
+    SX_CHECK_LAUNCH("tree_rows_max_kernel");
+    tree_rows_sum_kernel<<<grid_of(ub, occ[1]), kRowThreads, 0, stream>>>(w, L, z, ld);
+    SX_CHECK_LAUNCH("tree_rows_sum_kernel");
+    tree_rows_score_kernel<<<grid_of(ub, occ[2]), kRowThreads, 0, stream>>>(w, L, z, ld);
+    SX_CHECK_LAUNCH("tree_rows_score_kernel");
   } else if (score_mode == SX_SCORE_RAW) {
     if (row_kind == SX_ROWS_LOGITS_F32) {
-      tree_row_stats_kernel<<<B, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld);
+      tree_row_stats_kernel<<<nrows, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld, r0, r1);
       SX_CHECK_LAUNCH("tree_row_stats_kernel");
     }
-    dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, B);
-    tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, rows, row_kind, ld);
+    dim3 grid((V + 255) / 256 < 64 ? (V + 255) / 256 : 64, nrows);
+    tree_score_kernel<<<grid, 256, 0, stream>>>(w, L, rows, row_kind, ld, r0, r1);
     SX_CHECK_LAUNCH("tree_score_kernel");
   } else {
     return arg_error("tree: bad score mode %d", score_mode);
   }
   const size_t smem = upd_smem_bytes(L);
   if (smem > 227 * 1024) return arg_error("tree: update needs %zu B of shared memory", smem);
-  tree_update_kernel<<<1, kUpdThreads, smem, stream>>>(w, L);
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kUpdCluster);
+    cfg.blockDim = dim3(kUpdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kUpdCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tree_update_kernel, w, L, final);
+  }
   SX_CHECK_LAUNCH("tree_update_kernel");
   if (host_ctl) {
     cudaError_t e = cudaMemcpyAsync(host_ctl, w + L.ctl, sizeof(TreeCtl), cudaMemcpyDeviceToHost, stream);
@@ -1026,11 +1325,26 @@ extern "C" int sx_tree_round(void* ws, int K, int B, int V, int D, const void* r
   return SX_OK;
 }
 
+__global__ void tree_clear_err_kernel(uint8_t* ws, TreeLayout L) {
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  c->err = 0;
+  c->n_surv = 0;
+  at<int>(ws, L.r_aux)[0] = 0;
+}
+
+extern "C" int sx_tree_clear_overflow(void* ws, int K, int B, int V, int D, cudaStream_t stream) {
+  int st = check_tree_args(K, B, V, D);
+  if (st) return st;
+  tree_clear_err_kernel<<<1, 1, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), host_layout(K, B, V, D));
+  SX_CHECK_LAUNCH("tree_clear_err_kernel");
+  return SX_OK;
+}
+
 extern "C" int sx_tree_finalize(void* ws, int K, int B, int V, int D, int root_token, int* out_parent, int* out_token,
                                 double* out_edge, int* out_depth, int* out_slot, cudaStream_t stream) {
   int st = check_tree_args(K, B, V, D);
   if (st) return st;
-  TreeLayout L = tree_layout(K, B, V, D);
+  TreeLayout L = host_layout(K, B, V, D);
   tree_final_kernel<<<(K + 256) / 256, 256, 0, stream>>>(reinterpret_cast<uint8_t*>(ws), L, root_token, out_parent,
                                                           out_token, out_edge, out_depth, out_slot);
   SX_CHECK_LAUNCH("tree_final_kernel");
@@ -1043,7 +1357,7 @@ extern "C" int sx_markov_rows(const double* table, int V, int order, const int* 
   int st = check_tree_args(K, B, V, D);
   if (st) return st;
   if (order < 0 || order > 64) return arg_error("markov: order %d out of range", order);
-  TreeLayout L = tree_layout(K, B, V, D);
+  TreeLayout L = host_layout(K, B, V, D);
   const int grid = from_batch ? B : n_nodes;
   if (grid <= 0) return SX_OK;
   markov_rows_kernel<<<grid, 128, 0, stream>>>(table, V, order, ctx0, reinterpret_cast<uint8_t*>(ws), L, node_ids,

@@ -33,15 +33,39 @@ struct TreeLayout {
   long long remap;
   long long r_max, r_sum;
   long long w_rows;     // fp64 [B, V] warped rows (t > 0 scoring)
-  long long w_keys, w_idx, w_keys2, w_idx2;  // [B, V] sort scratch
+  long long w_keys, w_idx, w_keys2, w_idx2;  // [wsc, V] sort scratch, one row per CTA of the warp kernel
+  int wsc;              // CTAs (scratch rows) of tree_warp_rows_kernel = min(B, kWarpScratchRows)
   long long f_anc, f_anc_len, f_depth, f_token;  // final target-row tables [(K+1)]
   long long r_lsa;      // float [B]: fp32 log-sum-exp estimate (threshold prefilter), -inf: row skipped
+  // chunked logits-row path (tree_rows_{max,sum,score}_kernel)
+  long long r_pm, r_ps;  // float [B][kRowChunksMax]: per-chunk max / fp32 sum of exp(z - max)
+  long long r_cnt;       // int [2][B]: chunk arrival counters (max pass, sum pass); reset by the last arriver
+  long long r_list;      // int [B]: rows that need the exact passes (not prefiltered away)
+  long long r_aux;       // int [64]: [0] = rows in r_list
   long long total;
 };
 
+constexpr int kWarpScratchRows = 148;  // one warp-row CTA per SM (its shared-memory radix histograms fill the SM)
+constexpr int kRowChunkA = 4096;  // elements per work unit of the max pass
+constexpr int kRowChunkB = 1024;  // elements per work unit of the exp / score passes
+constexpr int kRowChunksMax = 64;  // V <= 262144 -> <= 64 max-pass chunks per row
+
 __host__ __device__ inline long long tl_align(long long x) { return (x + 255) & ~255LL; }
 
-__host__ __device__ inline TreeLayout tree_layout(int K, int B, int V, int D) {
+// Survivor capacity (candidates of one round that beat the threshold): B x V
+// bounds it, but only a first round without a threshold (<= V of the root) or
+// very flat rows come near it; 2^24 entries (448 MB) cover every measured round.
+// A round that still overflows is re-run in row slices (sx_tree_round_rows).
+constexpr long long kSurvivorCapMin = 1LL << 24;
+
+inline long long default_survivor_cap(int K, int B, int V) {
+  const long long full = (long long)B * V;
+  long long cap = (long long)V + K;
+  if (cap < kSurvivorCapMin) cap = kSurvivorCapMin;
+  return cap < full ? cap : full;
+}
+
+inline TreeLayout tree_layout(int K, int B, int V, int D, long long cap) {
   TreeLayout L{};
   L.K = K;
   L.B = B;
@@ -50,7 +74,7 @@ __host__ __device__ inline TreeLayout tree_layout(int K, int B, int V, int D) {
   int kp = 1;
   while (kp < K) kp <<= 1;
   L.kpad = kp;
-  L.cap = (long long)B * V;
+  L.cap = cap;
   long long o = 0;
   auto take = [&](long long bytes) {
     long long r = o;
@@ -84,15 +108,21 @@ __host__ __device__ inline TreeLayout tree_layout(int K, int B, int V, int D) {
   L.r_max = take(4LL * B);
   L.r_sum = take(8LL * B);
   L.w_rows = take(8LL * B * V);
-  L.w_keys = take(8LL * B * V);
-  L.w_idx = take(4LL * B * V);
-  L.w_keys2 = take(8LL * B * V);
-  L.w_idx2 = take(4LL * B * V);
+  L.wsc = B < kWarpScratchRows ? B : kWarpScratchRows;
+  L.w_keys = take(8LL * L.wsc * V);
+  L.w_idx = take(4LL * L.wsc * V);
+  L.w_keys2 = take(8LL * L.wsc * V);
+  L.w_idx2 = take(4LL * L.wsc * V);
   L.f_anc = take(4LL * (K + 1) * (D + 1));
   L.f_anc_len = take(4LL * (K + 1));
   L.f_depth = take(4LL * (K + 1));
   L.f_token = take(4LL * (K + 1));
   L.r_lsa = take(4LL * B);
+  L.r_pm = take(4LL * B * kRowChunksMax);
+  L.r_ps = take(4LL * B * kRowChunksMax);
+  L.r_cnt = take(8LL * B);
+  L.r_list = take(4LL * B);
+  L.r_aux = take(4LL * 64);
   L.total = o;
   return L;
 }

@@ -340,6 +340,9 @@ class TreeWorkspace:
         lib.sx_tree_offsets(K, B, V, D, offs, len(_OFF_NAMES))
         self.off = dict(zip(_OFF_NAMES, list(offs)))
         self.ctl_host = torch.zeros(16, dtype=torch.int32).pin_memory()
+        self.cap = lib.sx_tree_survivor_cap(K, B, V, D)
+        self.last_round = None
+        self.overflow_retries = 0
         self.rounds = 0
         # pinned staging of the finished tree (parent, token, slot | edge): copied
         # asynchronously so the host builds DraftTree while the target pass runs
@@ -378,14 +381,37 @@ class TreeWorkspace:
         return self.view("b_dense", torch.int32, self.B)
 
     def begin(self, root_slot: int = 0, pad_slot: int = 0) -> None:
+        if _lib.load().sx_tree_survivor_cap(self.K, self.B, self.V, self.D) != self.cap:
+            raise RuntimeError("tree workspace laid out under another survivor capacity (sx_tree_set_survivor_cap)")
         self.rounds = 0
         call("sx_tree_begin", ptr(self.buf), self.K, self.B, self.V, self.D, root_slot, pad_slot, stream_ptr())
 
     def launch_round(self, rows: torch.Tensor, score_mode: int, temperature: float = 1.0, top_p: float = 1.0) -> None:
         """Enqueue scoring + update + control-block readback (capturable in a CUDA graph)."""
         _require_cuda(rows)
+        self.last_round = (rows, score_mode, temperature, top_p)
         call("sx_tree_round", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(rows), row_kind(rows), rows.stride(0),
              score_mode, float(temperature), float(top_p), self.ctl_host.data_ptr(), stream_ptr())
+
+    def _retry_sliced(self) -> list:
+        """The last round overflowed the survivor buffer (nothing was committed):
+        re-run the same rows in slices whose candidates fit, merging each slice
+        into the K best (sx_tree_round_rows; the last slice picks the next batch)."""
+        rows, mode, temp, top_p = self.last_round
+        batch_n = self.ctl_host.tolist()[5]
+        per = max(1, int(self.cap // self.V))
+        call("sx_tree_clear_overflow", ptr(self.buf), self.K, self.B, self.V, self.D, stream_ptr())
+        self.overflow_retries += 1
+        for r0 in range(0, batch_n, per):
+            r1 = min(batch_n, r0 + per)
+            call("sx_tree_round_rows", ptr(self.buf), self.K, self.B, self.V, self.D, ptr(rows), row_kind(rows),
+                 rows.stride(0), mode, float(temp), float(top_p), r0, r1, int(r1 == batch_n),
+                 self.ctl_host.data_ptr(), stream_ptr())
+            torch.cuda.current_stream().synchronize()
+            c = self.ctl_host.tolist()
+            if c[8]:
+                raise RuntimeError(f"tree: survivor overflow in a {r1 - r0}-row slice (cap {self.cap})")
+        return c
 
     def round(self, rows: torch.Tensor, score_mode: int, temperature: float = 1.0, top_p: float = 1.0) -> dict:
         """Score the current batch's rows, update the tree; returns the control block."""
@@ -398,7 +424,7 @@ class TreeWorkspace:
         self.rounds += 1
         c = self.ctl_host.tolist()
         if c[8]:
-            raise RuntimeError("tree: survivor buffer overflow")
+            c = self._retry_sliced()
         return {"count": c[1], "has_thr": c[2], "slot_next": c[4], "batch_n": c[5]}
 
     def batch_pos(self) -> torch.Tensor:

@@ -815,6 +815,7 @@ class _LlamaDraftSession:
                 ws.launch_round(m.buf.logits[:n], mode, temp, top_p)
             g.sx_kernels = _lib.load().sx_launch_count() - n0
             ws._graphs[key] = g
+        ws.last_round = (m.buf.logits[:n], mode, temp, top_p)  # rows of a sliced re-run on survivor overflow
         g.replay()
         K.GRAPH_KERNELS[0] += g.sx_kernels
         ctl = ws.read_ctl()

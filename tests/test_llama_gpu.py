@@ -206,9 +206,10 @@ def test_fused_qkv_rope_matches_separate_kernels(pair):
 
 @pytest.mark.parametrize("V,K_,B_", [(32000, 1024, 256), (128256, 512, 128)])
 def test_fused_round_kernel_matches_two_kernel_path(cuda, V, K_, B_):
-    """sx_tree_set_impl A/B: the fused persistent row kernel (one HBM read per
-    row) and the tree_row_stats + tree_score pair build the same tree, node for
-    node, on the same draft rows."""
+    """sx_tree_set_impl A/B: the chunked logits-row path (max / sum / score
+    kernels over (row, chunk) units, one HBM read per prefiltered row) and the
+    tree_row_stats + tree_score pair build the same tree, node for node, on the
+    same draft rows."""
     from paper_2406_02532_b200 import _lib
     from paper_2406_02532_b200.llama import LlamaConfig
 

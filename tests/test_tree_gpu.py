@@ -168,3 +168,33 @@ def test_fault_injection_detected(cuda, monkeypatch):
         seq, _ = sx.generate_sequential((1, 2, 3, 4), target, cfg)
         diverged += got != seq
     assert diverged > 0
+
+
+def _with_survivor_cap(cap, fn):
+    from paper_2406_02532_b200 import _lib
+    from paper_2406_02532_b200.models import _WS
+
+    _WS._tls.ws = {}
+    _lib.call("sx_tree_set_survivor_cap", cap)
+    try:
+        return fn(_WS)
+    finally:
+        _lib.call("sx_tree_set_survivor_cap", 0)
+        _WS._tls.ws = {}
+
+
+@pytest.mark.parametrize("seed,K_,D_,B_,w", [(11, 512, 8, 64, None), (12, 300, 10, 32, (0.6, 0.9)), (13, 200, 6, 16, (0.0, 1.0))])
+def test_survivor_overflow_sliced_retry_vs_oracle(cuda, seed, K_, D_, B_, w):
+    """A survivor buffer of V entries overflows on most rounds of a V = 32 Markov
+    build: the round is re-run in row slices (merge-only updates, batch remapped,
+    the last slice picks the next batch) and the tree still equals the oracle's,
+    node for node and round for round."""
+    def run(WS):
+        g = sx.build_sssp((5, 7), sx.make_synthetic(seed, 32, 0.05), sx.BuilderParams(K_, D_, B_), warp_cfg(w))
+        return g, WS.get(K_, B_, 32, D_).overflow_retries
+
+    g, retries = _with_survivor_cap(32, run)
+    o = ox.build_sssp((5, 7), ox.make_synthetic(seed, 32, 0.05), ox.BuilderParams(K_, D_, B_), warp_cfg(w, False))
+    assert_same_tree(g, o, (seed, K_, w))
+    if w != (0.0, 1.0):  # argmax scoring yields one candidate per row: never overflows
+        assert retries > 0

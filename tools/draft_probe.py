@@ -28,7 +28,7 @@ def main():
     a = ap.parse_args()
     rows = [int(r) for r in a.rows.split(",")]
     nmax = max(rows)
-    m = LlamaModel(a.model, seed=2, max_ctx=a.ctx + nmax + 64, max_tokens=max(nmax, 128))
+    m = LlamaModel(a.model, seed=2, max_ctx=a.ctx + nmax + 64, max_tokens=max(nmax, a.ctx, 128))
     dev = m.device
     V = PRESETS[a.model].vocab
     # commit a prompt so the rows attend a real prefix
