@@ -176,55 +176,48 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvArgs g) {
 
 
 // ---------------------------------------------------------------------------
-// TMA-fed path (the default): one CTA per SM; a producer warp streams weight-row
-// segments into a 9-stage shared-memory ring with 1-D bulk copies (no register
-// cost per byte in flight: 144 KB per SM), the token rows stay resident in
-// shared memory, 8 consumer warps form the dot products.
-//   work item = (group, K chunk): group = 2 row pairs of one 128-row tile, rows
-//   (2j, 2j+1, 2j+64, 2j+65), i.e. the RoPE / SwiGLU-IL pairs; chunk = 2048
-//   columns. Groups are dealt round-robin to the CTAs (2-pair groups keep the
-//   last round >= 0.96 full on every 7B / 70B shape).
-//   consumer warp w: pair w >> 2, column quarter w & 3 of each chunk; at the end
-//   of a group the 4 quarter sums are added in order (deterministic) and the
-//   quarter-0 warp applies the epilogue.
-// The producer issues the first ring of weight copies BEFORE griddepcontrol.wait
-// (launched with programmatic stream serialization): the weights stream while
-// the kernel that produces X finishes.
+// TMA-fed path (the default): a producer warp streams weight-row segments into a
+// shared-memory ring with 1-D bulk copies (no register cost per byte in flight),
+// the token rows stay resident in shared memory, 8 consumer warps form the dot
+// products.
+//   Unit of work = a GROUP of 2 row pairs (f, f + 64) of one 128-row tile (the
+//   RoPE / SwiGLU-IL pairs): rows 2j, 2j+1, 2j+64, 2j+65. Each CTA owns a
+//   contiguous range of groups (groups / grid, +-1). A ring stage holds the 4
+//   rows of a group over kGemvKC = 4096 columns: every bulk copy is one 8 KB
+//   contiguous run of a weight row. Measured on B200 (tools/micro/stream_probe.cu,
+//   profiles/r2/stream_probe.txt): row segments of 1 / 2 / 4 / 8 KB stream at
+//   ~1.4 / 3.4 / 5.1 / 6.5 TB/s -- the segment length, not the bytes in flight,
+//   sets the rate -- so the stage is whole 8 KB row runs, not narrow column chunks.
+//   Consumer warp w: pair w >> 2, column quarter w & 3 of each stage; at the end
+//   of a group the 4 quarter sums of a pair meet in shared memory (named barrier
+//   of the pair's 4 warps, fixed order) and lane t of the quarter-0 warp stores
+//   token t.
+// The producer issues the first ring of weight copies BEFORE griddepcontrol.wait:
+// the weights do not depend on the kernel that produces X.
 constexpr int kTmaConsumers = 8;
 constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
-constexpr int kTmaKC = 2048;
-constexpr int kTmaStages = 9;
-constexpr int kTmaStageBytes = 4 * kTmaKC * 2;
-constexpr int kTmaXMax = 64 * 1024;
-constexpr int kTmaSmem = kTmaXMax + kTmaStages * kTmaStageBytes + 1024;
+constexpr int kGemvKC = 4096;
+constexpr int kGemvStageBytes = 4 * kGemvKC * 2;
 
-SX_DEV void tma_item(const GemvArgs& g, int i, int nchunk, int& tile, int& j, int& c0, int& kc) {
-  const int grp = blockIdx.x + (i / nchunk) * gridDim.x;
-  const int c = i % nchunk;
-  tile = grp >> 5;
-  j = grp & 31;
-  c0 = c * kTmaKC;
-  kc = min(kTmaKC, g.K - c0);
-}
+template <int S>
+static int gemv_tma_smem(int M, int K) { return S * kGemvStageBytes + 1024 + ((M * K * 2 + 127) / 128) * 128; }
 
-SX_DEV float dot_bf16x8(const uint4& w, const uint4& x, float acc) { return dot8(w, x, acc); }
-
-template <int MT>
+template <int MT, int S>
 __global__ void __launch_bounds__(kTmaThreads, 1) gemv_tma_kernel(GemvArgs g) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* xs = smem_raw;                                   // [M][K] bf16 token rows
-  uint8_t* ring = smem_raw + kTmaXMax;                       // [S][4][KC] bf16 weight segments
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kTmaStages * kTmaStageBytes);
-  uint64_t* empty = full + kTmaStages;
-  uint64_t* xbar = empty + kTmaStages;
-  float* red = reinterpret_cast<float*>(xbar + 1);           // [8 warps][2 rows][MT]
+  uint8_t* ring = smem_raw;                                            // [S][4 rows][kGemvKC] bf16
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * kGemvStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* xbar = empty + S;
+  float* red = reinterpret_cast<float*>(ring + S * kGemvStageBytes + 256);  // [2 parity][8 warps][2 rows][MT]
+  uint8_t* xs = ring + S * kGemvStageBytes + 1024;                       // [M][K] bf16 token rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles = (g.Nf + 127) / 128, groups = tiles * 32;
-  const int nchunk = (g.K + kTmaKC - 1) / kTmaKC;
-  const int my_groups = blockIdx.x < groups ? (groups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int n_items = my_groups * nchunk;
+  const int groups = ((g.Nf + 127) / 128) * 32;
+  const int g_begin = (int)((long long)groups * blockIdx.x / gridDim.x);
+  const int g_end = (int)((long long)groups * (blockIdx.x + 1) / gridDim.x);
+  const int nchunk = (g.K + kGemvKC - 1) / kGemvKC;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kTmaConsumers);
     }
@@ -236,28 +229,36 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gemv_tma_kernel(GemvArgs g) {
     // ---------------- producer ----------------
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-      auto issue = [&](int i) {
-        const int s = i % kTmaStages;
-        if (i >= kTmaStages) mbar_wait(&empty[s], ((i / kTmaStages) & 1) ^ 1);
-        int tile, j, c0, kc;
-        tma_item(g, i, nchunk, tile, j, c0, kc);
+      auto load_x = [&]() {
+        griddep_wait();
+        mbar_arrive_expect_tx(xbar, (uint32_t)(g.M * g.K * 2));
+        for (int t = 0; t < g.M; ++t)
+          bulk_load(xs + (long long)t * g.K * 2, g.X + (long long)t * g.K, (uint32_t)g.K * 2, xbar, pol_x);
+      };
+      int s = 0, ph = 0, issued = 0;
+      bool x_loaded = false;
+      for (int gi = g_begin; gi < g_end; ++gi) {
+        const int tile = gi >> 5, j = gi & 31;
         const int rows[4] = {tile * 128 + 2 * j, tile * 128 + 2 * j + 1, tile * 128 + 64 + 2 * j,
                              tile * 128 + 65 + 2 * j};
-        uint32_t bytes = 0;
-        for (int q = 0; q < 4; ++q) bytes += rows[q] < g.Nf ? (uint32_t)kc * 2 : 0u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        for (int q = 0; q < 4; ++q)
-          if (rows[q] < g.Nf)
-            bulk_load(ring + s * kTmaStageBytes + q * kTmaKC * 2, g.W + (long long)rows[q] * g.K + c0,
-                      (uint32_t)kc * 2, &full[s], pol_w);
-      };
-      int i = 0;
-      for (; i < n_items && i < kTmaStages; ++i) issue(i);  // weights do not depend on the previous kernel
-      griddep_wait();
-      mbar_arrive_expect_tx(xbar, (uint32_t)(g.M * g.K * 2));
-      for (int t = 0; t < g.M; ++t)
-        bulk_load(xs + (long long)t * g.K * 2, g.X + (long long)t * g.K, (uint32_t)g.K * 2, xbar, pol_x);
-      for (; i < n_items; ++i) issue(i);
+        for (int c0 = 0; c0 < g.K; c0 += kGemvKC) {
+          if (issued == S) load_x(), x_loaded = true;  // the first ring is in flight: now wait for X's producer
+          if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t seg = (uint32_t)min(kGemvKC, g.K - c0) * 2;
+          uint32_t bytes = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) bytes += rows[q] < g.Nf ? seg : 0u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (rows[q] < g.Nf)
+              bulk_load(ring + s * kGemvStageBytes + q * kGemvKC * 2, g.W + (long long)rows[q] * g.K + c0, seg,
+                        &full[s], pol_w);
+          ++issued;
+          if (++s == S) s = 0, ph ^= 1;
+        }
+      }
+      if (!x_loaded) load_x();  // the whole range fit in the first ring
     }
     griddep_launch_dependents();
     return;
@@ -265,68 +266,70 @@ __global__ void __launch_bounds__(kTmaThreads, 1) gemv_tma_kernel(GemvArgs g) {
   // ---------------- consumers ----------------
   griddep_wait();  // outputs (and the residual the ADD epilogue reads) are ordered after the previous kernel
   griddep_launch_dependents();
-  const int pair = warp >> 2, q = warp & 3;
   mbar_wait(xbar, 0);
-  float a0[MT], a1[MT];
+  const int pair = warp >> 2, q = warp & 3;
+  const int K8 = g.K >> 3;
+  const uint4* xv0 = reinterpret_cast<const uint4*>(xs);
+  int s = 0, ph = 0, par = 0;
+  for (int gi = g_begin; gi < g_end; ++gi, par ^= 1) {
+    float a0[MT], a1[MT];
 #pragma unroll
-  for (int t = 0; t < MT; ++t) a0[t] = a1[t] = 0.f;
-  for (int i = 0; i < n_items; ++i) {
-    const int s = i % kTmaStages;
-    int tile, j, c0, kc;
-    tma_item(g, i, nchunk, tile, j, c0, kc);
-    mbar_wait(&full[s], (i / kTmaStages) & 1);
-    const int qlen = kc >> 2, qv = qlen >> 3;  // columns / 16-byte vectors in this warp's quarter
-    const uint4* w0 = reinterpret_cast<const uint4*>(ring + s * kTmaStageBytes + pair * kTmaKC * 2) + (q * qlen >> 3);
-    const uint4* w1 = reinterpret_cast<const uint4*>(ring + s * kTmaStageBytes + (2 + pair) * kTmaKC * 2) + (q * qlen >> 3);
-    const int f0 = tile * 128 + 2 * j + pair;
-    const bool ok0 = f0 < g.Nf, ok1 = f0 + 64 < g.Nf;
-    for (int v = lane; v < qv; v += 32) {
-      const uint4 wa = ok0 ? w0[v] : make_uint4(0, 0, 0, 0);
-      const uint4 wb = ok1 ? w1[v] : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        if (t < g.M) {
-          const uint4 xv = reinterpret_cast<const uint4*>(xs + (long long)t * g.K * 2)[(c0 + q * qlen) / 8 + v];
-          a0[t] = dot_bf16x8(wa, xv, a0[t]);
-          a1[t] = dot_bf16x8(wb, xv, a1[t]);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (c0 + kc == g.K) {  // last chunk of the group: quarter sums -> epilogue
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a0[t] += __shfl_xor_sync(0xffffffffu, a0[t], o);
-          a1[t] += __shfl_xor_sync(0xffffffffu, a1[t], o);
-        }
-      }
-      if (lane == 0) {
+    for (int t = 0; t < MT; ++t) a0[t] = a1[t] = 0.f;
+    for (int c0 = 0; c0 < g.K; c0 += kGemvKC) {
+      const int kc = min(kGemvKC, g.K - c0);
+      const int qv = kc >> 5;  // 16-byte vectors in this warp's quarter (kc % 32 == 0)
+      mbar_wait(&full[s], ph);
+      const uint4* w0 = reinterpret_cast<const uint4*>(ring + s * kGemvStageBytes + pair * kGemvKC * 2) + q * qv;
+      const uint4* w1 = reinterpret_cast<const uint4*>(ring + s * kGemvStageBytes + (2 + pair) * kGemvKC * 2) + q * qv;
+      const uint4* xc = xv0 + ((c0 >> 3) + q * qv);
+#pragma unroll 4
+      for (int v = lane; v < qv; v += 32) {
+        const uint4 wa = w0[v], wb = w1[v];
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
-          red[(warp * 2 + 0) * MT + t] = a0[t];
-          red[(warp * 2 + 1) * MT + t] = a1[t];
+          if (t < g.M) {
+            const uint4 x = xc[(long long)t * K8 + v];
+            a0[t] = dot8(wa, x, a0[t]);
+            a1[t] = dot8(wb, x, a1[t]);
+          }
         }
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(kTmaConsumers * 32) : "memory");
-      if (q == 0 && lane < MT && lane < g.M) {
-        float x0 = 0.f, x1 = 0.f;
-        for (int qq = 0; qq < 4; ++qq) {  // fixed order
-          x0 += red[((pair * 4 + qq) * 2 + 0) * MT + lane];
-          x1 += red[((pair * 4 + qq) * 2 + 1) * MT + lane];
-        }
-        gemv_store(g, lane, tile, 2 * j + pair, x0, x1);
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(kTmaConsumers * 32) : "memory");  // red is rewritten by the next group
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) s = 0, ph ^= 1;
+    }
 #pragma unroll
-      for (int t = 0; t < MT; ++t) a0[t] = a1[t] = 0.f;
+    for (int t = 0; t < MT; ++t) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a0[t] += __shfl_xor_sync(0xffffffffu, a0[t], o);
+        a1[t] += __shfl_xor_sync(0xffffffffu, a1[t], o);
+      }
+    }
+    float* rp = red + par * (kTmaConsumers * 2 * MT);
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        rp[(warp * 2 + 0) * MT + t] = a0[t];
+        rp[(warp * 2 + 1) * MT + t] = a1[t];
+      }
+    }
+    // the 4 warps of this pair; red is double-buffered by group parity, so no second barrier
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + pair) : "memory");
+    if (q == 0 && lane < MT && lane < g.M) {
+      float x0 = 0.f, x1 = 0.f;
+      for (int qq = 0; qq < 4; ++qq) {  // fixed order
+        x0 += rp[((pair * 4 + qq) * 2 + 0) * MT + lane];
+        x1 += rp[((pair * 4 + qq) * 2 + 1) * MT + lane];
+      }
+      const int tile = gi >> 5, j = gi & 31;
+      gemv_store(g, lane, tile, 2 * j + pair, x0, x1);
     }
   }
 }
 
-static int g_gemv_enabled = 1;
+// SX_GEMV=0: the tile kernel for every M (A/B); sx_gemm_set_gemv sets it at run time
+static int g_gemv_enabled = getenv("SX_GEMV") ? atoi(getenv("SX_GEMV")) : 1;
 // programmatic dependent launch (weights prefetched into L2 during the producer's tail); SX_GEMV_PDL=0 disables
 static const int g_gemv_pdl = getenv("SX_GEMV_PDL") ? atoi(getenv("SX_GEMV_PDL")) : 1;
 // SX_GEMV_TMA=0: the register-load fallback for every shape (A/B)
@@ -362,32 +365,42 @@ static int launch_gemv_t(const GemvArgs& g, cudaStream_t stream) {
   return SX_OK;
 }
 
-template <int MT>
+// ring depth: SX_GEMV_STAGES = 4 (default, 128 KB) | 2 (64 KB: two CTAs per SM, the next projection co-resident)
+static const int g_gemv_stages = getenv("SX_GEMV_STAGES") ? atoi(getenv("SX_GEMV_STAGES")) : 4;
+
+template <int MT, int S>
 static int launch_gemv_tma_t(const GemvArgs& g, cudaStream_t stream) {
-  if (int st = ensure_smem_attr((const void*)gemv_tma_kernel<MT>, kTmaSmem)) return st;
+  const int smem = gemv_tma_smem<S>(g.M, g.K);
+  if (int st = ensure_smem_attr((const void*)gemv_tma_kernel<MT, S>, 227 * 1024)) return st;
   const int groups = ((g.Nf + 127) / 128) * 32;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(groups < kNumSMs ? groups : kNumSMs));
   cfg.blockDim = dim3(kTmaThreads);
-  cfg.dynamicSmemBytes = kTmaSmem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = g_gemv_pdl;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemv_tma_kernel<MT>, g);
+  cudaLaunchKernelEx(&cfg, gemv_tma_kernel<MT, S>, g);
   SX_CHECK_LAUNCH("gemv_tma_kernel");
   return SX_OK;
+}
+
+template <int MT>
+static int launch_gemv_tma_m(const GemvArgs& g, cudaStream_t stream) {
+  if (g_gemv_stages == 2) return launch_gemv_tma_t<MT, 2>(g, stream);
+  return launch_gemv_tma_t<MT, 4>(g, stream);
 }
 
 int launch_gemv(const GemvArgs& g, cudaStream_t stream) {
   if ((reinterpret_cast<uintptr_t>(g.W) & 15) || (reinterpret_cast<uintptr_t>(g.X) & 15) || (g.K % 8))
     return arg_error("sx_gemm (thin): W / X must be 16-byte aligned and K a multiple of 8");
-  if ((long long)g.M * g.K * 2 <= kTmaXMax && g.K % 64 == 0 && g_gemv_tma) {
-    if (g.M == 1) return launch_gemv_tma_t<1>(g, stream);
-    if (g.M == 2) return launch_gemv_tma_t<2>(g, stream);
-    return launch_gemv_tma_t<4>(g, stream);
+  if ((long long)g.M * g.K * 2 <= 64 * 1024 && g.K % 32 == 0 && g_gemv_tma) {
+    if (g.M == 1) return launch_gemv_tma_m<1>(g, stream);
+    if (g.M == 2) return launch_gemv_tma_m<2>(g, stream);
+    return launch_gemv_tma_m<4>(g, stream);
   }
   if (g.M == 1) return launch_gemv_t<1>(g, stream);
   if (g.M == 2) return launch_gemv_t<2>(g, stream);

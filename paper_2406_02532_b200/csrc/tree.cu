@@ -293,11 +293,16 @@ __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout
 // good to ~1e-5), and e_v / S are the same canonical values.
 constexpr int kMaxThreads = 128;  // max-pass CTA: small, so >= 1024 of them are resident (one row each at B = 1024)
 
+// kVec: 2 = pipelined batch-max loop, 1 = per-element online loop (A/B), 0 = scalar (unaligned rows);
+// separate instantiations, so the default path keeps its own (small) register budget
+template <int kVec>
 __global__ void __launch_bounds__(kMaxThreads) tree_rows_max_kernel(uint8_t* ws, TreeLayout L,
                                                                      const float* __restrict__ rows, long long ld,
-                                                                     int vec4, int r0, int r1) {
+                                                                     int r0, int r1) {
+  constexpr int vec4 = kVec;
   __shared__ float red_m[kMaxThreads / 32], red_s[kMaxThreads / 32];
   __shared__ int last_s;
+  griddep_launch_dependents();  // the sum pass may become resident now (it waits for this grid to finish)
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int batch_n = rows_end(c, r1) - r0, V = L.V, tid = threadIdx.x, lane = tid & 31;
   // Work units: whole rows when the batch fills the grid (no cross-CTA combine),
@@ -325,7 +330,43 @@ __global__ void __launch_bounds__(kMaxThreads) tree_rows_max_kernel(uint8_t* ws,
         sacc += __expf(x - m);
       }
     };
-    if (vec4) {  // chunk bounds are multiples of 4; 4 loads per thread in flight
+    if constexpr (vec4 == 2) {
+      // chunk bounds are multiples of 4. Register double buffer: the next 4 x 16 B
+      // per thread are in flight while the current ones are folded in; per batch
+      // one max, one rescale, then independent exps (no per-element branch chain).
+      const float4* z4 = reinterpret_cast<const float4*>(z + v0);
+      const int n4 = (v1 - v0) >> 2;
+      constexpr int U = 4;
+      const float4 ninf = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+      float4 cur[U], nxt[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) cur[k] = tid + k * kMaxThreads < n4 ? __ldcs(z4 + tid + k * kMaxThreads) : ninf;
+      float s0 = 0.f, s1 = 0.f;
+      for (int i = tid; i < n4; i += U * kMaxThreads) {
+        const int in = i + U * kMaxThreads;
+#pragma unroll
+        for (int k = 0; k < U; ++k) nxt[k] = in + k * kMaxThreads < n4 ? __ldcs(z4 + in + k * kMaxThreads) : ninf;
+        float bm = -CUDART_INF_F;
+#pragma unroll
+        for (int k = 0; k < U; ++k) bm = fmaxf(bm, fmaxf(fmaxf(cur[k].x, cur[k].y), fmaxf(cur[k].z, cur[k].w)));
+        if (bm > m) {
+          const float r = m == -CUDART_INF_F ? 0.f : __expf(m - bm);
+          s0 *= r;
+          s1 *= r;
+          m = bm;
+        }
+        if (m != -CUDART_INF_F) {
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            s0 += __expf(cur[k].x - m) + __expf(cur[k].y - m);
+            s1 += __expf(cur[k].z - m) + __expf(cur[k].w - m);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) cur[k] = nxt[k];
+      }
+      sacc = s0 + s1;
+    } else if constexpr (vec4 == 1) {  // chunk bounds are multiples of 4; 8 loads per thread in flight
       const float4* z4 = reinterpret_cast<const float4*>(z + v0);
       const int n4 = (v1 - v0) >> 2;
       for (int i = tid; i < n4; i += 8 * kMaxThreads) {  // 8 x 16 B per thread in flight, tail included
@@ -400,6 +441,8 @@ __global__ void __launch_bounds__(kRowThreads) tree_rows_sum_kernel(uint8_t* ws,
                                                                      const float* __restrict__ rows, long long ld) {
   __shared__ RowSmemLite sm;
   __shared__ int last;
+  griddep_wait();  // launched early (programmatic stream serialization): the max pass's work list
+  griddep_launch_dependents();
   const int V = L.V, tid = threadIdx.x;
   const int nwork = *(volatile int*)at<int>(ws, L.r_aux);
   const int nch = (V + kRowChunkB - 1) / kRowChunkB;
@@ -439,6 +482,8 @@ __global__ void __launch_bounds__(kRowThreads) tree_rows_sum_kernel(uint8_t* ws,
 
 __global__ void __launch_bounds__(kRowThreads) tree_rows_score_kernel(uint8_t* ws, TreeLayout L,
                                                                        const float* __restrict__ rows, long long ld) {
+  griddep_wait();  // launched early: the sums of the listed rows
+  griddep_launch_dependents();
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int V = L.V, tid = threadIdx.x, lane = tid & 31;
   const int nwork = at<int>(ws, L.r_aux)[0];
@@ -512,6 +557,7 @@ struct UpdSmem {
   int elig_total;
   int scan[kUpdThreads];
   int depth_start[256];
+  int wscan[kUpdThreads / 32 + 1];  // block_excl_scan_fast: per-warp totals, exclusive-scanned
 };
 
 SX_DEV void get_key(uint8_t* ws, const TreeLayout& L, int cur, int n_old, int i, unsigned long long& h,
@@ -589,6 +635,151 @@ SX_DEV void bitonic_sort_64(unsigned long long* kk, int* kv, int n) {
   }
 }
 
+// Register-resident bitonic sort of n = 2^m (64 <= n <= 8 * kUpdThreads) keys
+// held in shared memory (kh:kl 128-bit, or kl alone when !kWide; values kv),
+// ascending, identical result to bitonic_sort_128 / bitonic_sort_64 (the same
+// compare-exchange network). Thread t of T = min(n, blockDim.x) holds elements
+// i = e*T + t, e < n / T: partner distance j < 32 -> warp shuffle, j >= T ->
+// the thread's own registers, otherwise one shared-memory exchange (2 barriers).
+// n = 1024: 40 of the 55 stages stay in registers.
+// SX_TREE_SORT_REG=0: the shared-memory network for every stage (A/B)
+__constant__ int g_sort_reg = 1;
+
+template <bool kWide, int EM>
+SX_DEV void bitonic_sort_reg_e(unsigned long long* kh, unsigned long long* kl, int* kv, int n) {
+  const int T = n < (int)blockDim.x ? n : (int)blockDim.x;
+  const int E = n / T;
+  const int t = threadIdx.x;
+  const bool act = t < T;
+  unsigned long long h[EM], l[EM];
+  int v[EM];
+#pragma unroll
+  for (int e = 0; e < EM; ++e) {
+    h[e] = l[e] = 0;
+    v[e] = 0;
+    if (act && e < E) {
+      const int i = e * T + t;
+      if (kWide) h[e] = kh[i];
+      l[e] = kl[i];
+      v[e] = kv[i];
+    }
+  }
+  auto less = [&](unsigned long long ah, unsigned long long al, unsigned long long bh, unsigned long long bl) {
+    return kWide ? (ah < bh || (ah == bh && al < bl)) : (al < bl);
+  };
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= T) {  // partner in this thread: slot e ^ (j / T) (compile-time slots: no local-memory arrays)
+        const int js = j / T;
+#pragma unroll
+        for (int e = 0; e < EM; ++e) {
+#pragma unroll
+          for (int pe = e + 1; pe < EM; ++pe) {
+            if ((e ^ pe) == js && act) {
+              const int i = e * T + t;
+              const bool asc = (i & k) == 0;
+              if (less(h[pe], l[pe], h[e], l[e]) == asc) {
+                const unsigned long long th = h[e], tl = l[e];
+                const int tv = v[e];
+                h[e] = h[pe], l[e] = l[pe], v[e] = v[pe];
+                h[pe] = th, l[pe] = tl, v[pe] = tv;
+              }
+            }
+          }
+        }
+      } else if (j < 32) {  // partner lane t ^ j, same slot
+#pragma unroll
+        for (int e = 0; e < EM; ++e) {
+          if (e < E) {
+            const int i = e * T + t;
+            const unsigned long long ph = kWide ? __shfl_xor_sync(0xffffffffu, h[e], j) : 0ull;
+            const unsigned long long pl = __shfl_xor_sync(0xffffffffu, l[e], j);
+            const int pv = __shfl_xor_sync(0xffffffffu, v[e], j);
+            // the compare-exchange of bitonic_sort_128: swap iff (upper < lower) == asc
+            const bool asc = (i & k) == 0;
+            const bool swap = ((i & j) == 0) ? (less(ph, pl, h[e], l[e]) == asc) : (less(h[e], l[e], ph, pl) == asc);
+            if (swap) h[e] = ph, l[e] = pl, v[e] = pv;
+          }
+        }
+      } else {  // partner thread t ^ j: exchange through shared memory
+#pragma unroll
+        for (int e = 0; e < EM; ++e)
+          if (act && e < E) {
+            const int i = e * T + t;
+            if (kWide) kh[i] = h[e];
+            kl[i] = l[e];
+            kv[i] = v[e];
+          }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EM; ++e) {
+          if (act && e < E) {
+            const int i = e * T + t, p = i ^ j;
+            const unsigned long long ph = kWide ? kh[p] : 0ull, pl = kl[p];
+            const bool asc = (i & k) == 0;
+            const bool swap = ((i & j) == 0) ? (less(ph, pl, h[e], l[e]) == asc) : (less(h[e], l[e], ph, pl) == asc);
+            if (swap) h[e] = ph, l[e] = pl, v[e] = kv[p];
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < EM; ++e)
+    if (act && e < E) {
+      const int i = e * T + t;
+      if (kWide) kh[i] = h[e];
+      kl[i] = l[e];
+      kv[i] = v[e];
+    }
+  __syncthreads();
+}
+
+template <bool kWide>
+SX_DEV void bitonic_sort_reg(unsigned long long* kh, unsigned long long* kl, int* kv, int n) {
+  const int E = n / (int)blockDim.x;
+  if (E <= 1)
+    bitonic_sort_reg_e<kWide, 1>(kh, kl, kv, n);
+  else if (E == 2)
+    bitonic_sort_reg_e<kWide, 2>(kh, kl, kv, n);
+  else if (E == 4)
+    bitonic_sort_reg_e<kWide, 4>(kh, kl, kv, n);
+  else
+    bitonic_sort_reg_e<kWide, 8>(kh, kl, kv, n);
+}
+
+// block-wide exclusive scan of one int per thread (warp shuffles + one pass over
+// the 32 warp totals: 2 barriers); returns the total
+SX_DEV int block_excl_scan_fast(UpdSmem& sm, int v, int& excl) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm.wscan[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = kUpdThreads / 32;
+    const int t = lane < nw ? sm.wscan[lane] : 0;
+    int s = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sm.wscan[lane] = s - t;
+    if (lane == 31) sm.wscan[nw] = s;
+  }
+  __syncthreads();
+  excl = sm.wscan[w] + x - v;
+  const int total = sm.wscan[kUpdThreads / 32];
+  __syncthreads();  // wscan is reused by the next call
+  return total;
+}
+
 // block-wide exclusive scan of one int per thread; returns the total
 SX_DEV int block_excl_scan(UpdSmem& sm, int v, int& excl) {
   const int t = threadIdx.x;
@@ -621,6 +812,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
+  griddep_wait();  // launched early (chunked row path): the survivors of this round
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int tid = threadIdx.x;
   const int K = L.K;
@@ -792,7 +984,10 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     sk_v[i] = -1;
   }
   __syncthreads();
-  bitonic_sort_128(sk_h, sk_l, sk_v, np2);
+  if (np2 >= 64 && g_sort_reg)
+    bitonic_sort_reg<true>(sk_h, sk_l, sk_v, np2);
+  else
+    bitonic_sort_128(sk_h, sk_l, sk_v, np2);
 
   // ---- 3. write the new materialized list (sorted), remap old -> new ----
   int* remap = at<int>(ws, L.remap);
@@ -833,7 +1028,10 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   }
   for (int i = tid; i < 256; i += kUpdThreads) sm.depth_start[i] = 0x7fffffff;
   __syncthreads();
-  bitonic_sort_64(sk_l, sk_v, np2);
+  if (np2 >= 64 && g_sort_reg)
+    bitonic_sort_reg<false>(nullptr, sk_l, sk_v, np2);
+  else
+    bitonic_sort_64(sk_l, sk_v, np2);
   for (int r = tid; r < sel; r += kUpdThreads) {
     const int d = lo_depth(sk_l[r]);
     if (r == 0 || lo_depth(sk_l[r - 1]) != d) sm.depth_start[d] = r;
@@ -885,29 +1083,38 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   }  // n_new > 0
 
   // ---- 6. next batch: first B unexpanded nodes with depth < D and key < threshold ----
+  // The per-position data of the scan and of the ancestor walk is staged in
+  // shared memory first (CTA 0 owns the sort buffers now): the walk follows up
+  // to D dependent parent links per batch node, an L2 round trip each otherwise.
   const int per = (sel + kUpdThreads - 1) / kUpdThreads;
   const int p0 = min(sel, tid * per), p1 = min(sel, p0 + per);
   const double* nll_arr = at<double>(ws, L.m_nll[dst]);
   int* slot_arr = at<int>(ws, L.m_slot[dst]);
-  auto eligible = [&](int pos) -> bool {
-    if (slot_arr[pos] >= 0) return false;
+  int* par_s = reinterpret_cast<int*>(sk_h);  // [kpad]
+  int* slot_s = par_s + L.kpad;               // [kpad] (sk_h spans 2 kpad ints)
+  int* elig_s = sk_v;                         // [kpad]
+  for (int pos = tid; pos < sel; pos += kUpdThreads) {
+    const int sl = slot_arr[pos];
     const unsigned long long lo = lo_arr[pos];
-    if (lo_depth(lo) >= L.D) return false;
-    if (!has_thr) return true;
-    return key_less((unsigned long long)__double_as_longlong(nll_arr[pos]), lo, th, tl);
-  };
+    par_s[pos] = par[pos];
+    slot_s[pos] = sl;
+    elig_s[pos] = sl < 0 && lo_depth(lo) < L.D &&
+                  (!has_thr || key_less((unsigned long long)__double_as_longlong(nll_arr[pos]), lo, th, tl));
+  }
+  __syncthreads();
   int cnt = 0;
-  for (int pos = p0; pos < p1; ++pos) cnt += eligible(pos);
+  for (int pos = p0; pos < p1; ++pos) cnt += elig_s[pos];
   int excl;
-  const int total = block_excl_scan(sm, cnt, excl);
+  const int total = block_excl_scan_fast(sm, cnt, excl);
   const int batch_n = min(total, L.B);
   const int slot_base = c->slot_next;
   int rank = excl;
   for (int pos = p0; pos < p1 && rank < batch_n; ++pos) {
-    if (!eligible(pos)) continue;
+    if (!elig_s[pos]) continue;
     const int b = rank++;
     const int slot = slot_base + b;
     slot_arr[pos] = slot;
+    slot_s[pos] = slot;
     const unsigned long long lo = lo_arr[pos];
     const int depth = lo_depth(lo);
     at<int>(ws, L.b_node)[b] = pos;
@@ -922,12 +1129,12 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   // ancestor-slot lists, root first: [root_slot, slot(depth 1), ..., slot(self)]
   for (int b = tid; b < batch_n; b += kUpdThreads) {
     const int pos = at<int>(ws, L.b_node)[b];
-    const int depth = lo_depth(lo_arr[pos]);
+    const int depth = at<int>(ws, L.b_depth)[b];
     int* anc = at<int>(ws, L.b_anc) + b * (L.D + 1);
     int q = pos;
     for (int k = depth; k >= 1; --k) {
-      anc[k] = slot_arr[q];
-      q = par[q];
+      anc[k] = slot_s[q];
+      q = par_s[q];
     }
     anc[0] = c->root_slot;
     at<int>(ws, L.b_anc_len)[b] = depth + 1;
@@ -1231,6 +1438,24 @@ extern "C" int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot
   return SX_OK;
 }
 
+// SX_TREE_PDL=0: ordinary stream order for the chunked row path and the update (A/B)
+static const int g_tree_pdl = getenv("SX_TREE_PDL") ? atoi(getenv("SX_TREE_PDL")) : 1;
+
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_tree_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static int g_tree_unfused = 0;  // sx_tree_set_impl: 1 = the two-kernel row_stats + score path (A/B)
 
 extern "C" int sx_tree_set_impl(int unfused) {
@@ -1273,7 +1498,7 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
     // persistent grids of (row, chunk) units, sized to the resident CTAs
     static int occ[3] = {0, 0, 0};
     if (!occ[0]) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], tree_rows_max_kernel, kMaxThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], tree_rows_max_kernel<2>, kMaxThreads, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], tree_rows_sum_kernel, kRowThreads, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], tree_rows_score_kernel, kRowThreads, 0);
       for (int& o : occ) o = o < 1 ? 1 : o;
@@ -1282,12 +1507,22 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
     const long long ub = (long long)nrows * ((V + kRowChunkB - 1) / kRowChunkB);
     auto grid_of = [&](long long units, int o) { return (int)(units < (long long)o * kNumSMs ? units : (long long)o * kNumSMs); };
     const float* z = reinterpret_cast<const float*>(rows);
-    const int vec4 = (V % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0);
-    tree_rows_max_kernel<<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, vec4, r0, r1);
+    // vec4: 2 = pipelined batch-max loop, 1 = per-element online loop (SX_TREE_MAX_PIPE=0, A/B), 0 = scalar
+    static const int pipe = getenv("SX_TREE_MAX_PIPE") ? atoi(getenv("SX_TREE_MAX_PIPE")) : 1;
+    const int vec4 = ((V % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0)) ? (pipe ? 2 : 1) : 0;
+    if (vec4 == 2)
+      tree_rows_max_kernel<2><<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, r0, r1);
+    else if (vec4 == 1)
+      tree_rows_max_kernel<1><<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, r0, r1);
+    else
+      tree_rows_max_kernel<0><<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, r0, r1);
     SX_CHECK_LAUNCH("tree_rows_max_kernel");
-    tree_rows_sum_kernel<<<grid_of(ub, occ[1]), kRowThreads, 0, stream>>>(w, L, z, ld);
+    // sum, score and the update are launched with programmatic stream serialization:
+    // each grid becomes resident while its predecessor drains and waits in
+    // griddepcontrol.wait (full completion + memory flush), hiding the launch gaps
+    launch_pdl(tree_rows_sum_kernel, dim3(grid_of(ub, occ[1])), dim3(kRowThreads), 0, stream, w, L, z, ld);
     SX_CHECK_LAUNCH("tree_rows_sum_kernel");
-    tree_rows_score_kernel<<<grid_of(ub, occ[2]), kRowThreads, 0, stream>>>(w, L, z, ld);
+    launch_pdl(tree_rows_score_kernel, dim3(grid_of(ub, occ[2])), dim3(kRowThreads), 0, stream, w, L, z, ld);
     SX_CHECK_LAUNCH("tree_rows_score_kernel");
   } else if (score_mode == SX_SCORE_RAW) {
     if (row_kind == SX_ROWS_LOGITS_F32) {
@@ -1302,19 +1537,27 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
   }
   const size_t smem = upd_smem_bytes(L);
   if (smem > 227 * 1024) return arg_error("tree: update needs %zu B of shared memory", smem);
+  static const int sort_reg_init = [] {
+    const int v = getenv("SX_TREE_SORT_REG") ? atoi(getenv("SX_TREE_SORT_REG")) : 1;
+    if (v != 1) cudaMemcpyToSymbol(g_sort_reg, &v, sizeof(int));
+    return v;
+  }();
+  (void)sort_reg_init;
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(kUpdCluster);
     cfg.blockDim = dim3(kUpdThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kUpdCluster;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = g_tree_pdl;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, tree_update_kernel, w, L, final);
   }
   SX_CHECK_LAUNCH("tree_update_kernel");

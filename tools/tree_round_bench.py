@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.3)
     ap.add_argument("--builds", type=int, default=5)
     ap.add_argument("--impl", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=1, help="replay each round's launches as a CUDA graph (as the draft's fused round does)")
     a = ap.parse_args()
     _lib.call("sx_tree_set_impl", a.impl)
     peak = 6549.4
@@ -39,14 +40,25 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(0)
     rows = torch.empty((a.B, a.V), device="cuda")
     per_round = []  # (batch_n, ms)
+    graph = None
     for bi in range(a.builds + 1):
         ws.begin()
         n = 1
         while True:
             rows[:n].normal_(0.0, a.scale, generator=g)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if a.graph and graph is None and bi > 0 and n == a.B:
+                graph = torch.cuda.CUDAGraph()  # captured once the static launch state is warm
+                with torch.cuda.graph(graph):
+                    ws.launch_round(rows, SCORE_RAW)
+                ws.begin()  # the capture did not run; restart this build
+                n = 1
+                rows[:n].normal_(0.0, a.scale, generator=g)
             e0.record()
-            ws.launch_round(rows, SCORE_RAW)
+            if graph is not None and n == a.B:
+                graph.replay()
+            else:
+                ws.launch_round(rows, SCORE_RAW)
             e1.record()
             ctl = ws.read_ctl()
             if bi > 0:
@@ -56,6 +68,7 @@ def main():
                 break
     full = [(n, ms) for n, ms in per_round if n == a.B]
     out = {"V": a.V, "K": a.K, "B": a.B, "scale": a.scale, "impl": "fused" if a.impl == 0 else "row_stats+score",
+           "graph": bool(a.graph),
            "rounds_per_build": len(per_round) / a.builds}
     if full:
         ms = sum(x for _, x in full) / len(full)
