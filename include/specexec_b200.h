@@ -114,6 +114,9 @@ SX_API int sx_tp_reduce_bcast(const void* inbox, int rank, int world, int M, int
 enum { SX_ROWS_LOGITS_F32 = 0, SX_ROWS_PROBS_F64 = 1 };
 enum { SX_SCORE_RAW = 0, SX_SCORE_ARGMAX = 1, SX_SCORE_WARP = 2 };
 SX_API long long sx_tree_workspace_bytes(int K, int B, int V, int D);
+/* byte offsets into the workspace, in this order: ctl, b_node, b_nll, b_depth, b_lex,
+ * b_slot, b_token, b_anc, b_anc_len, f_anc, f_anc_len, f_depth, f_token, w_rows,
+ * b_pos, b_dense, total, r_aux; returns the number of offsets available */
 SX_API int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n);
 SX_API int sx_tree_begin(void* ws, int K, int B, int V, int D, int root_slot, int pad_slot,
                          cudaStream_t stream);

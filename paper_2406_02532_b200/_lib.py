@@ -12,7 +12,9 @@ import os
 import pathlib
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libspecexec_b200.so"
+# SX_LIB_PATH: an instrumented build of the same library (e.g. `make TRACE=1` for
+# tools/tree_round_bench.py --trace); the product default is the in-tree build
+LIB_PATH = pathlib.Path(os.environ.get("SX_LIB_PATH", _HERE / "libspecexec_b200.so"))
 
 _c_int = ctypes.c_int
 _c_ll = ctypes.c_longlong

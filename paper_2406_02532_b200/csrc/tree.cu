@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(256) tree_score_kernel(uint8_t* ws, TreeLayout
 // good to ~1e-5), and e_v / S are the same canonical values.
 constexpr int kMaxThreads = 128;  // max-pass CTA: small, so >= 1024 of them are resident (one row each at B = 1024)
 
-// kVec: 2 = pipelined batch-max loop, 1 = per-element online loop (A/B), 0 = scalar (unaligned rows);
+// kVec: 2 / 3 = pipelined batch-max loop with 4 / 8 x 16 B per thread per batch, 1 = per-element online loop (A/B), 0 = scalar (unaligned rows);
 // separate instantiations, so the default path keeps its own (small) register budget
 template <int kVec>
 __global__ void __launch_bounds__(kMaxThreads) tree_rows_max_kernel(uint8_t* ws, TreeLayout L,
@@ -330,13 +330,13 @@ __global__ void __launch_bounds__(kMaxThreads) tree_rows_max_kernel(uint8_t* ws,
         sacc += __expf(x - m);
       }
     };
-    if constexpr (vec4 == 2) {
+    if constexpr (vec4 >= 2) {
       // chunk bounds are multiples of 4. Register double buffer: the next 4 x 16 B
       // per thread are in flight while the current ones are folded in; per batch
       // one max, one rescale, then independent exps (no per-element branch chain).
       const float4* z4 = reinterpret_cast<const float4*>(z + v0);
       const int n4 = (v1 - v0) >> 2;
-      constexpr int U = 4;
+      constexpr int U = vec4 == 3 ? 8 : 4;
       const float4 ninf = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
       float4 cur[U], nxt[U];
 #pragma unroll
@@ -642,8 +642,25 @@ SX_DEV void bitonic_sort_64(unsigned long long* kk, int* kv, int n) {
 // i = e*T + t, e < n / T: partner distance j < 32 -> warp shuffle, j >= T ->
 // the thread's own registers, otherwise one shared-memory exchange (2 barriers).
 // n = 1024: 40 of the 55 stages stay in registers.
+// make TRACE=1: the update kernel's CTA 0 stamps %globaltimer at its phase
+// boundaries into r_aux[16..48) (8-byte slots; tools/tree_round_bench.py --trace)
+#ifdef SX_TREE_TRACE
+SX_DEV void trace_mark(uint8_t* ws, const TreeLayout& L, int slot) {
+  if (threadIdx.x == 0 && cluster_ctarank() == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    reinterpret_cast<unsigned long long*>(at<int>(ws, L.r_aux) + 16)[slot] = t;
+  }
+}
+#define SX_TRACE(slot) trace_mark(ws, L, slot)
+#else
+#define SX_TRACE(slot) ((void)0)
+#endif
+
 // SX_TREE_SORT_REG=0: the shared-memory network for every stage (A/B)
 __constant__ int g_sort_reg = 1;
+// SX_TREE_MERGE=0: radix select + sort of the union in every round (A/B)
+__constant__ int g_update_merge = 1;
 
 template <bool kWide, int EM>
 SX_DEV void bitonic_sort_reg_e(unsigned long long* kh, unsigned long long* kl, int* kv, int n) {
@@ -812,7 +829,9 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
+  SX_TRACE(0);
   griddep_wait();  // launched early (chunked row path): the survivors of this round
+  SX_TRACE(1);
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int tid = threadIdx.x;
   const int K = L.K;
@@ -834,6 +853,12 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   // writes after the cluster barriers of steps 1-2 (n_new > 0), and with
   // n_new == 0 the other CTAs have nothing to do
   if (n_new == 0 && crank != 0) return;
+  // Merge path: the materialized list is already sorted by key (relabelling lex
+  // ranks is monotone within a depth, so it stays sorted across rounds), so when
+  // the survivors fit the sort buffer, CTA 0 sorts just them and merges the two
+  // runs -- the same K smallest keys in the same order as select + sort of the union
+  const bool merge_path = g_update_merge && n_old > 0 && n_new <= L.kpad && L.kpad >= 64;
+  if (merge_path && crank != 0) return;
   const int i0 = (int)((long long)n * crank / kUpdCluster), i1 = (int)((long long)n * (crank + 1) / kUpdCluster);
   int* lex;
   const int* par;
@@ -861,6 +886,80 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   } else {
     dst = nxt;
 
+  int np2 = 1;  // power of two >= sel (the lex sort below)
+  if (merge_path) {
+    sel = min(n, K);
+    while (np2 < sel) np2 <<= 1;
+    // survivors -> shared memory, sorted (register bitonic network; pads sort last)
+    int np2s = 64;
+    while (np2s < n_new) np2s <<= 1;
+    for (int j = tid; j < np2s; j += kUpdThreads) {
+      if (j < n_new) {
+        sk_h[j] = (unsigned long long)__double_as_longlong(at<double>(ws, L.s_nll)[j]);
+        sk_l[j] = at<unsigned long long>(ws, L.s_lo)[j];
+        sk_v[j] = n_old + j;
+      } else {
+        sk_h[j] = ~0ull;
+        sk_l[j] = ~0ull;
+        sk_v[j] = -1;
+      }
+    }
+    __syncthreads();
+    bitonic_sort_reg<true>(sk_h, sk_l, sk_v, np2s);
+    // merge path over the output positions [0, sel): thread t takes [o0, o1); the
+    // split (i old, o - i survivors) is the merge-path diagonal (keys are unique)
+    const double* a_nll = at<double>(ws, L.m_nll[cur]);
+    const unsigned long long* a_lo = at<unsigned long long>(ws, L.m_lo[cur]);
+    constexpr int kMergeMax = 8;  // sel <= 8192 = 8 x kUpdThreads
+    const int per_o = (sel + kUpdThreads - 1) / kUpdThreads;
+    const int o0 = min(sel, tid * per_o), o1 = min(sel, o0 + per_o);
+    unsigned long long oh[kMergeMax], ol[kMergeMax];
+    int ov[kMergeMax];
+    {
+      // smallest i in [max(0, o0 - n_new), min(o0, n_old)] with A[i] > S[o0 - i - 1]
+      int lo_i = max(0, o0 - n_new), hi_i = min(o0, n_old);
+      while (lo_i < hi_i) {
+        const int mid = (lo_i + hi_i) >> 1;
+        const int j = o0 - mid - 1;  // compare A[mid] with S[j]
+        const unsigned long long ah = (unsigned long long)__double_as_longlong(a_nll[mid]);
+        if (key_less(sk_h[j], sk_l[j], ah, a_lo[mid]))
+          hi_i = mid;  // S[j] < A[mid]: A[mid] comes after S[j], so fewer than mid+1 old before o0
+        else
+          lo_i = mid + 1;
+      }
+      int i = lo_i, j = o0 - lo_i;
+      unsigned long long ah = i < n_old ? (unsigned long long)__double_as_longlong(a_nll[i]) : ~0ull;
+      unsigned long long al = i < n_old ? a_lo[i] : ~0ull;
+#pragma unroll
+      for (int k = 0; k < kMergeMax; ++k) {
+        if (o0 + k < o1) {
+          const bool take_s = j < n_new && (i >= n_old || key_less(sk_h[j], sk_l[j], ah, al));
+          if (take_s) {
+            oh[k] = sk_h[j];
+            ol[k] = sk_l[j];
+            ov[k] = sk_v[j];
+            ++j;
+          } else {
+            oh[k] = ah;
+            ol[k] = al;
+            ov[k] = i;
+            ++i;
+            ah = i < n_old ? (unsigned long long)__double_as_longlong(a_nll[i]) : ~0ull;
+            al = i < n_old ? a_lo[i] : ~0ull;
+          }
+        }
+      }
+    }
+    __syncthreads();  // every thread has read the survivor run
+#pragma unroll
+    for (int k = 0; k < kMergeMax; ++k)
+      if (o0 + k < o1) {
+        sk_h[o0 + k] = oh[k];
+        sk_l[o0 + k] = ol[k];
+        sk_v[o0 + k] = ov[k];
+      }
+    __syncthreads();
+  } else {
   // ---- 1. select the K smallest keys (radix select over 16 8-bit digits) ----
   // Every CTA of the cluster histograms its slice [i0, i1) of the n keys; the
   // 256-bin totals are summed over DSMEM and scanned in parallel by every CTA.
@@ -976,7 +1075,6 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   cluster.sync();  // CTA 0 holds every selected key; nobody touches a peer's smem after this
   if (crank != 0) return;
   sel = sm.elig_total;  // == min(n, K)
-  int np2 = 1;
   while (np2 < sel) np2 <<= 1;
   for (int i = sel + tid; i < np2; i += kUpdThreads) {
     sk_h[i] = ~0ull;
@@ -988,7 +1086,9 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     bitonic_sort_reg<true>(sk_h, sk_l, sk_v, np2);
   else
     bitonic_sort_128(sk_h, sk_l, sk_v, np2);
+  }  // select + sort
 
+  SX_TRACE(2);
   // ---- 3. write the new materialized list (sorted), remap old -> new ----
   int* remap = at<int>(ws, L.remap);
   int* b_node = at<int>(ws, L.b_node);
@@ -1021,25 +1121,125 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   }
   __syncthreads();
 
-  // ---- 4. lex ranks within depth: sort the lo keys (depth | lex(parent) | token) ----
-  for (int pos = tid; pos < np2; pos += kUpdThreads) {
-    sk_l[pos] = pos < sel ? at<unsigned long long>(ws, L.m_lo[nxt])[pos] : ~0ull;
-    sk_v[pos] = pos;
-  }
-  for (int i = tid; i < 256; i += kUpdThreads) sm.depth_start[i] = 0x7fffffff;
-  __syncthreads();
-  if (np2 >= 64 && g_sort_reg)
-    bitonic_sort_reg<false>(nullptr, sk_l, sk_v, np2);
-  else
-    bitonic_sort_64(sk_l, sk_v, np2);
-  for (int r = tid; r < sel; r += kUpdThreads) {
-    const int d = lo_depth(sk_l[r]);
-    if (r == 0 || lo_depth(sk_l[r - 1]) != d) sm.depth_start[d] = r;
-  }
-  __syncthreads();
+  SX_TRACE(3);
+  // ---- 4. lex ranks within depth: order by the lo keys (depth | lex(parent) | token) ----
   lex = at<int>(ws, L.m_lex[nxt]);
-  for (int r = tid; r < sel; r += kUpdThreads) lex[sk_v[r]] = r - sm.depth_start[lo_depth(sk_l[r])];
-  __syncthreads();
+  const unsigned long long* lo_new = at<unsigned long long>(ws, L.m_lo[nxt]);
+  if (merge_path) {
+    // The kept old nodes are already in lex order (their old lex ranks; removing
+    // nodes or relabelling parents preserves it), so only the new nodes are
+    // sorted, then the two runs are merged -- the order the full sort gives.
+    const unsigned long long* lo_old = at<unsigned long long>(ws, L.m_lo[cur]);
+    const int* lex_old = at<int>(ws, L.m_lex[cur]);
+    int* ds_old = sm.hist[0];  // exclusive depth starts of the old list (the histograms are unused here)
+    int* ds_new = sm.hist[1];  // ... and of the new list (= sm.depth_start of the sort path)
+    for (int i = tid; i < 256; i += kUpdThreads) ds_old[i] = ds_new[i] = 0;
+    __syncthreads();
+    for (int pos = tid; pos < n_old; pos += kUpdThreads) atomicAdd(&ds_old[lo_depth(lo_old[pos])], 1);
+    for (int pos = tid; pos < sel; pos += kUpdThreads) atomicAdd(&ds_new[lo_depth(lo_new[pos])], 1);
+    __syncthreads();
+    if (tid == 0 || tid == 32) {
+      int* a = tid == 0 ? ds_old : ds_new;
+      int s = 0;
+      for (int i = 0; i < 256; ++i) {
+        const int c = a[i];
+        a[i] = s;
+        s += c;
+      }
+    }
+    int* a_raw = reinterpret_cast<int*>(sk_h);  // [kpad]: old list in lex order -> new position or -1
+    int* mark = a_raw + L.kpad;                  // [kpad]: 1 = new node
+    for (int pos = tid; pos < sel; pos += kUpdThreads) mark[pos] = 1;
+    if (tid == 0) sm.sel_n = 0;
+    __syncthreads();
+    for (int pos = tid; pos < n_old; pos += kUpdThreads) {
+      const int r = remap[pos];
+      a_raw[ds_old[lo_depth(lo_old[pos])] + lex_old[pos]] = r;
+      if (r >= 0) mark[r] = 0;
+    }
+    __syncthreads();
+    for (int pos = tid; pos < sel; pos += kUpdThreads)
+      if (mark[pos]) {
+        const int k = atomicAdd(&sm.sel_n, 1);
+        sk_l[k] = lo_new[pos];
+        sk_v[k] = pos;
+      }
+    __syncthreads();
+    const int nb = sm.sel_n;
+    if (nb > 0) {
+      int npb = 64;
+      while (npb < nb) npb <<= 1;
+      for (int k = nb + tid; k < npb; k += kUpdThreads) {
+        sk_l[k] = ~0ull;
+        sk_v[k] = -1;
+      }
+      __syncthreads();
+      bitonic_sort_reg<false>(nullptr, sk_l, sk_v, npb);  // ends with a barrier
+    }
+    // ordered compaction of the kept old nodes, in place (each thread reads its chunk first)
+    constexpr int kCh = 8;  // n_old <= 8192 = 8 x kUpdThreads
+    const int per_a = (n_old + kUpdThreads - 1) / kUpdThreads;
+    const int a0 = min(n_old, tid * per_a), a1 = min(n_old, a0 + per_a);
+    int av[kCh], acnt = 0;
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+      av[k] = (a0 + k < a1) ? a_raw[a0 + k] : -1;
+      acnt += av[k] >= 0;
+    }
+    int aex;
+    const int na = block_excl_scan_fast(sm, acnt, aex);  // its barriers order the reads before the writes
+#pragma unroll
+    for (int k = 0; k < kCh; ++k)
+      if (av[k] >= 0) a_raw[aex++] = av[k];
+    __syncthreads();
+    // merge the kept old run (keys lo_new[a_raw[i]]) with the new run (sk_l / sk_v) over r in [0, sel)
+    const int per_o = (sel + kUpdThreads - 1) / kUpdThreads;
+    const int o0 = min(sel, tid * per_o), o1 = min(sel, o0 + per_o);
+    int lo_i = max(0, o0 - nb), hi_i = min(o0, na);
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i) >> 1;
+      if (sk_l[o0 - mid - 1] < lo_new[a_raw[mid]])
+        hi_i = mid;
+      else
+        lo_i = mid + 1;
+    }
+    int i = lo_i, j = o0 - lo_i;
+    unsigned long long ak = i < na ? lo_new[a_raw[i]] : ~0ull;
+    for (int r = o0; r < o1; ++r) {
+      int pos;
+      unsigned long long key;
+      if (j < nb && (i >= na || sk_l[j] < ak)) {
+        pos = sk_v[j];
+        key = sk_l[j];
+        ++j;
+      } else {
+        pos = a_raw[i];
+        key = ak;
+        ++i;
+        ak = i < na ? lo_new[a_raw[i]] : ~0ull;
+      }
+      lex[pos] = r - ds_new[lo_depth(key)];
+    }
+    __syncthreads();
+  } else {
+    for (int pos = tid; pos < np2; pos += kUpdThreads) {
+      sk_l[pos] = pos < sel ? lo_new[pos] : ~0ull;
+      sk_v[pos] = pos;
+    }
+    for (int i = tid; i < 256; i += kUpdThreads) sm.depth_start[i] = 0x7fffffff;
+    __syncthreads();
+    if (np2 >= 64 && g_sort_reg)
+      bitonic_sort_reg<false>(nullptr, sk_l, sk_v, np2);
+    else
+      bitonic_sort_64(sk_l, sk_v, np2);
+    for (int r = tid; r < sel; r += kUpdThreads) {
+      const int d = lo_depth(sk_l[r]);
+      if (r == 0 || lo_depth(sk_l[r - 1]) != d) sm.depth_start[d] = r;
+    }
+    __syncthreads();
+    for (int r = tid; r < sel; r += kUpdThreads) lex[sk_v[r]] = r - sm.depth_start[lo_depth(sk_l[r])];
+    __syncthreads();
+  }
   par = at<int>(ws, L.m_parent[nxt]);
   lo_arr = at<unsigned long long>(ws, L.m_lo[nxt]);
   for (int pos = tid; pos < sel; pos += kUpdThreads) {
@@ -1049,6 +1249,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   }
   __syncthreads();
 
+  SX_TRACE(4);
   // ---- 5. threshold ----
   has_thr = sel >= K;
   th = has_thr ? (unsigned long long)__double_as_longlong(at<double>(ws, L.m_nll[nxt])[K - 1]) : 0;
@@ -1082,6 +1283,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   }
   }  // n_new > 0
 
+  SX_TRACE(5);
   // ---- 6. next batch: first B unexpanded nodes with depth < D and key < threshold ----
   // The per-position data of the scan and of the ancestor walk is staged in
   // shared memory first (CTA 0 owns the sort buffers now): the walk follows up
@@ -1093,15 +1295,36 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   int* par_s = reinterpret_cast<int*>(sk_h);  // [kpad]
   int* slot_s = par_s + L.kpad;               // [kpad] (sk_h spans 2 kpad ints)
   int* elig_s = sk_v;                         // [kpad]
-  for (int pos = tid; pos < sel; pos += kUpdThreads) {
-    const int sl = slot_arr[pos];
-    const unsigned long long lo = lo_arr[pos];
-    par_s[pos] = par[pos];
-    slot_s[pos] = sl;
-    elig_s[pos] = sl < 0 && lo_depth(lo) < L.D &&
-                  (!has_thr || key_less((unsigned long long)__double_as_longlong(nll_arr[pos]), lo, th, tl));
+  int* bnode_s = reinterpret_cast<int*>(sk_l);  // [kpad]: batch b -> position (batch_n <= sel <= kpad)
+  int* bdepth_s = bnode_s + L.kpad;             // [kpad]
+  // The list is sorted by key and the threshold is its K-th key, so "key <
+  // threshold" is exactly "position < K - 1": no key loads. Loads are issued
+  // kStg at a time per thread (independent L2 round trips).
+  constexpr int kStg = 4;
+  for (int base = 0; base < sel; base += kStg * kUpdThreads) {
+    int sl[kStg], pr[kStg];
+    unsigned long long lo[kStg];
+#pragma unroll
+    for (int k = 0; k < kStg; ++k) {
+      const int pos = base + k * kUpdThreads + tid;
+      if (pos < sel) {
+        sl[k] = slot_arr[pos];
+        pr[k] = par[pos];
+        lo[k] = lo_arr[pos];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kStg; ++k) {
+      const int pos = base + k * kUpdThreads + tid;
+      if (pos < sel) {
+        par_s[pos] = pr[k];
+        slot_s[pos] = sl[k];
+        elig_s[pos] = sl[k] < 0 && lo_depth(lo[k]) < L.D && (!has_thr || pos < K - 1);
+      }
+    }
   }
   __syncthreads();
+  SX_TRACE(6);
   int cnt = 0;
   for (int pos = p0; pos < p1; ++pos) cnt += elig_s[pos];
   int excl;
@@ -1117,6 +1340,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     slot_s[pos] = slot;
     const unsigned long long lo = lo_arr[pos];
     const int depth = lo_depth(lo);
+    bnode_s[b] = pos;
+    bdepth_s[b] = depth;
     at<int>(ws, L.b_node)[b] = pos;
     at<double>(ws, L.b_nll)[b] = nll_arr[pos];
     at<int>(ws, L.b_depth)[b] = depth;
@@ -1126,20 +1351,24 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     at<int>(ws, L.b_pos)[b] = c->root_slot + depth;
   }
   __syncthreads();
+  SX_TRACE(7);
   // ancestor-slot lists, root first: [root_slot, slot(depth 1), ..., slot(self)]
+  // (walked through the staged parent / slot tables; assembling the rows in shared
+  // memory first and copying them out a warp per row measured slower)
+  const int root_slot = c->root_slot;
   for (int b = tid; b < batch_n; b += kUpdThreads) {
-    const int pos = at<int>(ws, L.b_node)[b];
-    const int depth = at<int>(ws, L.b_depth)[b];
+    const int depth = bdepth_s[b];
     int* anc = at<int>(ws, L.b_anc) + b * (L.D + 1);
-    int q = pos;
+    int q = bnode_s[b];
     for (int k = depth; k >= 1; --k) {
       anc[k] = slot_s[q];
       q = par_s[q];
     }
-    anc[0] = c->root_slot;
+    anc[0] = root_slot;
     at<int>(ws, L.b_anc_len)[b] = depth + 1;
-    at<int>(ws, L.b_dense)[b] = c->root_slot;
+    at<int>(ws, L.b_dense)[b] = root_slot;
   }
+  SX_TRACE(8);
   // padded rows [batch_n, B): a fixed-shape draft forward (CUDA graph) may run
   // them; they write only the scratch KV slot and see just the committed prefix
   for (int b = batch_n + tid; b < L.B; b += kUpdThreads) {
@@ -1152,6 +1381,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
     at<int>(ws, L.b_dense)[b] = c->root_slot;
   }
   __syncthreads();
+  SX_TRACE(9);
   if (tid == 0) {
     c->cur = dst;
     c->count = sel;
@@ -1415,7 +1645,7 @@ extern "C" long long sx_tree_workspace_bytes(int K, int B, int V, int D) {
 extern "C" int sx_tree_offsets(int K, int B, int V, int D, long long* out, int n) {
   TreeLayout L = host_layout(K, B, V, D);
   const long long vals[] = {L.ctl,   L.b_node,    L.b_nll, L.b_depth,   L.b_lex,   L.b_slot,  L.b_token, L.b_anc,
-                            L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows, L.b_pos, L.b_dense, L.total};
+                            L.b_anc_len, L.f_anc, L.f_anc_len, L.f_depth, L.f_token, L.w_rows, L.b_pos, L.b_dense, L.total, L.r_aux};
   const int m = (int)(sizeof(vals) / sizeof(vals[0]));
   for (int i = 0; i < n && i < m; ++i) out[i] = vals[i];
   return m;
@@ -1509,8 +1739,14 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
     const float* z = reinterpret_cast<const float*>(rows);
     // vec4: 2 = pipelined batch-max loop, 1 = per-element online loop (SX_TREE_MAX_PIPE=0, A/B), 0 = scalar
     static const int pipe = getenv("SX_TREE_MAX_PIPE") ? atoi(getenv("SX_TREE_MAX_PIPE")) : 1;
-    const int vec4 = ((V % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0)) ? (pipe ? 2 : 1) : 0;
-    if (vec4 == 2)
+    const int vec4 = ((V % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0))
+                         ? (pipe == 2 ? 3 : (pipe ? 2 : 1))
+                         : 0;
+    if (vec4 == 3) {
+      static int occ3 = 0;
+      if (!occ3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, tree_rows_max_kernel<3>, kMaxThreads, 0);
+      tree_rows_max_kernel<3><<<grid_of(ua, occ3 < 1 ? 1 : occ3), kMaxThreads, 0, stream>>>(w, L, z, ld, r0, r1);
+    } else if (vec4 == 2)
       tree_rows_max_kernel<2><<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, r0, r1);
     else if (vec4 == 1)
       tree_rows_max_kernel<1><<<grid_of(ua, occ[0]), kMaxThreads, 0, stream>>>(w, L, z, ld, r0, r1);
@@ -1540,6 +1776,8 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
   static const int sort_reg_init = [] {
     const int v = getenv("SX_TREE_SORT_REG") ? atoi(getenv("SX_TREE_SORT_REG")) : 1;
     if (v != 1) cudaMemcpyToSymbol(g_sort_reg, &v, sizeof(int));
+    const int m = getenv("SX_TREE_MERGE") ? atoi(getenv("SX_TREE_MERGE")) : 1;
+    if (m != 1) cudaMemcpyToSymbol(g_update_merge, &m, sizeof(int));
     return v;
   }();
   (void)sort_reg_init;

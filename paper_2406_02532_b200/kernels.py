@@ -322,7 +322,7 @@ def verify_walk(rows: torch.Tensor, parent: torch.Tensor, token: torch.Tensor, n
 # ---------------------------------------------------------------------------
 
 _OFF_NAMES = ["ctl", "b_node", "b_nll", "b_depth", "b_lex", "b_slot", "b_token", "b_anc", "b_anc_len",
-              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "b_pos", "b_dense", "total"]
+              "f_anc", "f_anc_len", "f_depth", "f_token", "w_rows", "b_pos", "b_dense", "total", "r_aux"]
 
 
 class TreeWorkspace:

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.3)
     ap.add_argument("--builds", type=int, default=5)
     ap.add_argument("--impl", type=int, default=0)
+    ap.add_argument("--trace", action="store_true", help="print the update kernel's phase stamps (a make TRACE=1 build)")
     ap.add_argument("--graph", type=int, default=1, help="replay each round's launches as a CUDA graph (as the draft's fused round does)")
     a = ap.parse_args()
     _lib.call("sx_tree_set_impl", a.impl)
@@ -40,6 +41,7 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(0)
     rows = torch.empty((a.B, a.V), device="cuda")
     per_round = []  # (batch_n, ms)
+    traces = []
     graph = None
     for bi in range(a.builds + 1):
         ws.begin()
@@ -63,6 +65,10 @@ def main():
             ctl = ws.read_ctl()
             if bi > 0:
                 per_round.append((n, e0.elapsed_time(e1)))
+                if a.trace:
+                    o = ws.off["r_aux"] + 64
+                    t = ws.buf[o : o + 80].view(torch.int64).cpu().tolist()
+                    traces.append({"batch": n, "us_from_start": [round((x - t[0]) / 1e3, 2) if x else None for x in t]})
             n = ctl["batch_n"]
             if n == 0:
                 break
@@ -77,6 +83,8 @@ def main():
                     "achieved_GBps": gbs, "hbm_peak_GBps": peak, "frac": gbs / peak})
     out["us_per_round_all"] = [round(x * 1e3, 1) for _, x in per_round[: 12]]
     out["batch_sizes"] = [n for n, _ in per_round[: 12]]
+    if a.trace:
+        out["update_phase_us"] = traces[:12]
     print(json.dumps(out))
 
 
