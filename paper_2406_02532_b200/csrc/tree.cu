@@ -437,108 +437,155 @@ __global__ void __launch_bounds__(kMaxThreads) tree_rows_max_kernel(uint8_t* ws,
   }
 }
 
+// One sum unit (row r_list[w], chunk j): e_v = exp(z_v - M) into the fp64 row
+// scratch; the last chunk to arrive forms the canonical row sum. `ready` != null
+// (fused exact pass): the sum's writer then publishes ready[b] = stamp.
+SX_DEV void rows_sum_unit(uint8_t* ws, const TreeLayout& L, const float* __restrict__ rows, long long ld, int u,
+                          int nch, RowSmemLite& sm, int& last, int* ready, int stamp) {
+  const int V = L.V, tid = threadIdx.x;
+  int* cnt = at<int>(ws, L.r_cnt) + L.B;
+  const int w = u / nch, j = u - w * nch;
+  const int b = at<int>(ws, L.r_list)[w];
+  const float* z = rows + b * ld;
+  const double M = (double)at<float>(ws, L.r_max)[b];
+  double* e = at<double>(ws, L.w_rows) + (long long)b * V;
+  const int v1 = min(V, (j + 1) * kRowChunkB);
+  for (int v = j * kRowChunkB + tid; v < v1; v += kRowThreads) e[v] = sx_exp(dsub((double)z[v], M));
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&cnt[b], 1) == nch - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double acc = 0.0;  // canonical sum: lane t adds e_t, e_t+256, ... in order
+    int v = tid;
+    for (; v + 7 * kRowThreads < V; v += 8 * kRowThreads) {  // 8 independent loads, then the ordered adds
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = __ldcg(e + v + k * kRowThreads);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = dadd(acc, x[k]);
+    }
+    for (; v < V; v += kRowThreads) acc = dadd(acc, __ldcg(e + v));
+    const double S = block_canon_sum(sm, acc);
+    if (tid == 0) {
+      at<double>(ws, L.r_sum)[b] = S;
+      cnt[b] = 0;
+      if (ready) {
+        __threadfence();
+        atomicExch(&ready[b], stamp);
+      }
+    }
+  }
+}
+
+// One score unit: exact edges log(e_v / S) and keys of the candidates the fp32
+// estimate cannot rule out; survivors appended. kFused: the row's e_v and S were
+// written by other CTAs of this grid, so they are read through L2 (__ldcg).
+template <bool kFused>
+SX_DEV void rows_score_unit(uint8_t* ws, const TreeLayout& L, const float* __restrict__ rows, long long ld, int u,
+                            int nch) {
+  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
+  const int V = L.V, tid = threadIdx.x, lane = tid & 31;
+  const bool has_thr = c->has_thr;
+  const double thr_nll = c->thr_nll;
+  const unsigned long long th = (unsigned long long)__double_as_longlong(thr_nll);
+  const unsigned long long tl = c->thr_lo;
+  const int w = u / nch, j = u - w * nch;
+  const int b = at<int>(ws, L.r_list)[w];
+  const float* z = rows + b * ld;
+  const float M = at<float>(ws, L.r_max)[b], lsa = at<float>(ws, L.r_lsa)[b];
+  const double S = kFused ? __ldcg(at<double>(ws, L.r_sum) + b) : at<double>(ws, L.r_sum)[b];
+  const double parent_nll = at<double>(ws, L.b_nll)[b];
+  const int depth = at<int>(ws, L.b_depth)[b] + 1;
+  const int plex = at<int>(ws, L.b_lex)[b];
+  const double* e = at<double>(ws, L.w_rows) + (long long)b * V;
+  const int v0 = j * kRowChunkB;
+  for (int vb = v0; vb < v0 + kRowChunkB; vb += kRowThreads) {  // whole warps iterate (ballot)
+    const int v = vb + tid;
+    bool keep = false;
+    double nll = 0.0, edge = 0.0;
+    unsigned long long lo = 0;
+    if (v < V) {
+      const float zv = z[v];
+      if (!has_thr || !(dsub(dsub(parent_nll, (double)((zv - M) - lsa)), kPrefilterSlack) > thr_nll)) {
+        const double pv = ddiv(kFused ? __ldcg(e + v) : e[v], S);
+        if (pv > 0.0) {
+          edge = sx_log(pv);
+          nll = dsub(parent_nll, edge);
+          lo = make_lo(depth, plex, v);
+          keep = !has_thr || key_less((unsigned long long)__double_as_longlong(nll), lo, th, tl);
+        }
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (mask) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&c->n_surv, __popc(mask));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        const long long k = base + __popc(mask & ((1u << lane) - 1));
+        if (k < L.cap) {
+          at<double>(ws, L.s_nll)[k] = nll;
+          at<unsigned long long>(ws, L.s_lo)[k] = lo;
+          at<double>(ws, L.s_edge)[k] = edge;
+          at<int>(ws, L.s_row)[k] = b;
+        } else {
+          c->err = 1;
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kRowThreads) tree_rows_sum_kernel(uint8_t* ws, TreeLayout L,
                                                                      const float* __restrict__ rows, long long ld) {
   __shared__ RowSmemLite sm;
   __shared__ int last;
   griddep_wait();  // launched early (programmatic stream serialization): the max pass's work list
   griddep_launch_dependents();
-  const int V = L.V, tid = threadIdx.x;
   const int nwork = *(volatile int*)at<int>(ws, L.r_aux);
-  const int nch = (V + kRowChunkB - 1) / kRowChunkB;
-  int* cnt = at<int>(ws, L.r_cnt) + L.B;
-  for (int u = blockIdx.x; u < nwork * nch; u += gridDim.x) {
-    const int w = u / nch, j = u - w * nch;
-    const int b = at<int>(ws, L.r_list)[w];
-    const float* z = rows + b * ld;
-    const double M = (double)at<float>(ws, L.r_max)[b];
-    double* e = at<double>(ws, L.w_rows) + (long long)b * V;
-    const int v1 = min(V, (j + 1) * kRowChunkB);
-    for (int v = j * kRowChunkB + tid; v < v1; v += kRowThreads) e[v] = sx_exp(dsub((double)z[v], M));
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last = atomicAdd(&cnt[b], 1) == nch - 1;
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      double acc = 0.0;  // canonical sum: lane t adds e_t, e_t+256, ... in order
-      int v = tid;
-      for (; v + 7 * kRowThreads < V; v += 8 * kRowThreads) {  // 8 independent loads, then the ordered adds
-        double x[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = __ldcg(e + v + k * kRowThreads);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc = dadd(acc, x[k]);
-      }
-      for (; v < V; v += kRowThreads) acc = dadd(acc, __ldcg(e + v));
-      const double S = block_canon_sum(sm, acc);
-      if (tid == 0) {
-        at<double>(ws, L.r_sum)[b] = S;
-        cnt[b] = 0;
-      }
-    }
-  }
+  const int nch = (L.V + kRowChunkB - 1) / kRowChunkB;
+  for (int u = blockIdx.x; u < nwork * nch; u += gridDim.x) rows_sum_unit(ws, L, rows, ld, u, nch, sm, last, nullptr, 0);
 }
 
 __global__ void __launch_bounds__(kRowThreads) tree_rows_score_kernel(uint8_t* ws, TreeLayout L,
                                                                        const float* __restrict__ rows, long long ld) {
   griddep_wait();  // launched early: the sums of the listed rows
   griddep_launch_dependents();
-  TreeCtl* c = at<TreeCtl>(ws, L.ctl);
-  const int V = L.V, tid = threadIdx.x, lane = tid & 31;
   const int nwork = at<int>(ws, L.r_aux)[0];
-  const int nch = (V + kRowChunkB - 1) / kRowChunkB;
-  const bool has_thr = c->has_thr;
-  const double thr_nll = c->thr_nll;
-  const unsigned long long th = (unsigned long long)__double_as_longlong(thr_nll);
-  const unsigned long long tl = c->thr_lo;
-  for (int u = blockIdx.x; u < nwork * nch; u += gridDim.x) {
-    const int w = u / nch, j = u - w * nch;
-    const int b = at<int>(ws, L.r_list)[w];
-    const float* z = rows + b * ld;
-    const float M = at<float>(ws, L.r_max)[b], lsa = at<float>(ws, L.r_lsa)[b];
-    const double S = at<double>(ws, L.r_sum)[b];
-    const double parent_nll = at<double>(ws, L.b_nll)[b];
-    const int depth = at<int>(ws, L.b_depth)[b] + 1;
-    const int plex = at<int>(ws, L.b_lex)[b];
-    const double* e = at<double>(ws, L.w_rows) + (long long)b * V;
-    const int v0 = j * kRowChunkB;
-    for (int vb = v0; vb < v0 + kRowChunkB; vb += kRowThreads) {  // whole warps iterate (ballot)
-      const int v = vb + tid;
-      bool keep = false;
-      double nll = 0.0, edge = 0.0;
-      unsigned long long lo = 0;
-      if (v < V) {
-        const float zv = z[v];
-        if (!has_thr || !(dsub(dsub(parent_nll, (double)((zv - M) - lsa)), kPrefilterSlack) > thr_nll)) {
-          const double pv = ddiv(e[v], S);
-          if (pv > 0.0) {
-            edge = sx_log(pv);
-            nll = dsub(parent_nll, edge);
-            lo = make_lo(depth, plex, v);
-            keep = !has_thr || key_less((unsigned long long)__double_as_longlong(nll), lo, th, tl);
-          }
-        }
-      }
-      const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (mask) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&c->n_surv, __popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) {
-          const long long k = base + __popc(mask & ((1u << lane) - 1));
-          if (k < L.cap) {
-            at<double>(ws, L.s_nll)[k] = nll;
-            at<unsigned long long>(ws, L.s_lo)[k] = lo;
-            at<double>(ws, L.s_edge)[k] = edge;
-            at<int>(ws, L.s_row)[k] = b;
-          } else {
-            c->err = 1;
-          }
-        }
-      }
-    }
+  const int nch = (L.V + kRowChunkB - 1) / kRowChunkB;
+  for (int u = blockIdx.x; u < nwork * nch; u += gridDim.x) rows_score_unit<false>(ws, L, rows, ld, u, nch);
+}
+
+// Fused exact pass (the default): the sum and score units of the listed rows in
+// ONE persistent grid (<= the resident CTAs, so every CTA is resident): each CTA
+// first takes its sum units, then its score units, and a score unit waits for
+// its row's readiness flag (ready[b] == this round's stamp, r_aux[1] + 1; the
+// update kernel advances r_aux[1] every round, so stale flags never match) --
+// one kernel boundary less per round, and with an empty work list one launch
+// instead of two. The successor (the update) is released only at the end:
+// it must not take SM resources a not-yet-resident CTA of this grid needs.
+__global__ void __launch_bounds__(kRowThreads) tree_rows_exact_kernel(uint8_t* ws, TreeLayout L,
+                                                                       const float* __restrict__ rows, long long ld) {
+  __shared__ RowSmemLite sm;
+  __shared__ int last;
+  griddep_wait();  // launched early: the max pass's work list
+  const int nwork = *(volatile int*)at<int>(ws, L.r_aux);
+  const int stamp = *(volatile int*)(at<int>(ws, L.r_aux) + 1) + 1;
+  int* ready = at<int>(ws, L.r_ready);
+  const int nch = (L.V + kRowChunkB - 1) / kRowChunkB;
+  const int units = nwork * nch;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) rows_sum_unit(ws, L, rows, ld, u, nch, sm, last, ready, stamp);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int b = at<int>(ws, L.r_list)[u / nch];
+    if (threadIdx.x == 0)
+      while (*(volatile int*)(ready + b) != stamp) __nanosleep(64);
+    __syncthreads();
+    __threadfence();
+    rows_score_unit<true>(ws, L, rows, ld, u, nch);
   }
+  griddep_launch_dependents();
 }
 
 // --------------------------------------------------------------------------
@@ -832,6 +879,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
   SX_TRACE(0);
   griddep_wait();  // launched early (chunked row path): the survivors of this round
   SX_TRACE(1);
+  if (crank == 0 && threadIdx.x == 0) ++at<int>(ws, L.r_aux)[1];  // round stamp of the fused exact pass
   TreeCtl* c = at<TreeCtl>(ws, L.ctl);
   const int tid = threadIdx.x;
   const int K = L.K;
@@ -1686,6 +1734,9 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// SX_TREE_FUSED_EXACT=0: separate sum and score kernels (A/B)
+static const int g_tree_fused_exact = getenv("SX_TREE_FUSED_EXACT") ? atoi(getenv("SX_TREE_FUSED_EXACT")) : 1;
+
 static int g_tree_unfused = 0;  // sx_tree_set_impl: 1 = the two-kernel row_stats + score path (A/B)
 
 extern "C" int sx_tree_set_impl(int unfused) {
@@ -1756,10 +1807,21 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
     // sum, score and the update are launched with programmatic stream serialization:
     // each grid becomes resident while its predecessor drains and waits in
     // griddepcontrol.wait (full completion + memory flush), hiding the launch gaps
-    launch_pdl(tree_rows_sum_kernel, dim3(grid_of(ub, occ[1])), dim3(kRowThreads), 0, stream, w, L, z, ld);
-    SX_CHECK_LAUNCH("tree_rows_sum_kernel");
-    launch_pdl(tree_rows_score_kernel, dim3(grid_of(ub, occ[2])), dim3(kRowThreads), 0, stream, w, L, z, ld);
-    SX_CHECK_LAUNCH("tree_rows_score_kernel");
+    if (g_tree_fused_exact) {
+      static int occx = 0;
+      if (!occx) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, tree_rows_exact_kernel, kRowThreads, 0);
+        if (occx < 1) occx = 1;
+      }
+      // grid <= resident capacity: the score units spin on flags set by sum units of other CTAs
+      launch_pdl(tree_rows_exact_kernel, dim3(grid_of(ub, occx)), dim3(kRowThreads), 0, stream, w, L, z, ld);
+      SX_CHECK_LAUNCH("tree_rows_exact_kernel");
+    } else {
+      launch_pdl(tree_rows_sum_kernel, dim3(grid_of(ub, occ[1])), dim3(kRowThreads), 0, stream, w, L, z, ld);
+      SX_CHECK_LAUNCH("tree_rows_sum_kernel");
+      launch_pdl(tree_rows_score_kernel, dim3(grid_of(ub, occ[2])), dim3(kRowThreads), 0, stream, w, L, z, ld);
+      SX_CHECK_LAUNCH("tree_rows_score_kernel");
+    }
   } else if (score_mode == SX_SCORE_RAW) {
     if (row_kind == SX_ROWS_LOGITS_F32) {
       tree_row_stats_kernel<<<nrows, kRowThreads, 0, stream>>>(w, L, reinterpret_cast<const float*>(rows), ld, r0, r1);

@@ -41,7 +41,8 @@ struct TreeLayout {
   long long r_pm, r_ps;  // float [B][kRowChunksMax]: per-chunk max / fp32 sum of exp(z - max)
   long long r_cnt;       // int [2][B]: chunk arrival counters (max pass, sum pass); reset by the last arriver
   long long r_list;      // int [B]: rows that need the exact passes (not prefiltered away)
-  long long r_aux;       // int [64]: [0] = rows in r_list
+  long long r_ready;     // int [B]: fused exact pass: row sum published for round stamp r_aux[1] + 1
+  long long r_aux;       // int [64]: [0] = rows in r_list, [1] = round stamp (never reset), [16..48) trace
   long long total;
 };
 
@@ -122,6 +123,7 @@ inline TreeLayout tree_layout(int K, int B, int V, int D, long long cap) {
   L.r_ps = take(4LL * B * kRowChunksMax);
   L.r_cnt = take(8LL * B);
   L.r_list = take(4LL * B);
+  L.r_ready = take(4LL * B);
   L.r_aux = take(4LL * 64);
   L.total = o;
   return L;
