@@ -95,6 +95,17 @@ def test_large_budget_markov_vs_oracle(cuda):
         assert_same_tree(g, o, (seed, K_, w))
 
 
+def test_deep_narrow_trees_vs_oracle(cuda):
+    # long ancestor chains (max_depth up to 250: the next-batch walk, the KV-slot
+    # lists and the lex merge over many depths) and small batches (many rounds)
+    for seed, V_, sharp, K_, D_, B_, w in [(21, 8, 0.02, 400, 200, 4, None), (22, 6, 0.05, 600, 250, 2, (0.6, 0.9)),
+                                           (23, 16, 0.03, 1000, 120, 8, None)]:
+        g = sx.build_sssp((3,), sx.make_synthetic(seed, V_, sharp), sx.BuilderParams(K_, D_, B_), warp_cfg(w))
+        o = ox.build_sssp((3,), ox.make_synthetic(seed, V_, sharp), ox.BuilderParams(K_, D_, B_), warp_cfg(w, False))
+        assert_same_tree(g, o, (seed, K_, D_, B_))
+        assert max(n.depth for n in g.nodes) > 15  # the chains really are deep
+
+
 def test_engine_grid_vs_reference(cuda):
     data = load("engine_grid.json")
     models = {}
