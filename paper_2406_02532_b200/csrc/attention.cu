@@ -19,6 +19,8 @@
 // lists of the CTA's tokens (<= D+1 keys each), each row masked to its own
 // segment -- so the ancestors fill the last partial committed tile. GQA:
 // one CTA serves one KV head and 64 query rows = (64 / G) tokens x G heads.
+#include <cstdlib>
+
 #include "capi_util.h"
 #include "common.cuh"
 #include "specexec_b200.h"
@@ -338,6 +340,7 @@ struct TcSmemHdr {
   int seg[kTcRows + 1];
   float red[2][kTcRows];  // per-half row max / final row sum exchange
   int last;               // key split: this CTA arrived last and merges
+  int maxanc;             // longest ancestor list of the CTA's tokens
 };
 // dynamic smem: [3 KB header][Q 32 KB][K 2 x 16 KB][V 2 x 16 KB][ancestor slots]
 constexpr int kTcQOff = 3072, kTcKOff = kTcQOff + 32768, kTcVOff = kTcKOff + 32768, kTcAncOff = kTcVOff + 32768;
@@ -467,6 +470,96 @@ SX_DEV void merge_splits(const AttnArgs& a, TcSmemHdr& hd, int kvh, int zsplit, 
   }
 }
 
+// SX_ATTN_ANC_CUDA=0: ancestors always as masked key tiles (A/B)
+__constant__ int g_attn_anc_cuda = 1;
+
+// dot of 8 bf16 pairs (16 B of a K row and 16 B of the Q row), fp32 FMA chain
+SX_DEV float dot_bf16x8(const uint4& x, const uint4& y, float acc) {
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
+    acc = fmaf(fa.x, fb.x, acc);
+    acc = fmaf(fa.y, fb.y, acc);
+  }
+  return acc;
+}
+
+// Per-row ancestor keys on the CUDA cores (MHA-like groups, G <= 2, when the
+// CTA's concatenated ancestor lists would add whole masked key tiles: 128 MHA
+// tokens x 2-3 ancestors = 4-6 tiles of which each row uses 2-3 keys; measured
+// 118.7 -> 51.4 us at N = 1024, 17 ancestors. For GQA (16 tokens x 8 heads per
+// CTA) the masked tiles are few and the tensor cores win: 59.9 vs 80.0 us). Called after the
+// dense tiles, with O final in TMEM: S_j = q . k_j for the row's own <= maxanc
+// slots (the two column-half threads of a row each dot 64 dims, exchanged
+// through the free K buffers), one max update, then O = O * 2^(m - m') +
+// sum_j 2^(s_j - m') v_j chunk by chunk through TMEM. Returns the row's new
+// running max; `l` (this half's share of the row sum) is rescaled and half 0
+// adds the ancestors' weights.
+SX_DEV float tc_ancestor_pass(const AttnArgs& a, TcSmemHdr& hd, uint8_t* base, const int* aslot,
+                              const __nv_bfloat16* kbase, const __nv_bfloat16* vbase, uint32_t t_o, uint32_t lane_off,
+                              int r, int half, bool o_valid, float m_used, float& l) {
+  float* dots = reinterpret_cast<float*>(base + kTcKOff);  // [2][kTcRows][maxanc] partial dots
+  const int A = hd.maxanc;
+  const int tok = r / a.G;
+  const int s0 = hd.seg[tok], na = hd.seg[tok + 1] - s0;
+  uint4 qv[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) qv[c] = *reinterpret_cast<const uint4*>(base + kTcQOff + half * 16384 + sw128(r, c));
+  for (int j = 0; j < na; ++j) {
+    const uint4* kp = reinterpret_cast<const uint4*>(kbase + (long long)aslot[s0 + j] * kHd + half * 64);
+    float d = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) d = dot_bf16x8(__ldg(kp + c), qv[c], d);
+    dots[(half * kTcRows + r) * A + j] = d;
+  }
+  __syncthreads();
+  const float scale = a.scale_log2;
+  float mx = m_used;
+  for (int j = 0; j < na; ++j) mx = fmaxf(mx, (dots[r * A + j] + dots[(kTcRows + r) * A + j]) * scale);
+  const float f0 = o_valid ? exp2f(m_used - mx) : 0.f;
+  l *= f0;
+  float psum = 0.f;
+#pragma unroll 1
+  for (int c4 = 0; c4 < 4; ++c4) {
+    float o[16];
+    if (o_valid) {
+      uint32_t u[16];
+      tmem_ld16(t_o + lane_off + half * 64 + c4 * 16, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) o[k] = __uint_as_float(u[k]) * f0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) o[k] = 0.f;
+    }
+    for (int j = 0; j < na; ++j) {
+      const float p = exp2f((dots[r * A + j] + dots[(kTcRows + r) * A + j]) * scale - mx);
+      if (c4 == 0) psum += p;
+      const uint4* vp = reinterpret_cast<const uint4*>(vbase + (long long)aslot[s0 + j] * kHd + half * 64 + c4 * 16);
+      const uint4 v0 = __ldg(vp), v1 = __ldg(vp + 1);
+      const __nv_bfloat162* w0 = reinterpret_cast<const __nv_bfloat162*>(&v0);
+      const __nv_bfloat162* w1 = reinterpret_cast<const __nv_bfloat162*>(&v1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 x0 = __bfloat1622float2(w0[k]), x1 = __bfloat1622float2(w1[k]);
+        o[2 * k] = fmaf(p, x0.x, o[2 * k]);
+        o[2 * k + 1] = fmaf(p, x0.y, o[2 * k + 1]);
+        o[8 + 2 * k] = fmaf(p, x1.x, o[8 + 2 * k]);
+        o[8 + 2 * k + 1] = fmaf(p, x1.y, o[8 + 2 * k + 1]);
+      }
+    }
+    uint32_t u[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) u[k] = __float_as_uint(o[k]);
+    tmem_st16(t_o + lane_off + half * 64 + c4 * 16, u);
+  }
+  tmem_st_wait();
+  if (half == 0) l += psum;
+  return mx;
+}
+
 __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const AttnArgs a) {
   griddep_launch_dependents();
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -514,6 +607,11 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   }
   __syncthreads();
   const int n_anc = hd.seg[a.QB];
+  if (tid == 0) {
+    int mx = 0;
+    for (int i = 0; i < a.QB; ++i) mx = max(mx, hd.seg[i + 1] - hd.seg[i]);
+    hd.maxanc = mx;
+  }
   for (int i = tid; i < a.QB * a.A; i += kTcThreads) {
     const int tl = i / a.A, j = i % a.A, t = t0 + tl;
     if (t < a.N && j < hd.seg[tl + 1] - hd.seg[tl]) aslot[hd.seg[tl] + j] = a.anc_base + a.anc[(long long)t * a.A + j];
@@ -521,7 +619,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   __syncthreads();  // aslot visible to the K/V loaders
   static_assert(sizeof(TcSmemHdr) <= kTcQOff, "attention smem header overlaps Q");
   const int maxlen = hd.maxlen;
-  const int ntiles_all = (maxlen + n_anc + kKeyTile - 1) / kKeyTile;
+  // ancestors on the CUDA cores when they would add whole masked key tiles
+  // (unsplit launches; a row's list <= 32 keys so its dots fit the K buffers)
+  const bool anc_cuda = g_attn_anc_cuda && a.G <= 2 && gridDim.z == 1 && hd.maxanc <= 32 &&
+                        (maxlen + n_anc + kKeyTile - 1) / kKeyTile > (maxlen + kKeyTile - 1) / kKeyTile;
+  const int n_anc_keys = anc_cuda ? 0 : n_anc;
+  const int ntiles_all = (maxlen + n_anc_keys + kKeyTile - 1) / kKeyTile;
   // key split (gridDim.z > 1): the first `nsplit` of the launched splits take
   // >= 4 key tiles each (fewer splits for short contexts -- a split costs a
   // CTA prologue and a partial round trip); this CTA takes tiles [kt0, kt0 + ntiles)
@@ -552,7 +655,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
       bool ok = true;
       if (key >= maxlen) {
         const int j = key - maxlen;
-        ok = j < n_anc;
+        ok = j < n_anc_keys;
         slot = ok ? aslot[j] : 0;
       }
       const long long off = (long long)slot * kHd + lc * 8;
@@ -570,7 +673,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;  // TMEM lane quadrant = warp % 4
   const int r = tid & (kTcRows - 1), half = tid >> 7;  // row, column half (keys / O dims)
   const int dl = hd.dlen[r];
-  const int slo = maxlen + hd.seg[r / a.G], shi = maxlen + hd.seg[r / a.G + 1];
+  const int slo = anc_cuda ? 0x3fffffff : maxlen + hd.seg[r / a.G];
+  const int shi = anc_cuda ? 0x3fffffff : maxlen + hd.seg[r / a.G + 1];
   constexpr uint32_t idesc_s = idesc_bf16_f32(kTcRows, kKeyTile);
   constexpr uint32_t idesc_o = idesc_bf16_f32(kTcRows, kHd) | (1u << 16);  // B (V) MN-major
   float m_used = -1e30f, l = 0.f;
@@ -667,14 +771,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
   // epilogue: O / l -> bf16; each thread stores its half (64 dims) of row r.
   // Key split: the unnormalised O half, plus (m, l) of the row, go to the
   // workspace instead and attn_combine_kernel merges the splits.
-  hd.red[half][r] = l;
-  __syncthreads();
-  const float lt = hd.red[0][r] + hd.red[1][r];
-  const int t = t0 + r / a.G;
   if (ntiles > 0) {
     mbar_wait(&hd.bar_o, (ntiles - 1) & 1);
     tc_fence_after();
   }
+  bool o_valid = ntiles > 0;
+  if (anc_cuda) {
+    m_used = tc_ancestor_pass(a, hd, base, aslot, kbase, vbase, t_o, lane_off, r, half, o_valid, m_used, l);
+    o_valid = true;
+  }
+  hd.red[half][r] = l;
+  __syncthreads();
+  const float lt = hd.red[0][r] + hd.red[1][r];
+  const int t = t0 + r / a.G;
   float* prow_ws = nullptr;
   if (nsplit > 1) {
     prow_ws = a.part + ((((long long)blockIdx.x * gridDim.y + kvh) * zsplit + split) * kTcRows + r) * kPartStride;
@@ -688,7 +797,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     uint32_t u[16];
-    if (ntiles > 0) {
+    if (o_valid) {
       tmem_ld16(t_o + lane_off + half * 64 + c * 16, u);
       tmem_ld_wait();
     }
@@ -696,7 +805,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
       float4* d4 = reinterpret_cast<float4*>(prow_ws + half * 64 + c * 16);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        d4[j] = ntiles > 0 ? make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]),
+        d4[j] = o_valid ? make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]),
                                          __uint_as_float(u[4 * j + 2]), __uint_as_float(u[4 * j + 3]))
                            : make_float4(0.f, 0.f, 0.f, 0.f);
       continue;
@@ -704,7 +813,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tree_attention_tc_kernel(const 
     uint32_t w[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      w[j] = ntiles > 0 ? pack_bf16(__uint_as_float(u[2 * j]) * inv, __uint_as_float(u[2 * j + 1]) * inv) : 0u;
+      w[j] = o_valid ? pack_bf16(__uint_as_float(u[2 * j]) * inv, __uint_as_float(u[2 * j + 1]) * inv) : 0u;
     if (t < a.N) {
       uint4* d4 = reinterpret_cast<uint4*>(dst + c * 16);
       d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -804,6 +913,12 @@ extern "C" int sx_tree_attention_ws(const void* q, const void* kcache, const voi
       a.counters = reinterpret_cast<int*>(ws);
       a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kAttnCounterBytes);
     }
+    static const int anc_cuda_init = [] {
+      const int v = getenv("SX_ATTN_ANC_CUDA") ? atoi(getenv("SX_ATTN_ANC_CUDA")) : 1;
+      if (v != 1) cudaMemcpyToSymbol(g_attn_anc_cuda, &v, sizeof(int));
+      return v;
+    }();
+    (void)anc_cuda_init;
     const size_t smem = 1024 + kTcAncOff + (size_t)((anc_bytes + 15) & ~15LL);
     if (int st = ensure_smem_attr((const void*)tree_attention_tc_kernel, (int)smem)) return st;
     dim3 grid((N + a.QB - 1) / a.QB, KVH, a.splits);

@@ -79,7 +79,10 @@ def make(N, H, KVH, slots, seed, kscale=1.0):
 
 @pytest.mark.parametrize("impl", [0, 1, 2])
 @pytest.mark.parametrize("H,KVH,N,ctx,D", [(64, 8, 1025, 130, 16), (32, 8, 300, 70, 16), (32, 32, 257, 200, 16),
-                                           (64, 8, 37, 0, 5)])
+                                           (64, 8, 37, 0, 5),
+                                           # grids >= 148 CTAs with G <= 2 (MHA-like drafts): the
+                                           # ancestors take the CUDA-core pass of the tcgen05 kernel
+                                           (32, 32, 1024, 100, 16), (32, 16, 600, 64, 12), (16, 16, 1500, 0, 20)])
 def test_tree_pass(cuda, impl, H, KVH, N, ctx, D):
     rng = np.random.default_rng(N + ctx)
     paths = random_tree(rng, N, D)

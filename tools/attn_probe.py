@@ -46,7 +46,7 @@ def run(N, ctx, A, H=64, KVH=8, reps=20):
 CASES = [(64, 8, 1025, 130, 2), (64, 8, 1025, 130, 17), (64, 8, 1025, 512, 0), (64, 8, 1025, 1024, 0),
          (64, 8, 2049, 130, 17), (64, 8, 4097, 200, 17), (32, 32, 1024, 160, 17), (32, 32, 256, 160, 17),
          (32, 8, 1024, 160, 17), (64, 8, 1, 300, 0), (32, 32, 1, 300, 0), (64, 8, 1, 2000, 0),
-         (32, 32, 512, 160, 17), (32, 32, 128, 160, 17)]
+         (32, 32, 512, 160, 17), (32, 32, 128, 160, 17), (32, 32, 1023, 160, 2), (32, 32, 1023, 160, 3)]
 
 
 def main():

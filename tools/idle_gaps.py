@@ -51,10 +51,19 @@ def main():
             kern.append((ev.time_range.start, ev.time_range.end, ev.name.split("(")[0][-40:]))
         elif ev.name.startswith("sx::"):
             ranges.append((ev.time_range.start, ev.time_range.end, ev.name))
-    kern.sort()
-    busy = sum(e - s for s, e, _ in kern)
+    kern = sorted(set(kern))  # the profiler can report a record twice
+    union, cur_s, cur_e = 0.0, None, None  # busy = union of the device intervals (PDL overlaps grids)
+    for s, e, _ in kern:
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                union += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    union += cur_e - cur_s
     span = kern[-1][1] - kern[0][0]
-    print(f"device span {span / 1e3 / a.steps:.2f} ms/step, kernel busy {busy / 1e3 / a.steps:.2f} ms/step")
+    print(f"device span {span / 1e3 / a.steps:.2f} ms/step, device busy (union) {union / 1e3 / a.steps:.2f} ms/step, "
+          f"idle {(span - union) / 1e3 / a.steps:.2f} ms/step")
     gaps = collections.defaultdict(lambda: [0, 0.0])
     big = []
     for (s0, e0, n0), (s1, e1, n1) in zip(kern, kern[1:]):
