@@ -66,8 +66,11 @@ def main():
           f"idle {(span - union) / 1e3 / a.steps:.2f} ms/step")
     gaps = collections.defaultdict(lambda: [0, 0.0])
     big = []
-    for (s0, e0, n0), (s1, e1, n1) in zip(kern, kern[1:]):
-        g = s1 - e0
+    run_end, run_name = kern[0][1], kern[0][2]
+    for s1, e1, n1 in kern[1:]:
+        g, n0 = s1 - run_end, run_name  # gap after everything that started earlier has ended
+        if e1 >= run_end:
+            run_end, run_name = e1, n1
         if g < a.min_us:
             continue
         key = f"{n0} -> {n1}"
