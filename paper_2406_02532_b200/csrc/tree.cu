@@ -16,10 +16,18 @@
 // reference's total order.
 //
 // Per round (one draft call):
-//   sx_tree_score  : canonical float64 probabilities of every batch row (from
+//   scoring        : canonical float64 probabilities of every batch row (from
 //                    fp32 logits, fp64 probabilities, or a warped row), edge =
 //                    sx_log(p), nll = parent_nll - edge, keep key < threshold.
-//   sx_tree_update : a cluster of kUpdCluster CTAs. Radix select (8-bit digits
+//                    fp32 logits (the Llama drafts) take the chunked persistent
+//                    path: a max pass (one HBM read, exact row max + an fp32
+//                    estimate that prefilters whole rows against the threshold)
+//                    and one fused exact pass (canonical sums, then the edges of
+//                    the candidates the estimate cannot rule out).
+//   sx_tree_update : a cluster of kUpdCluster CTAs. When the survivors fit the
+//                    sort buffer, CTA 0 sorts just them and merges them with the
+//                    (already sorted) materialized list, and merges the lex
+//                    order the same way. Otherwise (root round, floods): radix select (8-bit digits
 //                    over the 128-bit key) of the K best of materialized U
 //                    survivors: every CTA histograms its slice of the keys, the
 //                    histograms are summed over distributed shared memory and
