@@ -695,10 +695,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // 0 = auto (pair when the tree pass has >= 256 tokens), 1 = single-CTA only, 2 = pair whenever legal.
 static int g_pair_mode = 0;
-// programmatic dependent launch of the GEMM (opt-in, SX_GEMM_PDL=1): measured no
-// end-to-end change on C2 (156.4 vs 156.2 ms), and the early-resident CTAs waiting
-// in griddepcontrol.wait blur per-kernel timings -- off by default
-static const int g_pdl = getenv("SX_GEMM_PDL") ? atoi(getenv("SX_GEMM_PDL")) : 0;
+// programmatic dependent launch of the GEMM (SX_GEMM_PDL=0 disables): the weight
+// ring prefetch and the CTA prologue overlap the previous kernel's tail. Round 1
+// measured no change (156.4 vs 156.2 ms); round 2, six alternating C2 runs each
+// (profiles/r2/gemm_pdl_ab.txt): 147.2 vs 148.0 ms, 1229 vs 1224 TFLOP/s
+static const int g_pdl = getenv("SX_GEMM_PDL") ? atoi(getenv("SX_GEMM_PDL")) : 1;
 
 // tuning overrides (read once): SX_GEMM_BN_CAP (token-tile cap), SX_GEMM_STAGES (max pipeline depth),
 // SX_GEMM_KPB (64-wide k-blocks per stage; 0 = auto)
