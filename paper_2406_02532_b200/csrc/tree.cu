@@ -1821,8 +1821,22 @@ extern "C" int sx_tree_round_rows(void* ws, int K, int B, int V, int D, const vo
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, tree_rows_exact_kernel, kRowThreads, 0);
         if (occx < 1) occx = 1;
       }
-      // grid <= resident capacity: the score units spin on flags set by sum units of other CTAs
-      launch_pdl(tree_rows_exact_kernel, dim3(grid_of(ub, occx)), dim3(kRowThreads), 0, stream, w, L, z, ld);
+      // The score units spin on flags set by sum units of other CTAs, so every CTA
+      // must be resident at once: grid <= the resident capacity, and a cooperative
+      // launch makes the co-residency a guarantee even when other work (another
+      // engine's stream) shares the GPU.
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid_of(ub, occx));
+      cfg.blockDim = dim3(kRowThreads);
+      cfg.stream = stream;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = g_tree_pdl;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      cudaLaunchKernelEx(&cfg, tree_rows_exact_kernel, w, L, z, ld);
       SX_CHECK_LAUNCH("tree_rows_exact_kernel");
     } else {
       launch_pdl(tree_rows_sum_kernel, dim3(grid_of(ub, occ[1])), dim3(kRowThreads), 0, stream, w, L, z, ld);
