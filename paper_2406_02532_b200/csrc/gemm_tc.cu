@@ -931,15 +931,20 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& ma2, const CUte
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = cl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol.wait in the kernel)
   at[1].val.programmaticStreamSerializationAllowed = g_pdl;
+  // split tiles: owners wait on their helpers' flags, so the grid (<= one CTA or
+  // pair per SM) must be co-resident -- a cooperative launch guarantees it even
+  // when another engine's kernels share the GPU
+  at[2].id = cudaLaunchAttributeCooperative;
+  at[2].val.cooperative = g.flags != nullptr ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 3;
   cudaLaunchKernelEx(&cfg, kern, ma, ma2, mb, g);
   SX_CHECK_LAUNCH("gemm_tc_kernel");
   return SX_OK;
