@@ -82,6 +82,9 @@ def parse():
     ap.add_argument("--parallel", choices=["tp", "replicas"], default="tp",
                     help="N>1: tensor-parallel target (one stream) or N independent replicas")
     ap.add_argument("--reduce", choices=["bf16", "fp32"], default="bf16", help="TP all-reduce precision")
+    ap.add_argument("--tp-rows", choices=["argmax", "gather"], default="argmax",
+                    help="TP target at t=0: return per-row argmax keys (KV1: int64 MAX all-reduce of N x 8 B) "
+                         "instead of all-gathering the [N, V/n] logit slices")
     ap.add_argument("--tp-comm", choices=["fused", "nccl"], default="nccl",
                     help="TP reduction: NCCL all-reduce (default, north_star), or the opt-in GEMM epilogue "
                          "reduce-scatter over peer memory (not yet run on multi-GPU hardware)")
@@ -630,7 +633,8 @@ def main():
     offload = args.workload in OFFLOAD
     target = LlamaModel(tname, seed=1, max_ctx=ctx_cap + K + 2, max_tokens=max(K + 1, args.prompt_len), synthetic=syn,
                         offload=offload, offload_buffers=args.offload_buffers, tp=comm, reduce_bf16=args.reduce == "bf16",
-                        tp_fused=True if args.tp_comm == "fused" else False)
+                        tp_fused=True if args.tp_comm == "fused" else False,
+                        tp_argmax=temp == 0.0 and args.tp_rows == "argmax")
     draft = LlamaModel(dname, seed=2, max_ctx=ctx_cap + 4 * K + 2 * B * (D + 1) + 64, max_tokens=max(B, args.prompt_len),
                        synthetic=syn)
     torch.cuda.synchronize()
@@ -806,7 +810,8 @@ def main():
             "data": "synthetic: random-init weights (N(0,0.02)), random 128-token prompt" +
                     (f", shared synthetic prev-token bias scale {args.synthetic}" if syn else ""),
             "config": bench_config(args, K, B, scoring),
-            "parallelism": (f"tp{world} target ({'fused GEMM reduce-scatter over peer memory' if target.tp_fused else 'NCCL all-reduce'}, {args.reduce}), draft replicated"
+            "parallelism": (f"tp{world} target ({'fused GEMM reduce-scatter over peer memory' if target.tp_fused else 'NCCL all-reduce'}, {args.reduce}"
+                            f"{', KV1 argmax keys' if target.tp_argmax else ''}), draft replicated"
                             if tp else f"replicas x{world}") if world > 1 else "1 GPU",
             "accepted_tokens_per_iter": accepted_per_iter,
             "draft_calls_per_iter": draft_calls / max(1, iters),

@@ -111,7 +111,9 @@ SX_API int sx_tp_reduce_bcast(const void* inbox, int rank, int world, int M, int
  * block (batch size == 0 ends the build). sx_tree_finalize lays the result out
  * in node-id order (ids in key order, tree.py:320-327).
  */
-enum { SX_ROWS_LOGITS_F32 = 0, SX_ROWS_PROBS_F64 = 1 };
+/* SX_ROWS_ARGMAX_PACKED: one int64 key per row (sx_rows_argmax_packed, max-reduced
+ * over vocab shards): the row's argmax for t = 0 walks (KV1) */
+enum { SX_ROWS_LOGITS_F32 = 0, SX_ROWS_PROBS_F64 = 1, SX_ROWS_ARGMAX_PACKED = 2 };
 enum { SX_SCORE_RAW = 0, SX_SCORE_ARGMAX = 1, SX_SCORE_WARP = 2 };
 SX_API long long sx_tree_workspace_bytes(int K, int B, int V, int D);
 /* byte offsets into the workspace, in this order: ctl, b_node, b_nll, b_depth, b_lex,
@@ -180,6 +182,12 @@ SX_API int sx_warp_rows(const void* rows, int row_kind, long long ld, int V, con
 SX_API int sx_softmax_rows(const float* rows, long long ld, int V, const int* row_ids, int n, double* out,
                            long long ldo, cudaStream_t stream);
 SX_API int sx_argmax_rows(const void* rows, int row_kind, long long ld, int V, int n, int* out, cudaStream_t stream);
+/* KV1 (vocab-parallel LM head, t = 0): out[r] = max over v in the slice of
+ * orderable(logits[r][v]) << 31 | (0x7fffffff - (v0 + v)); an int64 MAX all-reduce
+ * of these keys over the shards gives the global argmax (lowest id on ties).
+ * Replaces the all-gather of the logit slices (engine.py:124 at t = 0). */
+SX_API int sx_rows_argmax_packed(const float* logits, long long ld, int n, int Vl, int v0, long long* out,
+                                 cudaStream_t stream);
 /* sample (sampling.py:101-113) from n warped fp64 rows with uniforms u[n] */
 SX_API int sx_sample_rows(const double* w, long long ld, int V, const double* u, int n, int* out,
                           cudaStream_t stream);

@@ -68,6 +68,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "sx_softmax_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _c_ll, _vp]),
     "sx_argmax_rows": (_c_int, [_vp, _c_int, _c_ll, _c_int, _c_int, _vp, _vp]),
+    "sx_rows_argmax_packed": (_c_int, [_vp, _c_ll, _c_int, _c_int, _c_int, _vp, _vp]),
     "sx_sample_rows": (_c_int, [_vp, _c_ll, _c_int, _vp, _c_int, _vp, _vp]),
     "sx_beam_scratch_bytes": (_c_ll, [_c_int, _c_int]),
     "sx_beam_step": (
@@ -121,7 +122,7 @@ SIGNATURES: dict[str, tuple] = {
     "sx_kv_compact_f32": (_c_int, [_vp, _vp, _c_int, _c_ll, _c_ll, _c_int, _vp, _vp, _c_int, _vp]),
 }
 
-ROWS_LOGITS_F32, ROWS_PROBS_F64 = 0, 1
+ROWS_LOGITS_F32, ROWS_PROBS_F64, ROWS_ARGMAX_PACKED = 0, 1, 2
 SCORE_RAW, SCORE_ARGMAX, SCORE_WARP = 0, 1, 2
 
 EPI_BF16, EPI_F32, EPI_ADD_F32, EPI_SWIGLU_BF16, EPI_SWIGLU_IL, EPI_RS_BF16, EPI_QKV_ROPE = 0, 1, 2, 3, 4, 5, 6

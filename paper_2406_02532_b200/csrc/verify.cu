@@ -41,7 +41,9 @@ __global__ void __launch_bounds__(kRowThreads) verify_walk_kernel(const void* ro
     const float* z = row_kind == SX_ROWS_LOGITS_F32 ? reinterpret_cast<const float*>(rows) + r * ld : nullptr;
     const double* p = row_kind == SX_ROWS_PROBS_F64 ? reinterpret_cast<const double*>(rows) + r * ld : nullptr;
     int tok;
-    if (temperature == 0.0) {
+    if (row_kind == SX_ROWS_ARGMAX_PACKED) {  // KV1 keys (t = 0 only): the row's argmax is in the key
+      tok = 0x7fffffff - (int)(reinterpret_cast<const long long*>(rows)[r * ld] & 0x7fffffff);
+    } else if (temperature == 0.0) {
       double bv = -CUDART_INF;
       int bi = 0x7fffffff;
       for (int v = threadIdx.x; v < V; v += kRowThreads) {
@@ -132,6 +134,40 @@ __global__ void __launch_bounds__(kRowThreads) argmax_rows_kernel(const void* ro
   if (threadIdx.x == 0) out[r] = best;
 }
 
+// KV1 for the vocab-parallel LM head at t = 0: per row the packed key of its
+// best logit, orderable(logit) << 31 | (0x7fffffff - global id). One int64 MAX
+// all-reduce over the vocab shards then gives every rank the global argmax with
+// the lowest id among equal logits (np.argmax) -- N x 8 bytes instead of the
+// all-gather of the [N, V / n] logit slices. Exact for the walk: fp32 logits that
+// differ stay distinct through the canonical exp(z - M) / S in float64, so the
+// logit argmax is the probability argmax.
+SX_DEV unsigned long long pack_argmax(float v, int id) {
+  unsigned u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // monotone in v
+  return ((unsigned long long)u << 31) | (unsigned long long)(0x7fffffff - id);
+}
+
+__global__ void __launch_bounds__(kRowThreads) argmax_packed_kernel(const float* __restrict__ z, long long ld, int Vl,
+                                                                     int v0, long long* out) {
+  __shared__ unsigned long long red[kRowThreads / 32];
+  const long long r = blockIdx.x;
+  unsigned long long best = 0;
+  for (int v = threadIdx.x; v < Vl; v += kRowThreads) {
+    const unsigned long long k = pack_argmax(z[r * ld + v], v0 + v);
+    best = k > best ? k : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long k = __shfl_xor_sync(0xffffffffu, best, o);
+    best = k > best ? k : best;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kRowThreads / 32; ++w) best = red[w] > best ? red[w] : best;
+    out[r] = (long long)best;
+  }
+}
+
 __global__ void sample_rows_kernel(const double* w, long long ld, int V, const double* u, int* out) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
@@ -156,8 +192,11 @@ extern "C" int sx_verify_walk(const void* rows, int row_kind, long long ld, int 
                               int n_nodes, int start_cursor, const double* uniforms, int max_steps, double temperature,
                               double top_p, int* out, void* scratch, cudaStream_t stream) {
   if (V < 1 || max_steps < 1) return arg_error("verify_walk: V and max_steps must be >= 1");
-  if (row_kind != SX_ROWS_LOGITS_F32 && row_kind != SX_ROWS_PROBS_F64) return arg_error("verify_walk: bad row kind");
+  if (row_kind != SX_ROWS_LOGITS_F32 && row_kind != SX_ROWS_PROBS_F64 && row_kind != SX_ROWS_ARGMAX_PACKED)
+    return arg_error("verify_walk: bad row kind");
   if (temperature < 0 || !(top_p > 0 && top_p <= 1)) return arg_error("verify_walk: bad warp");
+  if (row_kind == SX_ROWS_ARGMAX_PACKED && temperature != 0.0)
+    return arg_error("verify_walk: argmax-only rows (KV1 keys) serve t = 0 walks only");
   if (int st = set_rowsmem_attr((const void*)verify_walk_kernel)) return st;
   auto al = [](long long x) { return (x + 255) & ~255LL; };
   uint8_t* s = reinterpret_cast<uint8_t*>(scratch);
@@ -213,6 +252,16 @@ extern "C" int sx_argmax_rows(const void* rows, int row_kind, long long ld, int 
   if (n <= 0) return SX_OK;
   argmax_rows_kernel<<<n, kRowThreads, 0, stream>>>(rows, row_kind, ld, V, out);
   SX_CHECK_LAUNCH("argmax_rows_kernel");
+  return SX_OK;
+}
+
+extern "C" int sx_rows_argmax_packed(const float* logits, long long ld, int n, int Vl, int v0, long long* out,
+                                     cudaStream_t stream) {
+  if (n <= 0) return SX_OK;
+  if (Vl < 1 || v0 < 0 || ld < Vl || (long long)v0 + Vl > 0x7fffffffLL)
+    return arg_error("rows_argmax_packed: bad slice (Vl=%d v0=%d ld=%lld)", Vl, v0, ld);
+  argmax_packed_kernel<<<n, kRowThreads, 0, stream>>>(logits, ld, Vl, v0, out);
+  SX_CHECK_LAUNCH("argmax_packed_kernel");
   return SX_OK;
 }
 

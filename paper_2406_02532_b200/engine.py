@@ -80,6 +80,9 @@ class DeviceRows:
         if isinstance(i, tuple) or not isinstance(i, (int, np.integer)):
             return np.stack([self[j] for j in range(len(self))])[i]
         i = int(i)
+        if self.rows.dtype == torch.int64:
+            raise RuntimeError("argmax-only target rows (LlamaModel(tp_argmax=True), KV1): the full distribution "
+                               "is not kept -- build the target without tp_argmax to read rows")
         if self.rows.dtype == torch.float32:
             r = K.softmax_rows(self.rows[i : i + 1])[0]
         else:

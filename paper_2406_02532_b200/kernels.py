@@ -169,7 +169,7 @@ def gemm(
 # canonical row kernels (sampling.py / engine.py semantics)
 # ---------------------------------------------------------------------------
 
-from ._lib import ROWS_LOGITS_F32, ROWS_PROBS_F64, SCORE_ARGMAX, SCORE_RAW, SCORE_WARP  # noqa: E402
+from ._lib import ROWS_ARGMAX_PACKED, ROWS_LOGITS_F32, ROWS_PROBS_F64, SCORE_ARGMAX, SCORE_RAW, SCORE_WARP  # noqa: E402
 
 _scratch_cache: dict[tuple[int, str, int], torch.Tensor] = {}
 
@@ -234,7 +234,9 @@ def row_kind(rows: torch.Tensor) -> int:
         return ROWS_LOGITS_F32
     if rows.dtype == torch.float64:
         return ROWS_PROBS_F64
-    raise ValueError(f"rows must be fp32 logits or fp64 probabilities, got {rows.dtype}")
+    if rows.dtype == torch.int64:
+        return ROWS_ARGMAX_PACKED
+    raise ValueError(f"rows must be fp32 logits, fp64 probabilities or int64 argmax keys, got {rows.dtype}")
 
 
 def warp_rows(rows: torch.Tensor, temperature: float, top_p: float, row_ids: torch.Tensor | None = None) -> torch.Tensor:
@@ -271,6 +273,15 @@ def softmax_rows(logits: torch.Tensor, row_ids: torch.Tensor | None = None) -> t
     return out
 
 
+def rows_argmax_packed(logits: torch.Tensor, v0: int, out: torch.Tensor) -> torch.Tensor:
+    """KV1: int64 key per row of a vocab slice (columns v0 .. v0 + Vl) whose MAX
+    over the slices is the global argmax (lowest id on ties); out [n, 1] int64."""
+    _require_cuda(logits)
+    n, Vl = logits.shape
+    call("sx_rows_argmax_packed", ptr(logits), logits.stride(0), n, Vl, v0, ptr(out), stream_ptr())
+    return out
+
+
 def argmax_rows(rows: torch.Tensor) -> torch.Tensor:
     _require_cuda(rows)
     n, V = rows.shape
@@ -294,7 +305,7 @@ def verify_walk(rows: torch.Tensor, parent: torch.Tensor, token: torch.Tensor, n
                 out_host: torch.Tensor | None = None) -> WalkResult:
     """Acceptance walk over cached target rows (engine.py:118-128) on one CTA."""
     dev = rows.device
-    V = rows.shape[1]
+    V = rows.shape[1]  # 1 for int64 argmax keys (KV1): the walk reads only the key
     lib = _lib.load()
     sc = scratch(lib.sx_row_scratch_bytes(V), dev, "walk")
     u = torch.as_tensor(np.ascontiguousarray(uniforms[:max_steps], dtype=np.float64))

@@ -305,6 +305,7 @@ class _Buffers:
         if sh.world > 1:  # vocab-parallel LM head: local slice + all-gather staging
             self.logits_l = torch.empty((n, cfg.vocab // sh.world), dtype=torch.float32, device=device)
             self.logits_g = torch.empty((sh.world, n, cfg.vocab // sh.world), dtype=torch.float32, device=device)
+            self.argmax_keys = torch.empty((n, 1), dtype=torch.int64, device=device)  # KV1 (tp_argmax)
         self.tok = torch.empty(n, dtype=torch.int32, device=device)
         self.pos = torch.empty(n, dtype=torch.int32, device=device)
 
@@ -329,6 +330,7 @@ class LlamaModel(LanguageModel):
         tp=None,
         reduce_bf16: bool = True,
         tp_fused: bool | None = None,
+        tp_argmax: bool = False,
         offload_buffers: int = 8,
         init: str = "device",
         dtype: str = "bf16",
@@ -344,7 +346,12 @@ class LlamaModel(LanguageModel):
         writes each feature slice of its bf16 partial into the owner rank's inbox
         over peer memory (sx_gemm_bf16_rs) and the owner reduces and broadcasts
         the slice (sx_tp_reduce_bcast). None = fused when the communicator
-        provides peer memory, else the NCCL all-reduce."""
+        provides peer memory, else the NCCL all-reduce.
+        tp_argmax (KV1, t = 0 SpecExec only): the tree pass returns one int64
+        argmax key per row (sx_rows_argmax_packed on this rank's vocab slice, an
+        int64 MAX all-reduce over the ranks) instead of all-gathering the logit
+        slices into [N, V]; the acceptance walk needs nothing else at t = 0, and
+        a t > 0 walk or a full-row request raises."""
         if isinstance(cfg, str):
             cfg = PRESETS[cfg]
         if cfg.head_dim != 128:
@@ -363,6 +370,7 @@ class LlamaModel(LanguageModel):
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.seed = seed
         self.tp = tp if (tp is not None and tp.world > 1) else None
+        self.tp_argmax = bool(tp_argmax and self.tp is not None)
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else None
         if self.shard is not None:
             self.shard.check(cfg)
@@ -447,7 +455,8 @@ class LlamaModel(LanguageModel):
     # ------------------------------------------------------------------ forward
     def forward(self, n: int, tokens: torch.Tensor, pos: torch.Tensor | None, pos_base: int, slot: torch.Tensor | None,
                 slot_base: int, dense_len: torch.Tensor | None, dense_const: int, anc: torch.Tensor | None,
-                anc_base: int, anc_len: torch.Tensor | None, A: int, logits_from: int | None) -> torch.Tensor | None:
+                anc_base: int, anc_len: torch.Tensor | None, A: int, logits_from: int | None,
+                argmax_only: bool = False) -> torch.Tensor | None:
         """Run n tokens through the network; write their K/V into the cache.
 
         Token t sits at position pos_base + pos[t] (pos None: t) and KV slot
@@ -509,6 +518,18 @@ class LlamaModel(LanguageModel):
         hh = b.h[logits_from:n]
         _lib.call("sx_add_rmsnorm", p(x[logits_from:]), p(y[logits_from:]), ybf, p(w.nf), m, cfg.d, cfg.eps, p(hh), st)
         logits = b.logits[:m]
+        if tp is not None and argmax_only:  # KV1: packed argmax keys of this slice, MAX-reduced over the ranks
+            ll = b.logits_l[:m]
+            K.gemm(hh, w.lm, out=ll, epi=K.EPI_F32)
+            v0, v1 = self.shard.vocab(cfg)
+            if self.synthetic is not None:
+                bi = self.bias_in[:m]
+                torch.index_select(self.bias_u, 0, tokens[logits_from:n].long(), out=bi)
+                K.gemm(bi, self.bias_w[v0:v1], out=ll, epi=K.EPI_ADD_F32)
+            keys = b.argmax_keys[:m]
+            K.rows_argmax_packed(ll, v0, keys)
+            tp.max_reduce_(keys)
+            return keys
         if tp is None:
             K.gemm(hh, w.lm, out=logits, epi=K.EPI_F32)
         else:  # vocab-parallel LM head: local slice, all-gather, interleave the slices into [m, V]
@@ -683,7 +704,9 @@ class LlamaModel(LanguageModel):
             anc, anc_len, depth, tok = (torch.from_numpy(a).to(self.device, non_blocking=True) for a in tabs)
             A = tabs[0].shape[1]
             K.IO["h2d"] += sum(a.nbytes for a in tabs)
-        logits = self.forward(n, tok, depth, c, None, c, None, c, anc, c, anc_len, A, 0)
+        if self.tp_argmax and self.record is not None:
+            raise RuntimeError("tp_argmax keeps no logit rows; the replay record needs them")
+        logits = self.forward(n, tok, depth, c, None, c, None, c, anc, c, anc_len, A, 0, argmax_only=self.tp_argmax)
         self.committed.append(prefix[-1])  # the root's KV is at slot c = its position
         tree.target_base = c
         if self.record is not None:

@@ -139,6 +139,15 @@ class NcclComm:
             return
         self.dist.all_reduce(t, group=self.group)
 
+    def max_reduce_(self, t: torch.Tensor) -> None:
+        """Element-wise MAX all-reduce (int64 KV1 argmax keys)."""
+        if self.host_staging:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX, group=self.group)
+            t.copy_(h)
+            return
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
     def all_gather_(self, local: torch.Tensor, out: torch.Tensor) -> None:
         """local [world-slices of out]: out [world, *local.shape] contiguous."""
         # concatenated layout [world * rows, ...] (accepted by every backend)
@@ -208,6 +217,16 @@ class ThreadComm:
             acc = slots[0].float().clone()
             for s in slots[1:]:
                 acc += s.float()
+            for s in slots:
+                s.copy_(acc)
+
+        self._exchange(t, red)
+
+    def max_reduce_(self, t: torch.Tensor) -> None:
+        def red(slots):
+            acc = slots[0].clone()
+            for s in slots[1:]:
+                acc = torch.maximum(acc, s)
             for s in slots:
                 s.copy_(acc)
 

@@ -101,3 +101,62 @@ def test_tp_target_generation_ranks_agree_replay_parity(cuda, monkeypatch, fused
     exp, ost = ox.generate_specexec(prompt, lm(drec), lm(trec), ox.BuilderParams(64, 8, 16),
                                     ox.SamplingConfig(0.0, 1.0, seed=3, max_new_tokens=40), warp_scores=False)
     assert toks == exp and st.accepted_per_iteration == ost.accepted_per_iteration
+
+
+def test_tp_argmax_keys_walk_equals_gathered_rows(cuda):
+    """KV1: with tp_argmax the TP target returns one int64 argmax key per tree
+    row (a MAX all-reduce over the vocab slices) instead of all-gathered logits;
+    the t = 0 SpecExec run is token-for-token the gathered-rows run on every rank,
+    a t > 0 walk is refused, and a full-row read raises."""
+    world = 2
+    syn = SyntheticBias(seed=7, rank=64, scale=4.0)
+    prompt = tuple(int(x) for x in np.random.default_rng(11).integers(0, 32000, size=24))
+    params = sx.BuilderParams(64, 8, 16)
+    cfg = sx.SamplingConfig(0.0, 1.0, seed=3, max_new_tokens=40)
+    res = {}
+    for argmax in (False, True):
+        comms = ThreadComm.group(world)
+
+        def rank(r):
+            target = LlamaModel(CFG, seed=3, max_ctx=2048, max_tokens=512, synthetic=syn, tp=comms[r],
+                                tp_fused=False, tp_argmax=argmax)
+            draft = LlamaModel("tiny-draft", seed=2, max_ctx=4096, max_tokens=512, synthetic=syn)
+            draft.use_graphs = False
+            toks, st = sx.generate_specexec(prompt, draft, target, params, cfg, warp_scores=False)
+            extra = None
+            if argmax:
+                cache = sx.precompute(prompt + tuple(toks), draft, target, params, cfg, warp_scores=False)
+                assert cache.dists.rows.dtype == torch.int64
+                with pytest.raises(RuntimeError):
+                    cache.current_dist()
+                with pytest.raises(ValueError):
+                    cache.walk(np.zeros(4), sx.SamplingConfig(0.6, 0.9, seed=0), 4)
+                extra = True
+            return toks, st.accepted_per_iteration, extra
+
+        res[argmax] = run_ranks(world, rank)
+    for r in range(world):
+        assert res[True][r][0] == res[False][r][0] == res[False][0][0]
+        assert res[True][r][1] == res[False][r][1]
+
+
+def test_rows_argmax_packed_kernel(cuda):
+    """sx_rows_argmax_packed on vocab slices, max-combined: the global argmax with
+    the lowest id on exact ties (np.argmax), for negative / positive logits."""
+    from paper_2406_02532_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n, V, W = 37, 1000, 4
+    z = torch.randn(n, V, device="cuda", generator=g) * 3
+    z[3, 10] = z[3, 700] = z[3].max() + 1.0  # exact tie across slices -> lowest id
+    z[4, :] = -2.5  # all equal -> id 0
+    z[5, 999] = 1e30
+    keys = torch.zeros(W, n, 1, dtype=torch.int64, device="cuda")
+    Vl = V // W
+    for w in range(W):
+        K.rows_argmax_packed(z[:, w * Vl:(w + 1) * Vl], w * Vl, keys[w])
+    best = keys.max(0).values[:, 0]
+    got = (0x7FFFFFFF - (best & 0x7FFFFFFF)).cpu().numpy()
+    exp = np.argmax(z.cpu().numpy(), axis=1)
+    assert (got == exp).all()
+    assert got[3] == 10 and got[4] == 0 and got[5] == 999

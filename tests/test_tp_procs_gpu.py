@@ -50,6 +50,11 @@ def _worker(rank, world, port, out):
     res["spec"], st = sx.generate_specexec(prompt, draft, target, sx.BuilderParams(64, 8, 16), cfg_s, warp_scores=False)
     res["seq"], _ = sx.generate_sequential(prompt, target, cfg_s)
     res["accepted"] = st.accepted_per_iteration
+    # KV1: argmax keys MAX-reduced over the ranks (host-staged under gloo) instead of gathered rows
+    target_k = LlamaModel(cfg, seed=3, max_ctx=2048, max_tokens=256, tp=comm, tp_fused=False, tp_argmax=True)
+    draft_k = LlamaModel("tiny-draft", seed=4, max_ctx=4096, max_tokens=256)
+    res["spec_kv1"], _ = sx.generate_specexec(prompt, draft_k, target_k, sx.BuilderParams(64, 8, 16), cfg_s,
+                                              warp_scores=False)
     out[rank] = res
     dist.barrier()
     dist.destroy_process_group()
@@ -62,5 +67,5 @@ def test_two_process_tp_target(cuda):
     r0, r1 = out[0], out[1]
     assert r0["err_vs_unsharded"] < 2e-2, r0["err_vs_unsharded"]
     assert torch.equal(r0["rows"], r1["rows"])  # every rank holds the same all-reduced rows
-    assert r0["spec"] == r1["spec"] == r0["seq"] == r1["seq"]
+    assert r0["spec"] == r1["spec"] == r0["seq"] == r1["seq"] == r0["spec_kv1"] == r1["spec_kv1"]
     assert r0["accepted"] == r1["accepted"]
