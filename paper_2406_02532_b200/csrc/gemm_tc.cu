@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // 0 = auto (pair when the tree pass has >= 256 tokens), 1 = single-CTA only, 2 = pair whenever legal.
-static int g_pair_mode = 0;
+static int g_pair_mode = getenv("SX_GEMM_PAIR_MODE") ? atoi(getenv("SX_GEMM_PAIR_MODE")) : 0;  // A/B knob
 // programmatic dependent launch of the GEMM (SX_GEMM_PDL=0 disables): the weight
 // ring prefetch and the CTA prologue overlap the previous kernel's tail. Round 1
 // measured no change (156.4 vs 156.2 ms); round 2, six alternating C2 runs each
@@ -753,6 +753,12 @@ static int pair_cap(int M, int Nf, int dual, int cg_req) {
   if (M < 128) return 0;
   auto tiles = [&](int bn) { return (long long)((Nf + 255) / 256) * ((M + bn - 1) / bn); };
   if (M >= 256 && tiles(pick_bn(M, cap)) * 2 >= 3 * (kNumSMs / 2)) return cap;
+  // Wide token batches (the draft's 1024-token rounds) whose pair tiles fill >= 0.8
+  // of one wave (7B o / down projections: 64 pair tiles): pairs win under the
+  // power cap -- half the B-operand smem traffic per FLOP lifts the clock. In
+  // isolation the two plans tie; in the C2 loop pairs-wherever-legal measured
+  // 151.96 vs 153.46 ms over 7 alternating runs (profiles/r2/gemm_pair_ab.txt).
+  if (M >= 512 && tiles(pick_bn(M, cap)) * 5 >= 4 * (kNumSMs / 2)) return cap;
   if (M < 512 && cap >= 128 && tiles(pick_bn(M, 128)) * 2 >= 3 * (kNumSMs / 2)) return 128;
   return 0;
 }
