@@ -1277,6 +1277,37 @@ __global__ void __launch_bounds__(kUpdThreads, 1) tree_update_kernel(uint8_t* ws
       lex[pos] = r - ds_new[lo_depth(key)];
     }
     __syncthreads();
+  } else if (n_old == 0 && 2 * ((L.V + 31) / 32) <= L.kpad * 5 && g_sort_reg) {
+    // Root round: every selected node is a child of the root (depth 1, the same
+    // parent), so its lex rank is the rank of its token among the selected tokens:
+    // a V-bit token bitmap and a prefix popcount replace the sort (8192 keys:
+    // ~150 us of bitonic network -> a few us).
+    const int W = (L.V + 31) / 32;
+    unsigned* bits = reinterpret_cast<unsigned*>(sk_h);  // [W] (the sort buffers span 5 kpad words)
+    int* wrank = reinterpret_cast<int*>(bits + W);        // [W]: set bits in the words before
+    for (int w = tid; w < W; w += kUpdThreads) bits[w] = 0u;
+    __syncthreads();
+    for (int pos = tid; pos < sel; pos += kUpdThreads) {
+      const int tk = lo_token(lo_new[pos]);
+      atomicOr(&bits[tk >> 5], 1u << (tk & 31));
+    }
+    __syncthreads();
+    const int per_w = (W + kUpdThreads - 1) / kUpdThreads;
+    const int w0 = min(W, tid * per_w), w1 = min(W, w0 + per_w);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(bits[w]);
+    int wex;
+    block_excl_scan_fast(sm, cnt, wex);
+    for (int w = w0; w < w1; ++w) {
+      wrank[w] = wex;
+      wex += __popc(bits[w]);
+    }
+    __syncthreads();
+    for (int pos = tid; pos < sel; pos += kUpdThreads) {
+      const int tk = lo_token(lo_new[pos]);
+      lex[pos] = wrank[tk >> 5] + __popc(bits[tk >> 5] & ((1u << (tk & 31)) - 1u));
+    }
+    __syncthreads();
   } else {
     for (int pos = tid; pos < np2; pos += kUpdThreads) {
       sk_l[pos] = pos < sel ? lo_new[pos] : ~0ull;
